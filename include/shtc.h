@@ -1,0 +1,143 @@
+/*
+ * shtc.h — C ABI of the B200-native spherical harmonic transform (sm_100a, FP64).
+ *
+ * This is the drop-in boundary for the reference's accelerated path.
+ * Plain C types only: pointers, sizes, status codes.  Complex values are interleaved
+ * (re, im) float64 pairs.  a_lm use the reference AlmSet m-major triangle
+ * (offset(m) = m(lmax+1) - m(m-1)/2, alm.hpp:27-31); maps are ring-ordered pixels
+ * (alm.hpp:39-42); Delta panels are ring-major [ring][m] (alm.hpp:49-64).
+ *
+ * Reference interfaces each entry point replaces (file:line in /root/reference/proj):
+ *   shtc_alm2map / shtc_alm2map_dev   sht::synthesis              include/sht/transforms.hpp:73-74
+ *   shtc_map2alm / shtc_map2alm_dev   sht::analysis               include/sht/transforms.hpp:78-79
+ *   shtc_delta_a                      sht::compute_delta_a         include/sht/transforms.hpp:32-35
+ *                                     (and compute_delta_a_ring_major :40-43, same numbers)
+ *   shtc_accumulate_alm               sht::accumulate_alm /        include/sht/transforms.hpp:48-51
+ *                                     accumulate_alm_partial        include/sht/transforms.hpp:61-64
+ *   shtc_legendre_alm2map_dev         detail::delta_a_columns_paired  transforms.hpp:116-119
+ *   shtc_legendre_map2alm_dev         detail::accumulate_columns_paired transforms.hpp:121-124
+ *   shtc_ring_synthesis_dev           ring_synthesis_into (per ring)  include/sht/fourier.hpp:22-23
+ *   shtc_ring_analysis_dev            ring_analysis_into  (per ring)  include/sht/fourier.hpp:28-29
+ *   shtc_set_exchange_layout + the two stage calls above
+ *                                     distributed_synthesis / distributed_analysis stages
+ *                                     (distribution.cpp:300-490); the panel transpose
+ *                                     exchange_m_to_rings/rings_to_m (distribution.hpp:52-57)
+ *                                     becomes the caller's NCCL all-to-all on the packed
+ *                                     buffers these calls read and write.
+ *
+ * Error behaviour mirrors the reference: argument/layout violations -> SHTC_EINVAL
+ * (std::invalid_argument), beta_lm(l==m) style domain errors -> SHTC_EDOMAIN
+ * (std::domain_error); CUDA failures -> SHTC_ECUDA.  shtc_last_error() returns the message.
+ * There is no CPU fallback: without a usable sm_100 device every compute call fails.
+ */
+#ifndef SHTC_H
+#define SHTC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct shtc_ctx shtc_ctx;
+
+typedef enum {
+    SHTC_OK = 0,
+    SHTC_EINVAL = 1,       /* std::invalid_argument in the reference */
+    SHTC_EDOMAIN = 2,      /* std::domain_error in the reference */
+    SHTC_ECUDA = 3,        /* CUDA runtime / driver failure, no device */
+    SHTC_ENOMEM = 4,       /* device allocation failed */
+    SHTC_EUNSUPPORTED = 5  /* configuration outside what the kernels implement */
+} shtc_status;
+
+/* Per-call timing, CUDA events on the context stream (ms), plus side channels that the
+ * reference keeps in TransformOptions::step_counter / Profiler (perfmodel.hpp:63-84). */
+typedef struct {
+    double legendre_ms;     /* Legendre stage kernel time */
+    double fft_ms;          /* fold + ring FFT + unfold kernel time */
+    double h2d_ms;          /* host->device copies (host-buffer entry points only) */
+    double d2h_ms;          /* device->host copies (host-buffer entry points only) */
+    double total_ms;        /* whole call on the stream */
+    uint64_t nominal_steps; /* reference step count: sum over streams of lmax-m+1 */
+    uint64_t executed_steps;/* (l, m, stream) steps the kernels actually ran */
+} shtc_timing;
+
+/* ---- context ------------------------------------------------------------------------- */
+shtc_status shtc_create(int device, shtc_ctx** out);
+void shtc_destroy(shtc_ctx* ctx);
+const char* shtc_last_error(const shtc_ctx* ctx); /* ctx may be NULL (last global error) */
+int shtc_device_count(void);
+/* Use an external CUDA stream (cudaStream_t passed as void*; NULL = the context's own). */
+shtc_status shtc_set_stream(shtc_ctx* ctx, void* cuda_stream);
+
+/* ---- geometry and band (reference PixelGrid / AlmSet, grid.hpp:13-37, alm.hpp:16-35) --- */
+/* Copies the ring arrays.  mirror != 0 requests north/south stream pairing
+ * (PairPolicy::mirror, transforms.hpp:19-20); it is honoured only for grids that are
+ * mirror symmetric (symmetric_ring_pairs, grid.cpp:133-151), else rings run unpaired. */
+shtc_status shtc_set_grid(shtc_ctx* ctx, int n_rings, const double* cos_theta,
+                          const int32_t* n_phi, const double* phi_0, const double* weight,
+                          const int64_t* pixel_offset, int mirror);
+/* Band limits and the orders this context owns (NULL / n_m<=0 = all of 0..mmax).  The
+ * owned set is the worker's M_i of assign_m (distribution.cpp:82-99) for multi-GPU runs. */
+shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int32_t* ms);
+/* Builds (and caches) the Legendre plan (recurrence tables, underflow activation scan)
+ * and the ring-FFT plan; otherwise built lazily by the first transform. */
+shtc_status shtc_plan(shtc_ctx* ctx, double* plan_ms);
+/* Exact pair-step accounting of the plan: nominal, executed (after dead-tile skipping),
+ * useful (steps whose term the reference keeps, i.e. ladder scale k == 0). */
+shtc_status shtc_plan_stats(shtc_ctx* ctx, uint64_t* nominal, uint64_t* executed,
+                            uint64_t* useful);
+
+/* ---- whole transforms ---------------------------------------------------------------- */
+/* alm: 2*AlmSet::count(lmax,mmax) doubles; map: n_pix doubles.  Host buffers. */
+shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_timing* t);
+shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_timing* t);
+/* Same, device-resident buffers (no host copies). */
+shtc_status shtc_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* map_dev,
+                             shtc_timing* t);
+shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_dev,
+                             shtc_timing* t);
+
+/* ---- stages (multi-GPU building blocks; device buffers) ------------------------------ */
+/* Exchange layout of one worker (distributed_synthesis, distribution.cpp:300-380).
+ *   delta rows: the owned orders' panel is written ring-row by ring-row; row_off[r] is the
+ *     complex-element offset of ring r's row (n_cols = owned orders per row).  Grouping the
+ *     rows of each destination worker contiguously makes the Legendre output the NCCL send
+ *     buffer of exchange_m_to_rings without a pack kernel.
+ *   ring side: the rings this worker transforms (ring_list, ascending) and, per order m of
+ *     0..mmax, where Delta(ring_list[p], m) lives: m_base[m] + p * m_stride[m]
+ *     (complex elements) — the receive buffer of the all-to-all, unpacked in the fold.
+ * Passing NULL restores the single-GPU identity layout. */
+shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int n_ring_list,
+                                     const int32_t* ring_list, const int64_t* m_base,
+                                     const int64_t* m_stride);
+shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* delta_dev,
+                                      shtc_timing* t);
+shtc_status shtc_legendre_map2alm_dev(shtc_ctx* ctx, const double* delta_dev, double* alm_dev,
+                                      shtc_timing* t);
+shtc_status shtc_ring_synthesis_dev(shtc_ctx* ctx, const double* delta_dev, double* map_dev,
+                                    shtc_timing* t);
+shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double* delta_dev,
+                                   shtc_timing* t);
+
+/* ---- Legendre-stage operators (transforms.cpp:269-365), host buffers ------------------ */
+/* Delta^A_m(r) for the given latitudes and orders; delta: n_lat x n_m complex, ring-major.
+ * ms must be ascending and unique (the reference sorts, checked_m_set transforms.cpp:224). */
+shtc_status shtc_delta_a(shtc_ctx* ctx, const double* alm, int lmax, int mmax, int n_lat,
+                         const double* x, int n_m, const int32_t* ms, double* delta,
+                         uint64_t* steps);
+/* a_lm += sum_r Delta^S_m(r) P_lm(x_r) for the orders in ms (others untouched). */
+shtc_status shtc_accumulate_alm(shtc_ctx* ctx, const double* delta, int n_lat,
+                                const double* x, int n_m, const int32_t* ms, int lmax,
+                                int mmax, double* alm_inout, uint64_t* steps);
+
+/* ---- device helpers ------------------------------------------------------------------ */
+shtc_status shtc_device_info(int device, char* name, int name_len, int* sm_count,
+                             int* cc_major, int* cc_minor);
+/* Measured FP64 DFMA peak of the device (TFLOP/s), from a resident-loop kernel. */
+shtc_status shtc_measure_fp64_peak(int device, double* tflops, double* sm_clock_mhz);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SHTC_H */

@@ -1,0 +1,92 @@
+"""ctypes binding of libshtc.so (the C ABI declared in include/shtc.h).
+
+The library is built in-tree by `python -m paper_1106_0159_b200.build` (or
+`__graft_entry__.build()`).  Loading fails loudly if it is missing: there is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+PKG = Path(__file__).resolve().parent
+LIB_PATH = PKG / "libshtc.so"
+
+SHTC_OK, SHTC_EINVAL, SHTC_EDOMAIN, SHTC_ECUDA, SHTC_ENOMEM, SHTC_EUNSUPPORTED = range(6)
+
+# every symbol include/shtc.h declares (checked by the CPU test suite)
+EXPORTED = [
+    "shtc_create", "shtc_destroy", "shtc_last_error", "shtc_device_count", "shtc_set_stream",
+    "shtc_set_grid", "shtc_set_band", "shtc_plan", "shtc_plan_stats", "shtc_alm2map",
+    "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev", "shtc_set_exchange_layout",
+    "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev", "shtc_ring_synthesis_dev",
+    "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
+    "shtc_measure_fp64_peak",
+]
+
+
+class Timing(C.Structure):
+    _fields_ = [
+        ("legendre_ms", C.c_double), ("fft_ms", C.c_double), ("h2d_ms", C.c_double),
+        ("d2h_ms", C.c_double), ("total_ms", C.c_double), ("nominal_steps", C.c_uint64),
+        ("executed_steps", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+_LIB = None
+
+
+def lib():
+    global _LIB
+    if _LIB is None:
+        if not LIB_PATH.exists():
+            raise RuntimeError(
+                f"{LIB_PATH} is missing: build the CUDA extension first "
+                "(python -m paper_1106_0159_b200.build); there is no CPU fallback")
+        L = C.CDLL(str(LIB_PATH))
+        vp, i32, i64, dbl = C.c_void_p, C.c_int, C.c_int64, C.c_double
+        u64p = C.POINTER(C.c_uint64)
+        L.shtc_last_error.restype = C.c_char_p
+        L.shtc_last_error.argtypes = [vp]
+        L.shtc_create.argtypes = [i32, C.POINTER(vp)]
+        L.shtc_destroy.argtypes = [vp]
+        L.shtc_destroy.restype = None
+        L.shtc_device_count.restype = i32
+        L.shtc_set_stream.argtypes = [vp, vp]
+        L.shtc_set_grid.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32]
+        L.shtc_set_band.argtypes = [vp, i32, i32, i32, vp]
+        L.shtc_plan.argtypes = [vp, C.POINTER(dbl)]
+        L.shtc_plan_stats.argtypes = [vp, u64p, u64p, u64p]
+        for f in ("shtc_alm2map", "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev",
+                  "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev",
+                  "shtc_ring_synthesis_dev", "shtc_ring_analysis_dev"):
+            getattr(L, f).argtypes = [vp, vp, vp, C.POINTER(Timing)]
+        L.shtc_set_exchange_layout.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.shtc_delta_a.argtypes = [vp, vp, i32, i32, i32, vp, i32, vp, vp, u64p]
+        L.shtc_accumulate_alm.argtypes = [vp, vp, i32, vp, i32, vp, i32, i32, vp, u64p]
+        L.shtc_device_info.argtypes = [i32, C.c_char_p, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
+        L.shtc_measure_fp64_peak.argtypes = [i32, C.POINTER(dbl), C.POINTER(dbl)]
+        _LIB = L
+    return _LIB
+
+
+class ShtcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(msg)
+        self.code = code
+
+
+def check(rc: int, ctx=None):
+    if rc == SHTC_OK:
+        return
+    msg = lib().shtc_last_error(ctx).decode(errors="replace")
+    # error classes of the reference (std::invalid_argument / std::domain_error)
+    if rc == SHTC_EINVAL:
+        raise ValueError(msg)
+    if rc == SHTC_EDOMAIN:
+        raise ArithmeticError(msg)
+    if rc == SHTC_ENOMEM:
+        raise MemoryError(msg)
+    raise ShtcError(rc, msg)

@@ -1,0 +1,125 @@
+// Host-side launch interface of the sm_100a kernels (internal to libshtc).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace shtk {
+
+// ---------------------------------------------------------------------------------------
+// Legendre stage
+// ---------------------------------------------------------------------------------------
+
+// Streams of the recurrence: one per mirror pair (north, south) or per unpaired ring.
+struct LegStreams {
+    const double* x;       // cos(theta) of the north member
+    const double* log2s2;  // log2((1-x)(1+x)) computed on the host with glibc (parity)
+    const int* s2pos;      // (1-x)(1+x) > 0
+    const int* north;      // ring index of the north member
+    const int* south;      // ring index of the south member, -1 if unpaired
+    int n;
+};
+
+// Per-order recurrence tables for the renormalised recurrence
+//   Q_l = (A_l x) Q_{l-1} - Q_{l-2},   P_l = c_l Q_l,   activation threshold T_l = 2^512 / c_l
+// stored per order m contiguously for i = l - m = 0..lmax-m at tab_off[mi].
+struct LegTables {
+    double* A;
+    double* C;
+    double* T;
+    const int64_t* tab_off;
+};
+
+// Tile = TILE_STREAMS consecutive streams handled by one warp (32 lanes x R streams).
+constexpr int LEG_R = 4;
+constexpr int LEG_W = 8;  // warps per block
+constexpr int LEG_TILE = 32 * LEG_R;
+
+struct LegPlanView {
+    int lmax;
+    int n_m;
+    const int* ms;             // [n_m] ascending orders
+    const double* log_mu;      // [mmax+1] indexed by m (host glibc lgamma)
+    double exp_lmu0;           // exp(log_mu(0)) from the host (pmm_from_log m==0 path)
+    LegTables tab;
+    LegStreams st;
+    int n_tiles;               // ceil(st.n / LEG_TILE)
+    const int2* tile_info;     // [n_m * n_tiles]: (i_s, i_e) activation window, i_s < 0: dead
+    const int* tile_list;      // alive tiles, grouped per order
+    const int* tile_list_off;  // [n_m]
+    const int* tile_list_cnt;  // [n_m]
+    const int* m_order;        // block -> order index (cost descending)
+};
+
+void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s);
+// activation degree offset per (order, stream); INT_MAX = dead stream.
+void launch_leg_scan(const LegPlanView& p, int* act_dev, cudaStream_t s);
+// per (order, tile) activation window and useful-step totals.
+void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* tile_info_dev,
+                             unsigned long long* useful_dev, cudaStream_t s);
+
+// Delta rows: element (ring r, order index mi) at delta[row_off[r] + mi].
+void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
+                        const int64_t* row_off, cudaStream_t s);
+// a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.
+void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
+                        double2* alm, int accumulate, cudaStream_t s);
+
+// ---------------------------------------------------------------------------------------
+// Ring Fourier stage
+// ---------------------------------------------------------------------------------------
+constexpr int FFT_MAX_PASSES = 16;
+
+struct RingDesc {
+    int64_t pix_off;    // first pixel of the ring in the map
+    int64_t tw_off;     // e^{-2 pi i k / B}, k < B
+    int64_t hw_off;     // e^{-2 pi i k / n}, k <= N (half mode)
+    int64_t chirp_off;  // Bluestein chirp e^{-i pi (j^2 mod 2N)/N}, j < N
+    int64_t h_off;      // Bluestein FFT_B of conj(chirp) (cyclic), B entries
+    double phi0;
+    double weight;
+    int n;              // samples on the ring
+    int N;              // complex transform length (n/2 if n even, else n)
+    int B;              // buffer length (N if 7-smooth, else Bluestein power of two >= 2N-1)
+    int flags;          // bit0: half-length real trick, bit1: Bluestein
+    int ring_pos;       // row position of the ring in the Delta panel addressing
+    int npass;
+    unsigned char radix[FFT_MAX_PASSES];
+};
+
+struct RingStageArgs {
+    const RingDesc* rings;
+    int n_rings;
+    const double2* tabs;
+    int mmax;
+    const int64_t* m_base;    // Delta(ring_pos, m) at m_base[m] + ring_pos * m_stride[m]
+    const int64_t* m_stride;
+    const double2* delta_in;  // synthesis
+    double2* delta_out;       // analysis
+    const double* map_in;     // analysis
+    double* map_out;          // synthesis
+};
+
+// size classes: 0: B<=256 (64 thr), 1: B<=1024 (128), 2: B<=4096 (256), 3: B<=8192 (512)
+constexpr int FFT_N_CLASSES = 4;
+int fft_class_bmax(int c);
+int fft_class_for(int B);  // -1 if unsupported
+
+void launch_ring_synthesis(int cls, const RingStageArgs& a, cudaStream_t s);
+void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s);
+
+// Plan-time tables.
+struct TableJob {
+    int64_t off;
+    int L;     // length parameter
+    int kind;  // 0: e^{-2 pi i k/L}, k<L ; 1: e^{-2 pi i k/L}, k<=L/2 ; 2: chirp, k<L
+};
+void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cudaStream_t s);
+// For each Bluestein ring descriptor (deduplicated by N): tabs[h_off..] = FFT_B(h).
+void launch_bluestein_h(int cls, const RingDesc* descs_dev, int n, double2* tabs,
+                        cudaStream_t s);
+
+// FP64 peak probe.
+void launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);
+
+}  // namespace shtk

@@ -1,0 +1,1041 @@
+// libshtc: C ABI (include/shtc.h) over the sm_100a SHT kernels.
+//
+// Host-side responsibilities (all C++, no Python on the path):
+//   * geometry / band state, stream (ring-pair) construction   grid.cpp:133-151 semantics
+//   * log(mu_m) with glibc lgamma and per-stream log2(1-x^2)     legendre.cpp:16-20, 62-76
+//     (kept on the host so the seeds match the reference bit for bit)
+//   * Legendre plan: recurrence tables + activation scan + alive-tile lists ordered by cost
+//   * ring-FFT plan: per-ring descriptors, twiddle/chirp tables, size classes
+//   * validation with the reference's error classes (transforms.cpp:222-242, 338-345, 403-455)
+// There is no CPU fallback: every compute entry point needs the CUDA device.
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/shtc.h"
+#include "common.cuh"
+#include "kernels.h"
+
+using namespace shtk;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct ShtcError {
+    shtc_status code;
+    std::string msg;
+};
+
+[[noreturn]] void fail(shtc_status c, const std::string& m) { throw ShtcError{c, m}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        fail(e == cudaErrorMemoryAllocation ? SHTC_ENOMEM : SHTC_ECUDA,
+             std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) {
+            release();
+            p = o.p;
+            bytes = o.bytes;
+            o.p = nullptr;
+            o.bytes = 0;
+        }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes && p) return;
+        release();
+        if (b == 0) b = 16;
+        CK(cudaMalloc(&p, b));
+        bytes = b;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    void upload(const std::vector<T>& v, cudaStream_t s) {
+        ensure(v.size() * sizeof(T));
+        if (!v.empty()) CK(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+    }
+};
+
+constexpr double kLn2 = 0.69314718055994530942;
+constexpr double kLn4Pi = 2.5310242469692907930;  // legendre.cpp:9
+
+// log(mu_m), the reference expression verbatim (legendre.cpp:16-20).
+double host_log_mu(int m) {
+    return -m * kLn2 - std::lgamma(m + 1.0) + 0.5 * (std::lgamma(2.0 * m + 2.0) - kLn4Pi);
+}
+
+struct Stream {
+    double x;
+    int north, south;
+};
+
+struct LegPlan {
+    bool built = false;
+    int lmax = -1;
+    std::vector<int> ms;
+    std::vector<Stream> streams;
+    DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
+        tile_cnt, m_order;
+    LegPlanView view{};
+    uint64_t nominal = 0, executed = 0, useful = 0;
+    double build_ms = 0.0;
+};
+
+struct FftPlan {
+    bool built = false;
+    DevBuf descs[FFT_N_CLASSES];
+    int count[FFT_N_CLASSES] = {0, 0, 0, 0};
+    DevBuf tabs;
+    double build_ms = 0.0;
+};
+
+}  // namespace
+
+struct shtc_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaStream_t own_stream = nullptr;
+    std::string err;
+    // grid
+    int n_rings = 0;
+    std::vector<double> cos_theta, phi0, weight;
+    std::vector<int> nphi;
+    std::vector<int64_t> pixoff;
+    int64_t npix = 0;
+    bool symmetric = false, mirror = true, grid_set = false;
+    // band
+    int lmax = -1, mmax = -1;
+    std::vector<int> ms;
+    bool band_set = false;
+    std::vector<double> log_mu;
+    // exchange layout (stage API)
+    bool custom_layout = false;
+    std::vector<int64_t> row_off;
+    std::vector<int> ring_list;
+    std::vector<int64_t> m_base, m_stride;
+    DevBuf row_off_d, m_base_d, m_stride_d;
+    // identity layout for whole transforms
+    DevBuf id_row_off, id_m_base, id_m_stride;
+    // plans
+    LegPlan leg;
+    FftPlan fft_id;      // identity ring list
+    FftPlan fft_custom;  // custom ring list
+    // operator-API plan cache
+    LegPlan op_leg;
+    std::vector<double> op_x;
+    // scratch
+    DevBuf delta, alm_buf, map_buf, stats;
+    cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+bool is_smooth7(int n) {
+    for (int p : {2, 3, 5, 7})
+        while (n % p == 0) n /= p;
+    return n == 1;
+}
+
+std::vector<int> radix_plan(int B) {
+    std::vector<int> r;
+    int n = B;
+    while (n % 8 == 0) { r.push_back(8); n /= 8; }
+    while (n % 4 == 0) { r.push_back(4); n /= 4; }
+    while (n % 2 == 0) { r.push_back(2); n /= 2; }
+    for (int p : {3, 5, 7})
+        while (n % p == 0) { r.push_back(p); n /= p; }
+    if (n != 1) fail(SHTC_EUNSUPPORTED, "radix plan: length not 7-smooth");
+    return r;
+}
+
+int next_pow2(int v) {
+    int p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+void set_err(shtc_ctx* c, const std::string& m) {
+    g_last_error = m;
+    if (c) c->err = m;
+}
+
+template <class F>
+shtc_status guarded(shtc_ctx* c, F&& f) {
+    try {
+        if (c) CK(cudaSetDevice(c->device));
+        f();
+        return SHTC_OK;
+    } catch (const ShtcError& e) {
+        set_err(c, e.msg);
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        set_err(c, "host allocation failed");
+        return SHTC_ENOMEM;
+    } catch (const std::exception& e) {
+        set_err(c, e.what());
+        return SHTC_ECUDA;
+    }
+}
+
+void check_latitudes(const double* x, int n, const char* where) {
+    for (int i = 0; i < n; ++i)
+        if (!(std::fabs(x[i]) <= 1.0))
+            fail(SHTC_EINVAL, std::string(where) + ": cos_theta outside [-1, 1]");
+}
+
+void check_m_set(const int32_t* ms, int n, int mmax, const char* where) {
+    for (int i = 0; i < n; ++i) {
+        if (ms[i] < 0 || ms[i] > mmax) fail(SHTC_EINVAL, std::string(where) + ": order outside [0, mmax]");
+        if (i > 0 && ms[i] <= ms[i - 1])
+            fail(SHTC_EINVAL, std::string(where) + ": orders must be ascending and unique");
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Legendre plan
+// ---------------------------------------------------------------------------------------
+void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vector<int>& ms,
+                    std::vector<Stream> streams, const std::vector<double>& log_mu) {
+    cudaStream_t s = c->stream;
+    cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
+    CK(cudaEventRecord(e0, s));
+    P = LegPlan();  // release previous
+    P.lmax = lmax;
+    P.ms = ms;
+    // latitude-coherent tiles: streams ordered by |x| descending (polar first)
+    std::stable_sort(streams.begin(), streams.end(),
+                     [](const Stream& a, const Stream& b) { return std::fabs(a.x) > std::fabs(b.x); });
+    P.streams = streams;
+    const int ns = (int)streams.size();
+    const int n_m = (int)ms.size();
+    std::vector<double> sx(ns), sl2(ns);
+    std::vector<int> spos(ns), sno(ns), sso(ns);
+    for (int i = 0; i < ns; ++i) {
+        const double x = streams[i].x;
+        const double s2 = (1.0 - x) * (1.0 + x);  // legendre.cpp:67
+        sx[i] = x;
+        spos[i] = s2 > 0.0;
+        sl2[i] = s2 > 0.0 ? std::log2(s2) : 0.0;
+        sno[i] = streams[i].north;
+        sso[i] = streams[i].south;
+    }
+    std::vector<int64_t> toff(n_m);
+    int64_t tot = 0;
+    for (int i = 0; i < n_m; ++i) {
+        toff[i] = tot;
+        tot += lmax - ms[i] + 1;
+    }
+    P.ms_d.upload(ms, s);
+    P.logmu_d.upload(log_mu, s);
+    P.sx.upload(sx, s);
+    P.sl2.upload(sl2, s);
+    P.spos.upload(spos, s);
+    P.sn.upload(sno, s);
+    P.ss.upload(sso, s);
+    P.tab_off.upload(toff, s);
+    P.A.ensure(tot * sizeof(double));
+    P.C.ensure(tot * sizeof(double));
+    P.T.ensure(tot * sizeof(double));
+
+    LegPlanView& v = P.view;
+    v.lmax = lmax;
+    v.n_m = n_m;
+    v.ms = P.ms_d.as<int>();
+    v.log_mu = P.logmu_d.as<double>();
+    v.exp_lmu0 = std::exp(log_mu[0]);  // pmm_from_log m == 0 (legendre.cpp:65)
+    v.tab = LegTables{P.A.as<double>(), P.C.as<double>(), P.T.as<double>(), P.tab_off.as<int64_t>()};
+    v.st = LegStreams{P.sx.as<double>(), P.sl2.as<double>(), P.spos.as<int>(), P.sn.as<int>(),
+                      P.ss.as<int>(), ns};
+    v.n_tiles = (ns + LEG_TILE - 1) / LEG_TILE;
+
+    if (n_m > 0) launch_leg_tables(v.ms, n_m, lmax, v.tab, s);
+    CK(cudaGetLastError());
+
+    DevBuf act;
+    act.ensure((size_t)n_m * ns * sizeof(int));
+    P.tile_info.ensure((size_t)n_m * v.n_tiles * sizeof(int2));
+    c->stats.ensure(sizeof(unsigned long long));
+    CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long), s));
+    v.tile_info = P.tile_info.as<int2>();
+    if (n_m > 0) {
+        launch_leg_scan(v, act.as<int>(), s);
+        CK(cudaGetLastError());
+        launch_leg_tile_summary(v, act.as<int>(), P.tile_info.as<int2>(),
+                                c->stats.as<unsigned long long>(), s);
+        CK(cudaGetLastError());
+    }
+    std::vector<int2> info((size_t)n_m * v.n_tiles);
+    unsigned long long useful = 0;
+    if (!info.empty())
+        CK(cudaMemcpyAsync(info.data(), P.tile_info.p, info.size() * sizeof(int2), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&useful, c->stats.p, sizeof(useful), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    P.useful = useful;
+
+    // alive tile lists per order, orders by cost (descending) for the block schedule
+    std::vector<int> tl, toffs(n_m), tcnt(n_m);
+    std::vector<double> cost(n_m);
+    P.nominal = 0;
+    P.executed = 0;
+    for (int i = 0; i < n_m; ++i) {
+        const int n = lmax - ms[i];
+        P.nominal += (uint64_t)(n + 1) * ns;
+        toffs[i] = (int)tl.size();
+        for (int t = 0; t < v.n_tiles; ++t) {
+            if (info[(size_t)i * v.n_tiles + t].x < 0) continue;
+            tl.push_back(t);
+            const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
+            P.executed += (uint64_t)(n + 1) * in_tile;
+        }
+        tcnt[i] = (int)tl.size() - toffs[i];
+        cost[i] = (double)(n + 1) * std::ceil(tcnt[i] / (double)LEG_W);
+    }
+    std::vector<int> order(n_m);
+    std::iota(order.begin(), order.end(), 0);
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    if (tl.empty()) tl.push_back(0);
+    P.tile_list.upload(tl, s);
+    P.tile_off.upload(toffs, s);
+    P.tile_cnt.upload(tcnt, s);
+    P.m_order.upload(order, s);
+    v.tile_list = P.tile_list.as<int>();
+    v.tile_list_off = P.tile_off.as<int>();
+    v.tile_list_cnt = P.tile_cnt.as<int>();
+    v.m_order = P.m_order.as<int>();
+    CK(cudaEventRecord(e1, s));
+    CK(cudaStreamSynchronize(s));
+    float ms_el = 0.f;
+    CK(cudaEventElapsedTime(&ms_el, e0, e1));
+    P.build_ms = ms_el;
+    P.built = true;
+}
+
+std::vector<Stream> grid_streams(const shtc_ctx* c) {
+    std::vector<Stream> st;
+    const int n = c->n_rings;
+    if (c->mirror && c->symmetric) {
+        for (int k = 0; k < n / 2; ++k) st.push_back({c->cos_theta[k], k, n - 1 - k});
+        if (n % 2 == 1) st.push_back({c->cos_theta[n / 2], n / 2, -1});
+    } else {
+        for (int r = 0; r < n; ++r) st.push_back({c->cos_theta[r], r, -1});
+    }
+    return st;
+}
+
+void ensure_leg_plan(shtc_ctx* c) {
+    if (!c->grid_set) fail(SHTC_EINVAL, "no grid set");
+    if (!c->band_set) fail(SHTC_EINVAL, "no band set");
+    if (!c->leg.built) build_leg_plan(c, c->leg, c->lmax, c->mmax, c->ms, grid_streams(c), c->log_mu);
+}
+
+// ---------------------------------------------------------------------------------------
+// Ring FFT plan
+// ---------------------------------------------------------------------------------------
+void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
+    cudaStream_t s = c->stream;
+    cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
+    CK(cudaEventRecord(e0, s));
+    for (auto& d : F.descs) d.release();
+    F.tabs.release();
+    std::vector<TableJob> jobs;
+    int64_t tot = 0;
+    std::map<std::pair<int, int>, int64_t> table_at;  // (kind, L) -> offset
+    auto table = [&](int kind, int L) {
+        auto key = std::make_pair(kind, L);
+        auto it = table_at.find(key);
+        if (it != table_at.end()) return it->second;
+        const int64_t off = tot;
+        tot += (kind == 1) ? L / 2 + 1 : L;
+        jobs.push_back(TableJob{off, L, kind});
+        table_at[key] = off;
+        return off;
+    };
+    std::map<int, int64_t> h_at;  // Bluestein N -> H offset
+    std::vector<RingDesc> per_class[FFT_N_CLASSES];
+    std::vector<RingDesc> blue_class[FFT_N_CLASSES];
+    for (size_t pos = 0; pos < rings.size(); ++pos) {
+        const int r = rings[pos];
+        RingDesc d{};
+        d.n = c->nphi[r];
+        if (d.n < 1) fail(SHTC_EINVAL, "ring_synthesis: ring has no samples");
+        const bool half = (d.n % 2 == 0);
+        d.N = half ? d.n / 2 : d.n;
+        const bool smooth = is_smooth7(d.N);
+        d.B = smooth ? d.N : next_pow2(2 * d.N - 1);
+        d.flags = (half ? 1 : 0) | (smooth ? 0 : 2);
+        d.pix_off = c->pixoff[r];
+        d.phi0 = c->phi0[r];
+        d.weight = c->weight[r];
+        d.ring_pos = (int)pos;
+        const int cls = fft_class_for(d.B);
+        if (cls < 0)
+            fail(SHTC_EUNSUPPORTED, "ring length " + std::to_string(d.n) +
+                                        " needs an FFT buffer beyond the shared-memory classes");
+        auto rp = radix_plan(d.B);
+        d.npass = (int)rp.size();
+        for (size_t i = 0; i < rp.size(); ++i) d.radix[i] = (unsigned char)rp[i];
+        d.tw_off = table(0, d.B);
+        d.hw_off = half ? table(1, d.n) : 0;
+        if (!smooth) {
+            d.chirp_off = table(2, d.N);
+            auto it = h_at.find(d.N);
+            if (it == h_at.end()) {
+                d.h_off = tot;
+                tot += d.B;
+                h_at[d.N] = d.h_off;
+                blue_class[cls].push_back(d);
+            } else {
+                d.h_off = it->second;
+            }
+        }
+        per_class[cls].push_back(d);
+    }
+    F.tabs.ensure((size_t)std::max<int64_t>(tot, 1) * sizeof(double2));
+    DevBuf jobs_d;
+    jobs_d.upload(jobs, s);
+    launch_fill_tables(jobs_d.as<TableJob>(), (int)jobs.size(), F.tabs.as<double2>(), s);
+    CK(cudaGetLastError());
+    for (int k = 0; k < FFT_N_CLASSES; ++k) {
+        if (!blue_class[k].empty()) {
+            DevBuf bd;
+            bd.upload(blue_class[k], s);
+            launch_bluestein_h(k, bd.as<RingDesc>(), (int)blue_class[k].size(), F.tabs.as<double2>(), s);
+            CK(cudaGetLastError());
+            CK(cudaStreamSynchronize(s));
+        }
+        F.descs[k].upload(per_class[k], s);
+        F.count[k] = (int)per_class[k].size();
+    }
+    CK(cudaEventRecord(e1, s));
+    CK(cudaStreamSynchronize(s));
+    float el = 0.f;
+    CK(cudaEventElapsedTime(&el, e0, e1));
+    F.build_ms = el;
+    F.built = true;
+}
+
+void ensure_id_layout(shtc_ctx* c) {
+    if (c->id_row_off.p) return;
+    const int nm = (int)c->ms.size();
+    std::vector<int64_t> ro(c->n_rings), mb(c->mmax + 1), mst(c->mmax + 1);
+    for (int r = 0; r < c->n_rings; ++r) ro[r] = (int64_t)r * nm;
+    for (int m = 0; m <= c->mmax; ++m) {
+        mb[m] = m;
+        mst[m] = c->mmax + 1;
+    }
+    c->id_row_off.upload(ro, c->stream);
+    c->id_m_base.upload(mb, c->stream);
+    c->id_m_stride.upload(mst, c->stream);
+}
+
+void ensure_fft_id(shtc_ctx* c) {
+    if (!c->grid_set) fail(SHTC_EINVAL, "no grid set");
+    if (!c->fft_id.built) {
+        std::vector<int> all(c->n_rings);
+        std::iota(all.begin(), all.end(), 0);
+        build_fft_plan(c, c->fft_id, all);
+    }
+}
+
+void require_full_band(shtc_ctx* c) {
+    if (!c->band_set) fail(SHTC_EINVAL, "no band set");
+    if ((int)c->ms.size() != c->mmax + 1)
+        fail(SHTC_EINVAL, "whole transforms need every order 0..mmax on this context");
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
+                    const int64_t* mb, const int64_t* mst) {
+    for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
+        RingStageArgs a{};
+        a.rings = F.descs[k].as<RingDesc>();
+        a.n_rings = F.count[k];
+        a.tabs = F.tabs.as<double2>();
+        a.mmax = c->mmax;
+        a.m_base = mb;
+        a.m_stride = mst;
+        a.delta_in = delta;
+        a.map_out = map;
+        launch_ring_synthesis(k, a, c->stream);
+        CK(cudaGetLastError());
+    }
+}
+
+void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
+                   const int64_t* mst) {
+    for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
+        RingStageArgs a{};
+        a.rings = F.descs[k].as<RingDesc>();
+        a.n_rings = F.count[k];
+        a.tabs = F.tabs.as<double2>();
+        a.mmax = c->mmax;
+        a.m_base = mb;
+        a.m_stride = mst;
+        a.map_in = map;
+        a.delta_out = delta;
+        launch_ring_analysis(k, a, c->stream);
+        CK(cudaGetLastError());
+    }
+}
+
+void fill_timing(shtc_timing* t, double leg, double fft, double h2d, double d2h, double total,
+                 const LegPlan& P) {
+    if (!t) return;
+    t->legendre_ms = leg;
+    t->fft_ms = fft;
+    t->h2d_ms = h2d;
+    t->d2h_ms = d2h;
+    t->total_ms = total;
+    t->nominal_steps = P.nominal;
+    t->executed_steps = P.executed;
+}
+
+void do_alm2map_dev(shtc_ctx* c, const double* alm, double* map, shtc_timing* t, double h2d = 0) {
+    require_full_band(c);
+    ensure_leg_plan(c);
+    ensure_fft_id(c);
+    ensure_id_layout(c);
+    c->delta.ensure((size_t)c->n_rings * (c->mmax + 1) * sizeof(double2));
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(c->ev[0], s));
+    launch_leg_alm2map(c->leg.view, reinterpret_cast<const double2*>(alm), c->delta.as<double2>(),
+                       c->id_row_off.as<int64_t>(), s);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[1], s));
+    run_ring_synth(c, c->fft_id, c->delta.as<double2>(), map, c->id_m_base.as<int64_t>(),
+                   c->id_m_stride.as<int64_t>());
+    CK(cudaEventRecord(c->ev[2], s));
+    if (t) {
+        CK(cudaEventSynchronize(c->ev[2]));
+        const double leg = elapsed(c->ev[0], c->ev[1]), fft = elapsed(c->ev[1], c->ev[2]);
+        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg);
+    }
+}
+
+void do_map2alm_dev(shtc_ctx* c, const double* map, double* alm, shtc_timing* t, double h2d = 0) {
+    require_full_band(c);
+    ensure_leg_plan(c);
+    ensure_fft_id(c);
+    ensure_id_layout(c);
+    c->delta.ensure((size_t)c->n_rings * (c->mmax + 1) * sizeof(double2));
+    cudaStream_t s = c->stream;
+    CK(cudaEventRecord(c->ev[0], s));
+    run_ring_anal(c, c->fft_id, map, c->delta.as<double2>(), c->id_m_base.as<int64_t>(),
+                  c->id_m_stride.as<int64_t>());
+    CK(cudaEventRecord(c->ev[1], s));
+    launch_leg_map2alm(c->leg.view, c->delta.as<double2>(), c->id_row_off.as<int64_t>(),
+                       reinterpret_cast<double2*>(alm), 0, s);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev[2], s));
+    if (t) {
+        CK(cudaEventSynchronize(c->ev[2]));
+        const double fft = elapsed(c->ev[0], c->ev[1]), leg = elapsed(c->ev[1], c->ev[2]);
+        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg);
+    }
+}
+
+size_t alm_count(int lmax, int mmax) {
+    const size_t l = lmax, m = mmax;
+    return (m + 1) * (l + 1) - m * (m + 1) / 2;
+}
+
+}  // namespace
+
+// =========================================================================================
+// C ABI
+// =========================================================================================
+extern "C" {
+
+const char* shtc_last_error(const shtc_ctx* ctx) {
+    return ctx ? ctx->err.c_str() : g_last_error.c_str();
+}
+
+int shtc_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+shtc_status shtc_create(int device, shtc_ctx** out) {
+    if (!out) return SHTC_EINVAL;
+    *out = nullptr;
+    return guarded(nullptr, [&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (device < 0 || device >= n) fail(SHTC_EINVAL, "shtc_create: no such CUDA device");
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            fail(SHTC_EUNSUPPORTED, std::string("shtc_create: kernels are built for sm_100a, device is ") +
+                                        prop.name);
+        CK(cudaSetDevice(device));
+        auto c = std::make_unique<shtc_ctx>();
+        c->device = device;
+        CK(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+        c->stream = c->own_stream;
+        for (auto& e : c->ev) CK(cudaEventCreate(&e));
+        *out = c.release();
+    });
+}
+
+void shtc_destroy(shtc_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->stream);
+    for (auto& e : ctx->ev)
+        if (e) cudaEventDestroy(e);
+    if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
+    delete ctx;
+}
+
+shtc_status shtc_set_stream(shtc_ctx* ctx, void* cuda_stream) {
+    if (!ctx) return SHTC_EINVAL;
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own_stream;
+    return SHTC_OK;
+}
+
+shtc_status shtc_set_grid(shtc_ctx* ctx, int n_rings, const double* cos_theta, const int32_t* n_phi,
+                          const double* phi_0, const double* weight, const int64_t* pixel_offset,
+                          int mirror) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (n_rings < 1 || !cos_theta || !n_phi || !phi_0 || !weight)
+            fail(SHTC_EINVAL, "synthesis: empty grid");
+        check_latitudes(cos_theta, n_rings, "synthesis");
+        ctx->n_rings = n_rings;
+        ctx->cos_theta.assign(cos_theta, cos_theta + n_rings);
+        ctx->nphi.assign(n_phi, n_phi + n_rings);
+        ctx->phi0.assign(phi_0, phi_0 + n_rings);
+        ctx->weight.assign(weight, weight + n_rings);
+        ctx->pixoff.resize(n_rings);
+        int64_t off = 0;
+        for (int r = 0; r < n_rings; ++r) {
+            if (n_phi[r] < 1) fail(SHTC_EINVAL, "ring_synthesis: ring has no samples");
+            ctx->pixoff[r] = pixel_offset ? pixel_offset[r] : off;
+            off += n_phi[r];
+        }
+        ctx->npix = off;
+        // symmetric_ring_pairs (grid.cpp:133-151)
+        bool sym = true;
+        for (int k = 0; k < n_rings / 2; ++k) {
+            const int j = n_rings - 1 - k;
+            if (n_phi[k] != n_phi[j] || std::fabs(cos_theta[k] + cos_theta[j]) > 1e-14) sym = false;
+        }
+        if (n_rings % 2 == 1 && std::fabs(cos_theta[n_rings / 2]) > 1e-14) sym = false;
+        ctx->symmetric = sym;
+        ctx->mirror = mirror != 0;
+        ctx->grid_set = true;
+        ctx->leg.built = false;
+        ctx->fft_id.built = false;
+        ctx->fft_custom.built = false;
+        ctx->id_row_off.release();
+        ctx->custom_layout = false;
+    });
+}
+
+shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int32_t* ms) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (lmax < mmax || mmax < 0) fail(SHTC_EINVAL, "analysis: need lmax >= mmax >= 0");
+        std::vector<int> v;
+        if (ms && n_m > 0) {
+            check_m_set(ms, n_m, mmax, "shtc_set_band");
+            v.assign(ms, ms + n_m);
+        } else {
+            v.resize(mmax + 1);
+            std::iota(v.begin(), v.end(), 0);
+        }
+        ctx->lmax = lmax;
+        ctx->mmax = mmax;
+        ctx->ms = v;
+        ctx->log_mu.resize(mmax + 1);
+        for (int m = 0; m <= mmax; ++m) ctx->log_mu[m] = host_log_mu(m);
+        ctx->band_set = true;
+        ctx->leg.built = false;
+        ctx->id_row_off.release();
+        ctx->custom_layout = false;
+    });
+}
+
+shtc_status shtc_plan(shtc_ctx* ctx, double* plan_ms) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        ensure_fft_id(ctx);
+        if (plan_ms) *plan_ms = ctx->leg.build_ms + ctx->fft_id.build_ms;
+    });
+}
+
+shtc_status shtc_plan_stats(shtc_ctx* ctx, uint64_t* nominal, uint64_t* executed, uint64_t* useful) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        if (nominal) *nominal = ctx->leg.nominal;
+        if (executed) *executed = ctx->leg.executed;
+        if (useful) *useful = ctx->leg.useful;
+    });
+}
+
+shtc_status shtc_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* map_dev, shtc_timing* t) {
+    if (!ctx || !alm_dev || !map_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] { do_alm2map_dev(ctx, alm_dev, map_dev, t); });
+}
+
+shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_dev, shtc_timing* t) {
+    if (!ctx || !map_dev || !alm_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] { do_map2alm_dev(ctx, map_dev, alm_dev, t); });
+}
+
+shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_timing* t) {
+    if (!ctx || !alm || !map) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        require_full_band(ctx);
+        if (!ctx->grid_set) fail(SHTC_EINVAL, "no grid set");
+        const size_t na = alm_count(ctx->lmax, ctx->mmax) * sizeof(double2);
+        const size_t nb = (size_t)ctx->npix * sizeof(double);
+        ctx->alm_buf.ensure(na);
+        ctx->map_buf.ensure(nb);
+        cudaStream_t s = ctx->stream;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        CK(cudaMemcpyAsync(ctx->alm_buf.p, alm, na, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ctx->ev[4], s));
+        shtc_timing tt{};
+        do_alm2map_dev(ctx, ctx->alm_buf.as<double>(), ctx->map_buf.as<double>(), &tt);
+        CK(cudaEventRecord(ctx->ev[5], s));
+        CK(cudaMemcpyAsync(map, ctx->map_buf.p, nb, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ctx->ev[6], s));
+        CK(cudaEventSynchronize(ctx->ev[6]));
+        if (t) {
+            *t = tt;
+            t->h2d_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+            t->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+            t->total_ms = elapsed(ctx->ev[3], ctx->ev[6]);
+        }
+    });
+}
+
+shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_timing* t) {
+    if (!ctx || !alm || !map) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        require_full_band(ctx);
+        if (!ctx->grid_set) fail(SHTC_EINVAL, "no grid set");
+        const size_t na = alm_count(ctx->lmax, ctx->mmax) * sizeof(double2);
+        const size_t nb = (size_t)ctx->npix * sizeof(double);
+        ctx->alm_buf.ensure(na);
+        ctx->map_buf.ensure(nb);
+        cudaStream_t s = ctx->stream;
+        CK(cudaEventRecord(ctx->ev[3], s));
+        CK(cudaMemcpyAsync(ctx->map_buf.p, map, nb, cudaMemcpyHostToDevice, s));
+        CK(cudaEventRecord(ctx->ev[4], s));
+        shtc_timing tt{};
+        do_map2alm_dev(ctx, ctx->map_buf.as<double>(), ctx->alm_buf.as<double>(), &tt);
+        CK(cudaEventRecord(ctx->ev[5], s));
+        CK(cudaMemcpyAsync(alm, ctx->alm_buf.p, na, cudaMemcpyDeviceToHost, s));
+        CK(cudaEventRecord(ctx->ev[6], s));
+        CK(cudaEventSynchronize(ctx->ev[6]));
+        if (t) {
+            *t = tt;
+            t->h2d_ms = elapsed(ctx->ev[3], ctx->ev[4]);
+            t->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
+            t->total_ms = elapsed(ctx->ev[3], ctx->ev[6]);
+        }
+    });
+}
+
+// ---- stage API -------------------------------------------------------------------------
+shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int n_ring_list,
+                                     const int32_t* ring_list, const int64_t* m_base,
+                                     const int64_t* m_stride) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->grid_set || !ctx->band_set) fail(SHTC_EINVAL, "set grid and band first");
+        if (!row_off) {
+            ctx->custom_layout = false;
+            return;
+        }
+        if (n_ring_list < 0 || (n_ring_list > 0 && (!ring_list || !m_base || !m_stride)))
+            fail(SHTC_EINVAL, "exchange layout: malformed");
+        ctx->row_off.assign(row_off, row_off + ctx->n_rings);
+        ctx->ring_list.assign(ring_list, ring_list + n_ring_list);
+        for (int i = 0; i < n_ring_list; ++i) {
+            if (ring_list[i] < 0 || ring_list[i] >= ctx->n_rings)
+                fail(SHTC_EINVAL, "exchange: invalid ring layout");
+            if (i > 0 && ring_list[i] <= ring_list[i - 1])
+                fail(SHTC_EINVAL, "exchange: ring list must be ascending");
+        }
+        ctx->m_base.assign(m_base, m_base + ctx->mmax + 1);
+        ctx->m_stride.assign(m_stride, m_stride + ctx->mmax + 1);
+        ctx->row_off_d.upload(ctx->row_off, ctx->stream);
+        ctx->m_base_d.upload(ctx->m_base, ctx->stream);
+        ctx->m_stride_d.upload(ctx->m_stride, ctx->stream);
+        build_fft_plan(ctx, ctx->fft_custom, ctx->ring_list);
+        ctx->custom_layout = true;
+    });
+}
+
+namespace {
+const int64_t* stage_row_off(shtc_ctx* c) {
+    if (c->custom_layout) return c->row_off_d.as<int64_t>();
+    ensure_id_layout(c);
+    return c->id_row_off.as<int64_t>();
+}
+}  // namespace
+
+shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* delta_dev,
+                                      shtc_timing* t) {
+    if (!ctx || !alm_dev || !delta_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        const int64_t* ro = stage_row_off(ctx);
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        launch_leg_alm2map(ctx->leg.view, reinterpret_cast<const double2*>(alm_dev),
+                           reinterpret_cast<double2*>(delta_dev), ro, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+        }
+    });
+}
+
+shtc_status shtc_legendre_map2alm_dev(shtc_ctx* ctx, const double* delta_dev, double* alm_dev,
+                                      shtc_timing* t) {
+    if (!ctx || !alm_dev || !delta_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        const int64_t* ro = stage_row_off(ctx);
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        launch_leg_map2alm(ctx->leg.view, reinterpret_cast<const double2*>(delta_dev), ro,
+                           reinterpret_cast<double2*>(alm_dev), 0, ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+        }
+    });
+}
+
+shtc_status shtc_ring_synthesis_dev(shtc_ctx* ctx, const double* delta_dev, double* map_dev,
+                                    shtc_timing* t) {
+    if (!ctx || !delta_dev || !map_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        FftPlan* F;
+        const int64_t *mb, *mst;
+        if (ctx->custom_layout) {
+            F = &ctx->fft_custom;
+            mb = ctx->m_base_d.as<int64_t>();
+            mst = ctx->m_stride_d.as<int64_t>();
+        } else {
+            require_full_band(ctx);
+            ensure_fft_id(ctx);
+            ensure_id_layout(ctx);
+            F = &ctx->fft_id;
+            mb = ctx->id_m_base.as<int64_t>();
+            mst = ctx->id_m_stride.as<int64_t>();
+        }
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_ring_synth(ctx, *F, reinterpret_cast<const double2*>(delta_dev), map_dev, mb, mst);
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            *t = shtc_timing{};
+            t->fft_ms = t->total_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+        }
+    });
+}
+
+shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double* delta_dev,
+                                   shtc_timing* t) {
+    if (!ctx || !delta_dev || !map_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        FftPlan* F;
+        const int64_t *mb, *mst;
+        if (ctx->custom_layout) {
+            F = &ctx->fft_custom;
+            mb = ctx->m_base_d.as<int64_t>();
+            mst = ctx->m_stride_d.as<int64_t>();
+        } else {
+            require_full_band(ctx);
+            ensure_fft_id(ctx);
+            ensure_id_layout(ctx);
+            F = &ctx->fft_id;
+            mb = ctx->id_m_base.as<int64_t>();
+            mst = ctx->id_m_stride.as<int64_t>();
+        }
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_ring_anal(ctx, *F, map_dev, reinterpret_cast<double2*>(delta_dev), mb, mst);
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            *t = shtc_timing{};
+            t->fft_ms = t->total_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+        }
+    });
+}
+
+// ---- Legendre-stage operators ---------------------------------------------------------
+namespace {
+void op_plan(shtc_ctx* c, int lmax, int mmax, int n_lat, const double* x, int n_m, const int32_t* ms) {
+    std::vector<int> mv(ms, ms + n_m);
+    std::vector<double> xv(x, x + n_lat);
+    if (c->op_leg.built && c->op_leg.lmax == lmax && c->op_leg.ms == mv && c->op_x == xv &&
+        (int)c->log_mu.size() >= mmax + 1)
+        return;
+    std::vector<double> lmu(mmax + 1);
+    for (int m = 0; m <= mmax; ++m) lmu[m] = host_log_mu(m);
+    std::vector<Stream> st(n_lat);
+    for (int r = 0; r < n_lat; ++r) st[r] = {x[r], r, -1};
+    build_leg_plan(c, c->op_leg, lmax, mmax, mv, st, lmu);
+    c->op_x = xv;
+}
+}  // namespace
+
+shtc_status shtc_delta_a(shtc_ctx* ctx, const double* alm, int lmax, int mmax, int n_lat,
+                         const double* x, int n_m, const int32_t* ms, double* delta, uint64_t* steps) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (lmax < mmax || mmax < 0) fail(SHTC_EINVAL, "AlmSet: need lmax >= mmax >= 0");
+        if (n_lat < 0 || n_m < 0) fail(SHTC_EINVAL, "compute_delta_a: negative sizes");
+        check_m_set(ms, n_m, mmax, "compute_delta_a");
+        check_latitudes(x, n_lat, "compute_delta_a");
+        uint64_t nominal = 0;
+        for (int i = 0; i < n_m; ++i) nominal += (uint64_t)(lmax - ms[i] + 1) * n_lat;
+        if (steps) *steps += nominal;
+        if (n_lat == 0 || n_m == 0) return;
+        op_plan(ctx, lmax, mmax, n_lat, x, n_m, ms);
+        cudaStream_t s = ctx->stream;
+        const size_t na = alm_count(lmax, mmax) * sizeof(double2);
+        const size_t nd = (size_t)n_lat * n_m * sizeof(double2);
+        DevBuf a, d, ro;
+        a.ensure(na);
+        d.ensure(nd);
+        std::vector<int64_t> rov(n_lat);
+        for (int r = 0; r < n_lat; ++r) rov[r] = (int64_t)r * n_m;
+        ro.upload(rov, s);
+        CK(cudaMemcpyAsync(a.p, alm, na, cudaMemcpyHostToDevice, s));
+        launch_leg_alm2map(ctx->op_leg.view, a.as<double2>(), d.as<double2>(), ro.as<int64_t>(), s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(delta, d.p, nd, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+shtc_status shtc_accumulate_alm(shtc_ctx* ctx, const double* delta, int n_lat, const double* x,
+                                int n_m, const int32_t* ms, int lmax, int mmax, double* alm_inout,
+                                uint64_t* steps) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (lmax < mmax || mmax < 0) fail(SHTC_EINVAL, "accumulate_alm: need lmax >= mmax >= 0");
+        if (n_lat < 0 || n_m < 0) fail(SHTC_EINVAL, "accumulate_alm: negative sizes");
+        check_latitudes(x, n_lat, "accumulate_alm");
+        check_m_set(ms, n_m, mmax, "accumulate_alm: panel order outside [0, mmax]");
+        uint64_t nominal = 0;
+        for (int i = 0; i < n_m; ++i) nominal += (uint64_t)(lmax - ms[i] + 1) * n_lat;
+        if (steps) *steps += nominal;
+        if (n_lat == 0 || n_m == 0) return;
+        op_plan(ctx, lmax, mmax, n_lat, x, n_m, ms);
+        cudaStream_t s = ctx->stream;
+        const size_t na = alm_count(lmax, mmax) * sizeof(double2);
+        const size_t nd = (size_t)n_lat * n_m * sizeof(double2);
+        DevBuf a, d, ro;
+        a.ensure(na);
+        d.ensure(nd);
+        std::vector<int64_t> rov(n_lat);
+        for (int r = 0; r < n_lat; ++r) rov[r] = (int64_t)r * n_m;
+        ro.upload(rov, s);
+        CK(cudaMemcpyAsync(a.p, alm_inout, na, cudaMemcpyHostToDevice, s));
+        CK(cudaMemcpyAsync(d.p, delta, nd, cudaMemcpyHostToDevice, s));
+        launch_leg_map2alm(ctx->op_leg.view, d.as<double2>(), ro.as<int64_t>(), a.as<double2>(), 1, s);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(alm_inout, a.p, na, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    });
+}
+
+// ---- device helpers --------------------------------------------------------------------
+shtc_status shtc_device_info(int device, char* name, int name_len, int* sm_count, int* cc_major,
+                             int* cc_minor) {
+    return guarded(nullptr, [&] {
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (name && name_len > 0) {
+            std::strncpy(name, prop.name, name_len - 1);
+            name[name_len - 1] = 0;
+        }
+        if (sm_count) *sm_count = prop.multiProcessorCount;
+        if (cc_major) *cc_major = prop.major;
+        if (cc_minor) *cc_minor = prop.minor;
+    });
+}
+
+shtc_status shtc_measure_fp64_peak(int device, double* tflops, double* sm_clock_mhz) {
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        CK(cudaGetDeviceProperties(&prop, device));
+        DevBuf out;
+        out.ensure(sizeof(double));
+        cudaStream_t s;
+        CK(cudaStreamCreate(&s));
+        cudaEvent_t a, b;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b));
+        const int blocks = prop.multiProcessorCount * 4, threads = 256, iters = 4096;
+        launch_dfma_peak(out.as<double>(), blocks, threads, 64, s);  // warm-up
+        CK(cudaEventRecord(a, s));
+        launch_dfma_peak(out.as<double>(), blocks, threads, iters, s);
+        CK(cudaEventRecord(b, s));
+        CK(cudaEventSynchronize(b));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, a, b));
+        const double flops = 2.0 * 8 * 16 * (double)iters * blocks * threads;
+        if (tflops) *tflops = flops / (ms * 1e-3) / 1e12;
+        if (sm_clock_mhz) {
+            int khz = 0;
+            cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, device);
+            *sm_clock_mhz = khz / 1000.0;
+        }
+        cudaEventDestroy(a);
+        cudaEventDestroy(b);
+        cudaStreamDestroy(s);
+    });
+}
+
+}  // extern "C"

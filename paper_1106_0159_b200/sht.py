@@ -1,0 +1,633 @@
+"""Python host mirror of the reference's SHT operator interface, backed by libshtc (CUDA).
+
+Names, argument meaning and error classes follow /root/reference/proj/include/sht:
+  build_healpix_grid / build_gauss_legendre_grid / gauss_legendre_nodes   grid.hpp:45-58
+  symmetric_ring_pairs                                                     grid.hpp:62-63
+  AlmSet count / offset (m-major triangle)                                 alm.hpp:16-35
+  synthesis / analysis (alm2map / map2alm)                                 transforms.hpp:73-79
+  compute_delta_a / compute_delta_a_ring_major / accumulate_alm /
+  accumulate_alm_partial / reduce_partials                                 transforms.hpp:32-69
+  splitmix64_at / uniform_pm1 / random_alm                                 experiment.hpp:14-25
+  assign_m / assign_rings / thread_partition / WorkerLayout                distribution.hpp:15-40
+Every transform runs on the GPU through the C ABI; the geometry, layouts and input
+generators are host-side bookkeeping (they are not on the hot path).
+std::invalid_argument maps to ValueError, std::domain_error to ArithmeticError.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from ._lib import Timing, check, lib
+
+# ----------------------------------------------------------------------------------------
+# containers and geometry
+# ----------------------------------------------------------------------------------------
+
+
+def alm_count(lmax: int, mmax: int) -> int:
+    """AlmSet::count (alm.cpp:13-16)."""
+    return (mmax + 1) * (lmax + 1) - mmax * (mmax + 1) // 2
+
+
+def alm_offset(m: int, lmax: int) -> int:
+    """AlmSet::offset (alm.hpp:27-30)."""
+    return m * (lmax + 1) - m * (m - 1) // 2
+
+
+def alm_index(l: int, m: int, lmax: int) -> int:
+    return alm_offset(m, lmax) + (l - m)
+
+
+@dataclass
+class PixelGrid:
+    """sht::PixelGrid (grid.hpp:27-37) as plain ring arrays."""
+
+    scheme: str
+    nside: int
+    cos_theta: np.ndarray
+    n_phi: np.ndarray
+    phi_0: np.ndarray
+    weight: np.ndarray
+    pixel_offset: np.ndarray = field(default=None)
+
+    def __post_init__(self):
+        self.cos_theta = np.ascontiguousarray(self.cos_theta, dtype=np.float64)
+        self.n_phi = np.ascontiguousarray(self.n_phi, dtype=np.int32)
+        self.phi_0 = np.ascontiguousarray(self.phi_0, dtype=np.float64)
+        self.weight = np.ascontiguousarray(self.weight, dtype=np.float64)
+        if self.pixel_offset is None:
+            self.pixel_offset = np.concatenate(
+                [[0], np.cumsum(self.n_phi.astype(np.int64))[:-1]]).astype(np.int64)
+        self.pixel_offset = np.ascontiguousarray(self.pixel_offset, dtype=np.int64)
+
+    @property
+    def n_rings(self) -> int:
+        return int(self.cos_theta.shape[0])
+
+    @property
+    def n_pix(self) -> int:
+        return int(self.n_phi.astype(np.int64).sum())
+
+    def cos_thetas(self) -> np.ndarray:
+        return self.cos_theta.copy()
+
+
+def build_healpix_grid(nside: int) -> PixelGrid:
+    """HEALPix ring scheme (grid.cpp:23-67)."""
+    if nside < 1:
+        raise ValueError("healpix grid: nside must be >= 1")
+    n_rings = 4 * nside - 1
+    npix = 12 * nside * nside
+    z = np.zeros(n_rings)
+    nphi = np.zeros(n_rings, np.int32)
+    p0 = np.zeros(n_rings)
+    w = np.full(n_rings, 4.0 * math.pi / float(npix))
+    for i in range(1, 2 * nside + 1):
+        if i < nside:
+            nphi[i - 1] = 4 * i
+            z[i - 1] = 1.0 - float(i) * i / (3.0 * nside * nside)
+            p0[i - 1] = math.pi / (4.0 * i)
+        else:
+            nphi[i - 1] = 4 * nside
+            z[i - 1] = 4.0 / 3.0 - 2.0 * i / (3.0 * nside)
+            p0[i - 1] = math.pi / (4.0 * nside) if (i - nside) % 2 == 0 else 0.0
+    for i in range(2 * nside + 1, n_rings + 1):
+        src = (4 * nside - i) - 1
+        nphi[i - 1] = nphi[src]
+        p0[i - 1] = p0[src]
+        z[i - 1] = -z[src]
+    return PixelGrid("healpix-ring", nside, z, nphi, p0, w)
+
+
+def gauss_legendre_nodes(n: int):
+    """Nodes (descending) and weights by Newton iteration on P_n (grid.cpp:69-104)."""
+    if n < 1:
+        raise ValueError("gauss_legendre_nodes: n must be >= 1")
+    x = np.zeros(n)
+    w = np.zeros(n)
+    for i in range((n + 1) // 2):
+        t = math.cos(math.pi * (i + 0.75) / (n + 0.5))
+        dp = 0.0
+        for _ in range(100):
+            p0, p1 = 1.0, t
+            for l in range(2, n + 1):
+                p0, p1 = p1, ((2.0 * l - 1.0) * t * p1 - (l - 1.0) * p0) / l
+            dp = n * (p0 - t * p1) / (1.0 - t * t)
+            dt = p1 / dp
+            t -= dt
+            if abs(dt) < 1e-15:
+                break
+        else:
+            raise RuntimeError("gauss_legendre_nodes: Newton iteration failed")
+        x[i] = t
+        w[i] = 2.0 / ((1.0 - t * t) * dp * dp)
+        x[n - 1 - i] = -t
+        w[n - 1 - i] = w[i]
+    if n % 2 == 1:
+        x[n // 2] = 0.0
+    return x, w
+
+
+def build_gauss_legendre_grid(n_rings: int, n_phi: int) -> PixelGrid:
+    """Gauss-Legendre grid (grid.cpp:106-131)."""
+    if n_rings < 1:
+        raise ValueError("gauss-legendre grid: n_rings must be >= 1")
+    if n_phi < 1:
+        raise ValueError("gauss-legendre grid: n_phi must be >= 1")
+    x, glw = gauss_legendre_nodes(n_rings)
+    return PixelGrid("gauss-legendre", 0, x, np.full(n_rings, n_phi, np.int32),
+                     np.zeros(n_rings), 2.0 * math.pi / n_phi * glw)
+
+
+def symmetric_ring_pairs(grid: PixelGrid):
+    """grid.cpp:133-151."""
+    n = grid.n_rings
+    pairs = []
+    for k in range(n // 2):
+        j = n - 1 - k
+        if grid.n_phi[k] != grid.n_phi[j] or abs(grid.cos_theta[k] + grid.cos_theta[j]) > 1e-14:
+            raise ValueError("symmetric_ring_pairs: grid is not mirror symmetric")
+        pairs.append((k, j))
+    if n % 2 == 1:
+        if abs(grid.cos_theta[n // 2]) > 1e-14:
+            raise ValueError("symmetric_ring_pairs: central ring is off the equator")
+        pairs.append((n // 2, None))
+    return pairs
+
+
+# ----------------------------------------------------------------------------------------
+# synthetic inputs (experiment.cpp:11-33)
+# ----------------------------------------------------------------------------------------
+_M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
+
+
+def splitmix64_at(seed, index):
+    """Counter-based splitmix64 (experiment.cpp:11-16), vectorised over index."""
+    with np.errstate(over="ignore"):
+        idx = np.asarray(index, dtype=np.uint64)
+        z = np.uint64(seed) + (idx + np.uint64(1)) * np.uint64(0x9E3779B97F4A7C15)
+        z = (z ^ (z >> np.uint64(30))) * np.uint64(0xBF58476D1CE4E5B9)
+        z = (z ^ (z >> np.uint64(27))) * np.uint64(0x94D049BB133111EB)
+        return z ^ (z >> np.uint64(31))
+
+
+def uniform_pm1(seed, index):
+    u = ((splitmix64_at(seed, index) >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    return 2.0 * u - 1.0
+
+
+def random_alm(lmax: int, mmax: int, seed: int) -> np.ndarray:
+    """Re, Im i.i.d. uniform(-1,1), Im a_l0 = 0 (experiment.cpp:24-33)."""
+    n = alm_count(lmax, mmax)
+    k = np.arange(n, dtype=np.uint64)
+    a = uniform_pm1(seed, 2 * k) + 1j * uniform_pm1(seed, 2 * k + np.uint64(1))
+    a[: lmax + 1] = a[: lmax + 1].real  # m == 0 block
+    return a
+
+
+def gaussian_alm(lmax: int, mmax: int, seed: int) -> np.ndarray:
+    """N(0,1) re/im by Box-Muller on the same counter stream, Im a_l0 = 0."""
+    n = alm_count(lmax, mmax)
+    k = np.arange(n, dtype=np.uint64)
+    u1 = ((splitmix64_at(seed, 2 * k) >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    u2 = ((splitmix64_at(seed, 2 * k + np.uint64(1)) >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    r = np.sqrt(-2.0 * np.log(u1))
+    a = r * np.cos(2 * np.pi * u2) + 1j * r * np.sin(2 * np.pi * u2)
+    a[: lmax + 1] = a[: lmax + 1].real
+    return a
+
+
+def gaussian_map(n_pix: int, seed: int) -> np.ndarray:
+    k = np.arange(n_pix, dtype=np.uint64)
+    u1 = ((splitmix64_at(seed, 2 * k) >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    u2 = ((splitmix64_at(seed, 2 * k + np.uint64(1)) >> np.uint64(11)).astype(np.float64) + 0.5) * 2.0 ** -53
+    return np.sqrt(-2.0 * np.log(u1)) * np.cos(2 * np.pi * u2)
+
+
+# ----------------------------------------------------------------------------------------
+# distribution layouts (distribution.cpp:82-171) — host bookkeeping for multi-GPU runs
+# ----------------------------------------------------------------------------------------
+def assign_m(mmax: int, n_workers: int):
+    if mmax < 0:
+        raise ValueError("assign_m: mmax must be >= 0")
+    if n_workers < 1:
+        raise ValueError("assign_m: n_workers must be >= 1")
+    if n_workers > 1 and n_workers > (mmax + 1) // 2:
+        raise ValueError("assign_m: n_workers > mmax/2")
+    sets = [[] for _ in range(n_workers)]
+    lo, hi, w = 0, mmax, 0
+    while lo < hi:
+        sets[w] += [lo, hi]
+        lo += 1
+        hi -= 1
+        w = (w + 1) % n_workers
+    if lo == hi:
+        sets[w].append(lo)
+    return [sorted(s) for s in sets]
+
+
+def assign_rings(grid: PixelGrid, n_workers: int):
+    r_n = grid.n_rings
+    if n_workers < 1:
+        raise ValueError("assign_rings: n_workers must be >= 1")
+    if r_n < 1:
+        raise ValueError("assign_rings: empty grid")
+    if n_workers == 1:
+        return [list(range(r_n))]
+    if 2 * n_workers > r_n:
+        raise ValueError("assign_rings: n_workers > n_rings/2")
+    h = (r_n + 1) // 2
+    q, rem = divmod(h, n_workers)
+    sets, row = [], 0
+    for w in range(n_workers):
+        s = []
+        for _ in range(q + (1 if w < rem else 0)):
+            s.append(row)
+            if r_n - 1 - row != row:
+                s.append(r_n - 1 - row)
+            row += 1
+        sets.append(sorted(s))
+    return sets
+
+
+def thread_partition(m_set, n_threads: int):
+    if n_threads <= 0:
+        raise ValueError("thread_partition: n_threads must be >= 1")
+    ms = sorted(m_set)
+    sets = [[] for _ in range(n_threads)]
+    if not ms:
+        return sets
+    top = ms[-1]
+    load = [0] * n_threads
+    lo, hi, t = 0, len(ms) - 1, 0
+    while lo < hi:
+        sets[t] += [ms[lo], ms[hi]]
+        load[t] += (top + 1 - ms[lo]) + (top + 1 - ms[hi])
+        lo += 1
+        hi -= 1
+        t = (t + 1) % n_threads
+    if lo == hi:
+        best = min(range(n_threads), key=lambda j: (load[j], j))
+        sets[best].append(ms[lo])
+    return [sorted(s) for s in sets]
+
+
+@dataclass
+class WorkerLayout:
+    n_workers: int
+    mmax: int
+    n_rings: int
+    m_sets: list
+    ring_sets: list
+
+    @staticmethod
+    def create(grid: PixelGrid, mmax: int, n_workers: int) -> "WorkerLayout":
+        m_sets = [list(range(mmax + 1))] if n_workers == 1 else assign_m(mmax, n_workers)
+        return WorkerLayout(n_workers, mmax, grid.n_rings, m_sets, assign_rings(grid, n_workers))
+
+
+def exchange_layout(layout: WorkerLayout, rank: int):
+    """Packed all-to-all layouts of one worker (exchange_m_to_rings, distribution.cpp:233-298).
+
+    Send side (Legendre output, alm2map): rows grouped by destination worker j, each block
+    [|R_j| rows x |M_rank| cols] contiguous; row_off[r] = complex offset of ring r's row.
+    Receive side (fold input): block from source j is [|R_rank| x |M_j|]; order m of M_j lives
+    at m_base[m] + pos * m_stride[m] for ring position pos in R_rank.
+    Returns (row_off, send_counts, recv_counts, ring_list, m_base, m_stride) in complex units.
+    The same layouts serve map2alm in reverse (analysis writes the recv-shaped blocks per
+    destination owner, the Legendre stage reads rows through row_off).
+    """
+    W = layout.n_workers
+    Mi = layout.m_sets[rank]
+    row_off = np.zeros(layout.n_rings, np.int64)
+    send_counts = []
+    off = 0
+    for j in range(W):
+        Rj = layout.ring_sets[j]
+        for p, r in enumerate(Rj):
+            row_off[r] = off + p * len(Mi)
+        send_counts.append(len(Rj) * len(Mi))
+        off += len(Rj) * len(Mi)
+    Ri = layout.ring_sets[rank]
+    m_base = np.zeros(layout.mmax + 1, np.int64)
+    m_stride = np.zeros(layout.mmax + 1, np.int64)
+    recv_counts = []
+    off = 0
+    for j in range(W):
+        Mj = layout.m_sets[j]
+        for c, m in enumerate(Mj):
+            m_base[m] = off + c
+            m_stride[m] = len(Mj)
+        recv_counts.append(len(Ri) * len(Mj))
+        off += len(Ri) * len(Mj)
+    return row_off, send_counts, recv_counts, np.asarray(Ri, np.int32), m_base, m_stride
+
+
+# ----------------------------------------------------------------------------------------
+# GPU context
+# ----------------------------------------------------------------------------------------
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None else None
+
+
+class Context:
+    """One GPU's transform state (geometry, band, cached plans) — the C ABI shtc_ctx."""
+
+    def __init__(self, device: int = 0):
+        self._h = C.c_void_p()
+        check(lib().shtc_create(int(device), C.byref(self._h)))
+        self.device = device
+        self.grid = None
+        self.lmax = self.mmax = None
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().shtc_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _check(self, rc):
+        check(rc, self._h)
+
+    def set_stream(self, stream_ptr: int | None):
+        self._check(lib().shtc_set_stream(self._h, C.c_void_p(stream_ptr) if stream_ptr else None))
+
+    def set_grid(self, grid: PixelGrid, mirror: bool = True):
+        self._check(lib().shtc_set_grid(self._h, grid.n_rings, _p(grid.cos_theta), _p(grid.n_phi),
+                                        _p(grid.phi_0), _p(grid.weight), _p(grid.pixel_offset),
+                                        int(bool(mirror))))
+        self.grid = grid
+
+    def set_band(self, lmax: int, mmax: int, ms=None):
+        if ms is None:
+            self._check(lib().shtc_set_band(self._h, lmax, mmax, 0, None))
+        else:
+            ms = np.ascontiguousarray(ms, np.int32)
+            self._check(lib().shtc_set_band(self._h, lmax, mmax, len(ms), _p(ms)))
+        self.lmax, self.mmax = lmax, mmax
+
+    def plan(self) -> float:
+        t = C.c_double()
+        self._check(lib().shtc_plan(self._h, C.byref(t)))
+        return t.value
+
+    def plan_stats(self):
+        a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._check(lib().shtc_plan_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
+        return {"nominal": a.value, "executed": b.value, "useful": c.value}
+
+    # host-buffer transforms ---------------------------------------------------------
+    def alm2map(self, alm: np.ndarray, out: np.ndarray | None = None, timing: bool = False):
+        alm = np.ascontiguousarray(alm, np.complex128)
+        if alm.size != alm_count(self.lmax, self.mmax):
+            raise ValueError("alm2map: coefficient count != AlmSet::count(lmax, mmax)")
+        mp = out if out is not None else np.empty(self.grid.n_pix)
+        t = Timing()
+        self._check(lib().shtc_alm2map(self._h, _p(alm), _p(mp), C.byref(t)))
+        return (mp, t.as_dict()) if timing else mp
+
+    def map2alm(self, mp: np.ndarray, out: np.ndarray | None = None, timing: bool = False):
+        mp = np.ascontiguousarray(mp, np.float64)
+        if mp.size != self.grid.n_pix:
+            raise ValueError("analysis: pixel count != grid")
+        alm = out if out is not None else np.empty(alm_count(self.lmax, self.mmax), np.complex128)
+        t = Timing()
+        self._check(lib().shtc_map2alm(self._h, _p(mp), _p(alm), C.byref(t)))
+        return (alm, t.as_dict()) if timing else alm
+
+    # device-pointer entry points (ints are raw CUDA pointers, e.g. torch.data_ptr()) --
+    def alm2map_dev(self, alm_ptr: int, map_ptr: int, timing: bool = False):
+        t = Timing()
+        self._check(lib().shtc_alm2map_dev(self._h, C.c_void_p(alm_ptr), C.c_void_p(map_ptr),
+                                           C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def map2alm_dev(self, map_ptr: int, alm_ptr: int, timing: bool = False):
+        t = Timing()
+        self._check(lib().shtc_map2alm_dev(self._h, C.c_void_p(map_ptr), C.c_void_p(alm_ptr),
+                                           C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def set_exchange_layout(self, row_off=None, ring_list=None, m_base=None, m_stride=None):
+        if row_off is None:
+            self._check(lib().shtc_set_exchange_layout(self._h, None, 0, None, None, None))
+            return
+        ro = np.ascontiguousarray(row_off, np.int64)
+        rl = np.ascontiguousarray(ring_list, np.int32)
+        mb = np.ascontiguousarray(m_base, np.int64)
+        mst = np.ascontiguousarray(m_stride, np.int64)
+        self._check(lib().shtc_set_exchange_layout(self._h, _p(ro), len(rl), _p(rl), _p(mb), _p(mst)))
+
+    def legendre_alm2map_dev(self, alm_ptr, delta_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_legendre_alm2map_dev(self._h, C.c_void_p(alm_ptr), C.c_void_p(delta_ptr),
+                                                    C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def legendre_map2alm_dev(self, delta_ptr, alm_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_legendre_map2alm_dev(self._h, C.c_void_p(delta_ptr), C.c_void_p(alm_ptr),
+                                                    C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def ring_synthesis_dev(self, delta_ptr, map_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_ring_synthesis_dev(self._h, C.c_void_p(delta_ptr), C.c_void_p(map_ptr),
+                                                  C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def ring_analysis_dev(self, map_ptr, delta_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_ring_analysis_dev(self._h, C.c_void_p(map_ptr), C.c_void_p(delta_ptr),
+                                                 C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    # Legendre-stage operators ----------------------------------------------------------
+    def delta_a(self, alm, lmax, mmax, x, ms):
+        alm = np.ascontiguousarray(alm, np.complex128)
+        x = np.ascontiguousarray(x, np.float64)
+        ms = np.ascontiguousarray(ms, np.int32)
+        out = np.zeros((len(x), len(ms)), np.complex128)
+        steps = C.c_uint64(0)
+        self._check(lib().shtc_delta_a(self._h, _p(alm), lmax, mmax, len(x), _p(x), len(ms), _p(ms),
+                                       _p(out), C.byref(steps)))
+        return out, steps.value
+
+    def accumulate_alm(self, delta, x, ms, lmax, mmax, alm_inout=None):
+        d = np.ascontiguousarray(delta, np.complex128)
+        x = np.ascontiguousarray(x, np.float64)
+        ms = np.ascontiguousarray(ms, np.int32)
+        out = (np.zeros(alm_count(lmax, mmax), np.complex128) if alm_inout is None
+               else np.ascontiguousarray(alm_inout, np.complex128).copy())
+        steps = C.c_uint64(0)
+        self._check(lib().shtc_accumulate_alm(self._h, _p(d), len(x), _p(x), len(ms), _p(ms), lmax, mmax,
+                                              _p(out), C.byref(steps)))
+        return out, steps.value
+
+
+_DEFAULT = {}
+
+
+def default_context(device: int = 0) -> Context:
+    """Process-wide context per device (the reference API has no handle)."""
+    if device not in _DEFAULT:
+        _DEFAULT[device] = Context(device)
+    return _DEFAULT[device]
+
+
+def _grid_ctx(grid: PixelGrid, lmax: int, mmax: int, pairing: bool, device: int) -> Context:
+    ctx = default_context(device)
+    key = (id(grid), grid.n_rings, grid.n_pix, bool(pairing))
+    if getattr(ctx, "_grid_key", None) != key:
+        ctx.set_grid(grid, mirror=pairing)
+        ctx._grid_key = key
+        ctx._band_key = None
+    if getattr(ctx, "_band_key", None) != (lmax, mmax):
+        ctx.set_band(lmax, mmax)
+        ctx._band_key = (lmax, mmax)
+    return ctx
+
+
+# ----------------------------------------------------------------------------------------
+# reference-named operators
+# ----------------------------------------------------------------------------------------
+def synthesis(alm: np.ndarray, lmax: int, mmax: int, grid: PixelGrid, pairing: bool = True,
+              device: int = 0) -> np.ndarray:
+    """alm2map (transforms.cpp:402-445); mirror pairing is used whenever the grid allows it."""
+    if grid.n_rings == 0:
+        raise ValueError("synthesis: empty grid")
+    return _grid_ctx(grid, lmax, mmax, pairing, device).alm2map(alm)
+
+
+def analysis(mp: np.ndarray, lmax: int, mmax: int, grid: PixelGrid, pairing: bool = True,
+             device: int = 0) -> np.ndarray:
+    """map2alm (transforms.cpp:447-485)."""
+    if lmax < mmax or mmax < 0:
+        raise ValueError("analysis: need lmax >= mmax >= 0")
+    if grid.n_rings == 0:
+        raise ValueError("analysis: empty grid")
+    if np.asarray(mp).size != grid.n_pix:
+        raise ValueError("analysis: pixel count != grid")
+    return _grid_ctx(grid, lmax, mmax, pairing, device).map2alm(mp)
+
+
+def _checked_m_set(m_set, mmax, where):
+    ms = sorted(int(m) for m in m_set)
+    for i, m in enumerate(ms):
+        if m < 0 or m > mmax:
+            raise ValueError(f"{where}: order outside [0, mmax]")
+        if i and ms[i - 1] == m:
+            raise ValueError(f"{where}: duplicate order")
+    return ms
+
+
+def compute_delta_a(alm, lmax: int, mmax: int, cos_thetas, m_set, device: int = 0):
+    """Delta panel [ring][m] (transforms.cpp:269-286); returns (panel, steps)."""
+    ms = _checked_m_set(m_set, mmax, "compute_delta_a")
+    x = np.ascontiguousarray(cos_thetas, np.float64)
+    if np.any(~(np.abs(x) <= 1.0)):
+        raise ValueError("compute_delta_a: cos_theta outside [-1, 1]")
+    return default_context(device).delta_a(alm, lmax, mmax, x, ms)
+
+
+def compute_delta_a_ring_major(alm, lmax, mmax, cos_thetas, m_set, n_work_items: int = 1, device: int = 0):
+    """Same numbers as compute_delta_a (transforms.cpp:288-331): the loop order is a CPU detail."""
+    if n_work_items < 1:
+        raise ValueError("compute_delta_a_ring_major: n_work_items must be >= 1")
+    ms = _checked_m_set(m_set, mmax, "compute_delta_a_ring_major")
+    x = np.ascontiguousarray(cos_thetas, np.float64)
+    if np.any(~(np.abs(x) <= 1.0)):
+        raise ValueError("compute_delta_a_ring_major: cos_theta outside [-1, 1]")
+    return default_context(device).delta_a(alm, lmax, mmax, x, ms)
+
+
+def accumulate_alm(panel, rings, ms, cos_thetas, lmax: int, mmax: int, device: int = 0):
+    """a_lm = sum_r Delta^S_m(r) P_lm (transforms.cpp:357-365); returns (alm, steps)."""
+    rings = list(rings)
+    if rings != list(range(len(rings))):
+        raise ValueError("accumulate_alm: ring coverage incomplete")
+    return _accumulate_core(panel, rings, ms, cos_thetas, lmax, mmax, "accumulate_alm", device)
+
+
+def _accumulate_core(panel, rings, ms, cos_thetas, lmax, mmax, where, device):
+    if lmax < mmax or mmax < 0:
+        raise ValueError(f"{where}: need lmax >= mmax >= 0")
+    x = np.ascontiguousarray(cos_thetas, np.float64)
+    if len(x) != len(rings):
+        raise ValueError(f"{where}: latitude count != panel rings")
+    if np.any(~(np.abs(x) <= 1.0)):
+        raise ValueError(f"{where}: cos_theta outside [-1, 1]")
+    ms = [int(m) for m in ms]
+    for m in ms:
+        if m < 0 or m > mmax:
+            raise ValueError(f"{where}: panel order outside [0, mmax]")
+    panel = np.ascontiguousarray(panel, np.complex128).reshape(len(x), len(ms))
+    order = np.argsort(ms, kind="stable")
+    return default_context(device).accumulate_alm(panel[:, order], x, np.asarray(ms)[order], lmax, mmax)
+
+
+@dataclass
+class PartialAlm:
+    alm: np.ndarray
+    rings: list
+    lmax: int
+    mmax: int
+
+
+def accumulate_alm_partial(panel, rings, ms, cos_thetas, lmax, mmax, device: int = 0):
+    """transforms.cpp:367-378."""
+    rings = list(rings)
+    for i in range(1, len(rings)):
+        if rings[i] <= rings[i - 1]:
+            raise ValueError("accumulate_alm_partial: rings not strictly ascending")
+    alm, steps = _accumulate_core(panel, rings, ms, cos_thetas, lmax, mmax, "accumulate_alm_partial", device)
+    return PartialAlm(alm, rings, lmax, mmax), steps
+
+
+def reduce_partials(parts, n_rings: int) -> np.ndarray:
+    """Sums partials in list order after the disjoint/cover checks (transforms.cpp:380-400)."""
+    if not parts:
+        raise ValueError("reduce_partials: no partials")
+    lmax, mmax = parts[0].lmax, parts[0].mmax
+    seen = []
+    for p in parts:
+        if p.lmax != lmax or p.mmax != mmax:
+            raise ValueError("reduce_partials: mismatched band limits")
+        seen += list(p.rings)
+    seen.sort()
+    for i in range(1, len(seen)):
+        if seen[i] == seen[i - 1]:
+            raise ValueError("reduce_partials: overlapping ring subsets")
+    if len(seen) != n_rings or (n_rings > 0 and (seen[0] != 0 or seen[-1] != n_rings - 1)):
+        raise ValueError("reduce_partials: ring subsets do not cover the grid")
+    out = np.zeros(alm_count(lmax, mmax), np.complex128)
+    for p in parts:
+        out += p.alm
+    return out
+
+
+def device_count() -> int:
+    return int(lib().shtc_device_count())
+
+
+def device_info(device: int = 0):
+    name = C.create_string_buffer(128)
+    sm, ma, mi = C.c_int(), C.c_int(), C.c_int()
+    check(lib().shtc_device_info(device, name, 128, C.byref(sm), C.byref(ma), C.byref(mi)))
+    return {"name": name.value.decode(), "sm_count": sm.value, "cc": f"{ma.value}.{mi.value}"}
+
+
+def measure_fp64_peak(device: int = 0):
+    t, mhz = C.c_double(), C.c_double()
+    check(lib().shtc_measure_fp64_peak(device, C.byref(t), C.byref(mhz)))
+    return t.value, mhz.value

@@ -1,0 +1,117 @@
+"""GPU parity: the sm_100a path (through the C ABI) against the reference implementation.
+
+The oracle is the reference itself (oracle/_ref/libsht_ref.so, built from
+/root/reference/proj/src by oracle/build_ref.sh).  Tolerances: the north star's FP64 bar is
+rel-RMS <= 1e-10 on maps and a_lm; at these sizes the renormalised/FMA recurrence agrees to
+~1e-13, so most tests gate tighter and report the worst case.
+"""
+import numpy as np
+import pytest
+
+from oracle import ref
+from paper_1106_0159_b200 import sht
+
+pytestmark = pytest.mark.gpu
+
+RMS_TOL = 1e-10
+
+
+def rel_rms(a, b):
+    a = np.asarray(a); b = np.asarray(b)
+    den = np.sqrt(np.sum(np.abs(b) ** 2))
+    return float(np.sqrt(np.sum(np.abs(a - b) ** 2)) / (den if den > 0 else 1.0))
+
+
+def worst(a, b):
+    m = np.max(np.abs(b))
+    return float(np.max(np.abs(a - b)) / (m if m > 0 else 1.0))
+
+
+def as_sht(g: ref.Grid) -> sht.PixelGrid:
+    return sht.PixelGrid("x", g.nside, g.cos_theta, g.n_phi, g.phi_0, g.weight)
+
+
+@pytest.mark.parametrize("nside,lmax", [(1, 2), (2, 5), (4, 12), (8, 20), (16, 40), (32, 64), (128, 256)])
+def test_alm2map_healpix_matches_reference(gpu_ctx, nside, lmax):
+    g = ref.healpix_grid(nside)
+    alm = ref.random_alm(lmax, lmax, 12345)
+    want, _ = ref.synthesis(alm, lmax, lmax, g, pairing=True)
+    gpu_ctx.set_grid(as_sht(g)); gpu_ctx.set_band(lmax, lmax)
+    got = gpu_ctx.alm2map(alm)
+    assert rel_rms(got, want) <= 1e-12, (rel_rms(got, want), worst(got, want))
+    assert worst(got, want) <= 1e-11
+
+
+@pytest.mark.parametrize("nside,lmax", [(1, 2), (2, 5), (4, 12), (8, 20), (16, 40), (32, 64), (128, 256)])
+def test_map2alm_healpix_matches_reference(gpu_ctx, nside, lmax):
+    g = ref.healpix_grid(nside)
+    alm = ref.random_alm(lmax, lmax, 777)
+    mp, _ = ref.synthesis(alm, lmax, lmax, g, pairing=True)
+    want, _ = ref.analysis(mp, lmax, lmax, g, pairing=True)
+    gpu_ctx.set_grid(as_sht(g)); gpu_ctx.set_band(lmax, lmax)
+    got = gpu_ctx.map2alm(mp)
+    assert rel_rms(got, want) <= 1e-12, (rel_rms(got, want), worst(got, want))
+
+
+@pytest.mark.parametrize("nr,nphi,lmax", [(17, 34, 16), (33, 66, 32), (10, 24, 9), (21, 44, 20), (26, 104, 25),
+                                           (9, 20, 8), (12, 7, 5), (13, 101, 12), (8, 202, 7)])
+def test_gauss_legendre_grids(gpu_ctx, nr, nphi, lmax):
+    g = ref.gl_grid(nr, nphi)
+    alm = ref.random_alm(lmax, lmax, 91)
+    want, _ = ref.synthesis(alm, lmax, lmax, g, pairing=True)
+    gpu_ctx.set_grid(as_sht(g)); gpu_ctx.set_band(lmax, lmax)
+    got = gpu_ctx.alm2map(alm)
+    assert rel_rms(got, want) <= 1e-12
+    back_ref, _ = ref.analysis(want, lmax, lmax, g, pairing=True)
+    back = gpu_ctx.map2alm(want)
+    assert rel_rms(back, back_ref) <= 1e-12
+
+
+def test_delta_panel_matches_reference(gpu_ctx):
+    lmax = 40
+    x, _ = ref.gl_nodes(41)
+    alm = ref.random_alm(lmax, lmax, 91)
+    ms = np.arange(lmax + 1)
+    want, wsteps = ref.compute_delta_a(alm, lmax, lmax, x, ms)
+    got, steps = gpu_ctx.delta_a(alm, lmax, lmax, x, ms)
+    assert steps == wsteps
+    assert worst(got, want) <= 1e-12
+
+
+def test_accumulate_matches_reference(gpu_ctx):
+    lmax = 20
+    x, _ = ref.gl_nodes(24)
+    rng = np.random.default_rng(808)
+    ms = np.arange(lmax + 1)
+    panel = rng.uniform(-1, 1, (24, lmax + 1)) + 1j * rng.uniform(-1, 1, (24, lmax + 1))
+    want, _ = ref.accumulate_alm(panel, x, ms, lmax, lmax)
+    got, _ = gpu_ctx.accumulate_alm(panel, x, ms, lmax, lmax)
+    assert rel_rms(got, want) <= 1e-13
+
+
+def test_deep_order_stream(gpu_ctx):
+    """m=2000, lmax=2200 at x=0.999 (test_legendre.cpp:167-224): seed needs scale << 0."""
+    m, lmax = 2000, 2200
+    alm = np.zeros(ref.alm_count(lmax, lmax), np.complex128)
+    rng = np.random.default_rng(5)
+    off = m * (lmax + 1) - m * (m - 1) // 2
+    alm[off:off + lmax - m + 1] = rng.standard_normal(lmax - m + 1)
+    x = np.array([0.999, 0.9, 0.5, -0.3, 0.0])
+    want, _ = ref.compute_delta_a(alm, lmax, lmax, x, [m])
+    got, _ = gpu_ctx.delta_a(alm, lmax, lmax, x, [m])
+    assert np.all(np.isfinite(got))
+    assert worst(got, want) <= 1e-10
+
+
+def test_c2_alm2map_and_map2alm(gpu_ctx):
+    """C2/C3 (nside 1024, lmax 2048) against the reference on the same a_lm."""
+    nside, lmax = 1024, 2048
+    g = ref.healpix_grid(nside)
+    alm = ref.random_alm(lmax, lmax, 12345)
+    want, _ = ref.distributed_synthesis(alm, lmax, lmax, g, n_workers=1, n_threads=8, pairing=True)
+    gpu_ctx.set_grid(as_sht(g)); gpu_ctx.set_band(lmax, lmax)
+    got = gpu_ctx.alm2map(alm)
+    assert rel_rms(got, want) <= RMS_TOL, (rel_rms(got, want), worst(got, want))
+    back_ref, _ = ref.distributed_analysis(want, lmax, lmax, g, n_workers=1, n_threads=8, pairing=True)
+    back = gpu_ctx.map2alm(want)
+    assert rel_rms(back, back_ref) <= RMS_TOL, (rel_rms(back, back_ref), worst(back, back_ref))
