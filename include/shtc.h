@@ -87,6 +87,10 @@ shtc_status shtc_plan(shtc_ctx* ctx, double* plan_ms);
  * useful (steps whose term the reference keeps, i.e. ladder scale k == 0). */
 shtc_status shtc_plan_stats(shtc_ctx* ctx, uint64_t* nominal, uint64_t* executed,
                             uint64_t* useful);
+/* Executed pair-steps split by kernel phase: before the tile's first activation (recurrence +
+ * ladder check only), inside the activation window (checked), after it (unchecked). */
+shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* checked,
+                                  uint64_t* fast);
 
 /* ---- whole transforms ---------------------------------------------------------------- */
 /* alm: 2*AlmSet::count(lmax,mmax) doubles; map: n_pix doubles.  Host buffers. */

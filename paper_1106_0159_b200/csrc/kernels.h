@@ -30,10 +30,19 @@ struct LegTables {
     const int64_t* tab_off;
 };
 
-// Tile = TILE_STREAMS consecutive streams handled by one warp (32 lanes x R streams).
+// Tile = LEG_TILE consecutive streams handled by one warp (32 lanes x LEG_R streams).
 constexpr int LEG_R = 4;
-constexpr int LEG_W = 8;  // warps per block
 constexpr int LEG_TILE = 32 * LEG_R;
+constexpr int LEG_WARPS = 4;      // warps per block of the persistent Legendre kernels
+constexpr int LEG_CL = 32;        // degree steps staged per chunk (one entry per lane)
+constexpr int LEG_M2A_GROUP = 4;  // tiles per map2alm work item (partials reduce G-fold)
+
+// One warp-sized unit of work of the persistent kernels.
+//   alm2map: (mi, tile id, -, -); map2alm: (mi, first index into tile_list, tile count, item
+//   index g within the order), items of an order write partial sums into scratch slots.
+struct LegItem {
+    int mi, a, b, g;
+};
 
 struct LegPlanView {
     int lmax;
@@ -48,7 +57,13 @@ struct LegPlanView {
     const int* tile_list;      // alive tiles, grouped per order
     const int* tile_list_off;  // [n_m]
     const int* tile_list_cnt;  // [n_m]
-    const int* m_order;        // block -> order index (cost descending)
+    const LegItem* a2m_items;  // cost-descending
+    int n_a2m_items;
+    const LegItem* m2a_items;  // cost-descending
+    int n_m2a_items;
+    const int* m2a_items_per_m;     // [n_m]
+    const int64_t* m2a_slot_base;   // [n_m] double2 offset of the order's first partial slot
+    int64_t m2a_scratch_elems;
 };
 
 void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s);
@@ -59,11 +74,14 @@ void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* til
                              unsigned long long* useful_dev, cudaStream_t s);
 
 // Delta rows: element (ring r, order index mi) at delta[row_off[r] + mi].
+// counters: >= 1 + n_m ints of device scratch (zeroed by the launcher).
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
-                        const int64_t* row_off, cudaStream_t s);
-// a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.
+                        const int64_t* row_off, int* counters, cudaStream_t s);
+// a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.  scratch: m2a_scratch_elems.
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
-                        double2* alm, int accumulate, cudaStream_t s);
+                        double2* alm, int accumulate, int* counters, double2* scratch,
+                        cudaStream_t s);
+int leg_persistent_blocks(int device);
 
 // ---------------------------------------------------------------------------------------
 // Ring Fourier stage
@@ -84,7 +102,7 @@ struct RingDesc {
     int flags;          // bit0: half-length real trick, bit1: Bluestein
     int ring_pos;       // row position of the ring in the Delta panel addressing
     int npass;
-    unsigned char radix[FFT_MAX_PASSES];
+    unsigned long long radices;  // radix of pass p in bits [4p, 4p+4)
 };
 
 struct RingStageArgs {
@@ -92,15 +110,16 @@ struct RingStageArgs {
     int n_rings;
     const double2* tabs;
     int mmax;
-    const int64_t* m_base;    // Delta(ring_pos, m) at m_base[m] + ring_pos * m_stride[m]
-    const int64_t* m_stride;
+    const int64_t* m_base;    // Delta(ring_pos, m) at m_base[m] + ring_pos * m_stride[m],
+    const int64_t* m_stride;  // or (m_base == nullptr) at m + ring_pos * ld
+    int64_t ld;
     const double2* delta_in;  // synthesis
     double2* delta_out;       // analysis
     const double* map_in;     // analysis
     double* map_out;          // synthesis
 };
 
-// size classes: 0: B<=256 (64 thr), 1: B<=1024 (128), 2: B<=4096 (256), 3: B<=8192 (512)
+// size classes: 0: B<=256 (64 thr), 1: B<=1024 (256), 2: B<=4096 (512), 3: B<=8192 (1024)
 constexpr int FFT_N_CLASSES = 4;
 int fft_class_bmax(int c);
 int fft_class_for(int B);  // -1 if unsupported

@@ -20,9 +20,14 @@
 //     (order, stream); tiles whose streams never activate are skipped, steps before the first
 //     activation of a tile run without accumulation, steps after the last activation run
 //     without any check.
-//   * block = one order m, W warps, each warp one tile of 32 x R latitude-contiguous streams;
-//     recurrence coefficients and a_lm are staged through shared memory in double-buffered
-//     chunks shared by the whole block.
+//   * persistent, warp-independent kernels: each warp pulls (order, tile of 32 x R
+//     latitude-contiguous streams) items from a cost-sorted queue and stages the order's
+//     coefficients (and c_l-scaled a_lm) in its own shared-memory slice LEG_CL degrees at a
+//     time, so no block-wide barrier couples warps that sit in different phases.
+//   * map2alm reduces over the 32 x R streams of a warp through a shared-memory transpose every
+//     8 degrees, accumulates up to LEG_M2A_GROUP tiles per work item into a scratch slot, and
+//     the last item of an order to finish sums the order's slots in a fixed order (no atomics
+//     on data, bitwise reproducible).
 
 #include <climits>
 
@@ -179,27 +184,41 @@ void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* til
 }
 
 // ---------------------------------------------------------------------------------------
-// alm2map: Delta^A_m(r) = sum_l a_lm P_lm(x_r), mirror paired
+// Persistent, warp-independent Legendre kernels.  Every warp pulls (order, tile) items from a
+// cost-sorted queue, stages the order's coefficients for LEG_CL degrees at a time in its own
+// shared-memory slice (no block barriers), and runs the three phases per degree pair:
+//   PREFIX  (both steps before the tile's first activation): recurrence + ladder check
+//   CHECKED (activation window of the tile): + accumulation, + per-lane activation
+//   FAST    (after the tile's last activation): recurrence + accumulation only
 // ---------------------------------------------------------------------------------------
 namespace {
 
 enum Phase { PREFIX = 0, CHECKED = 1, FAST = 2 };
 
+struct Coef {
+    double A, T, ar, ai;  // recurrence coefficient, ladder threshold, staged a_lm * c_l
+};
+
+__device__ __forceinline__ int warp_next_item(int* counter) {
+    int it = 0;
+    if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
+    return __shfl_sync(0xffffffffu, it, 0);
+}
+
 template <int R>
 struct A2MLane {
     double x[R], q0[R], q1[R];
-    double2 ae[R], ao[R];  // even / odd degree offset accumulators
+    double2 ae[R], ao[R];  // even / odd degree-offset accumulators
     int k[R];
 };
 
-// One recurrence step for all R streams of the lane; ODD selects the accumulator.
 template <int R, int PH, bool ODD>
-__device__ __forceinline__ void a2m_step(A2MLane<R>& L, double A, double T, double2 al) {
+__device__ __forceinline__ void a2m_step(A2MLane<R>& L, const Coef& cf) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
+        double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
         if (PH != FAST) {
-            if (fabs(q2) >= T) {
+            if (fabs(q2) >= cf.T) {
                 q2 *= SCALE_DOWN;
                 L.q1[r] *= SCALE_DOWN;
                 if (++L.k[r] == 0) {
@@ -211,58 +230,55 @@ __device__ __forceinline__ void a2m_step(A2MLane<R>& L, double A, double T, doub
         }
         if (PH != PREFIX) {
             double2& acc = ODD ? L.ao[r] : L.ae[r];
-            acc.x = __fma_rn(al.x, q2, acc.x);
-            acc.y = __fma_rn(al.y, q2, acc.y);
+            acc.x = __fma_rn(cf.ar, q2, acc.x);
+            acc.y = __fma_rn(cf.ai, q2, acc.y);
         }
         L.q0[r] = L.q1[r];
         L.q1[r] = q2;
     }
 }
 
-template <int CL>
-struct A2MStage {
-    double A[2][CL];
-    double T[2][CL];
-    double2 al[2][CL];
-};
+template <int R>
+__device__ __forceinline__ void a2m_enter_fast(A2MLane<R>& L) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (L.k[r] != 0) L.q0[r] = L.q1[r] = 0.0;  // dead lanes: keep them finite and silent
+}
 
 }  // namespace
 
-template <int R, int W, int CL>
-__global__ void __launch_bounds__(W * 32)
+template <int R>
+__global__ void __launch_bounds__(LEG_WARPS * 32, 3)
     leg_alm2map_kernel(LegPlanView p, const double2* __restrict__ alm, double2* __restrict__ delta,
-                       const int64_t* __restrict__ row_off) {
-    __shared__ A2MStage<CL> sm;
-    const int mi = p.m_order[blockIdx.x];
-    const int m = p.ms[mi];
-    const int n = p.lmax - m;
+                       const int64_t* __restrict__ row_off, int* __restrict__ counter) {
+    __shared__ Coef sm_all[LEG_WARPS][LEG_CL];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t toff = p.tab.tab_off[mi];
-    const double* __restrict__ gA = p.tab.A + toff;
-    const double* __restrict__ gC = p.tab.C + toff;
-    const double* __restrict__ gT = p.tab.T + toff;
-    const double2* __restrict__ galm = alm + alm_offset(m, p.lmax);
-    const int tbeg = p.tile_list_off[mi], tcnt = p.tile_list_cnt[mi];
-    const double lmu = p.log_mu[m];
-    const int nchunks = (n + CL - 1) / CL;  // steps i = 1..n
-    const double2 a0 = galm[0];
+    Coef* sm = sm_all[warp];
 
-    for (int r0 = 0; r0 < tcnt; r0 += W) {
-        const int ti = r0 + warp;
-        const bool has = ti < tcnt;
-        const int tile = has ? p.tile_list[tbeg + ti] : 0;
-        const int2 info = has ? p.tile_info[(size_t)mi * p.n_tiles + tile] : make_int2(INT_MAX, -1);
+    for (;;) {
+        const int it = warp_next_item(counter);
+        if (it >= p.n_a2m_items) return;
+        const LegItem item = p.a2m_items[it];
+        const int mi = item.mi, tile = item.a;
+        const int m = p.ms[mi];
+        const int n = p.lmax - m;
+        const int64_t toff = p.tab.tab_off[mi];
+        const double* __restrict__ gA = p.tab.A + toff;
+        const double* __restrict__ gC = p.tab.C + toff;
+        const double* __restrict__ gT = p.tab.T + toff;
+        const double2* __restrict__ galm = alm + alm_offset(m, p.lmax);
+        const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
         const int is = info.x, ie = info.y;
+        const double lmu = p.log_mu[m];
+        const double2 a0 = galm[0];
 
         A2MLane<R> L;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int s = tile * (32 * R) + r * 32 + lane;
-            const bool valid = has && s < p.st.n;
-            double mant = 0.0;
+            double mant = 0.0, x = 0.0;
             int k = 0;
-            double x = 0.0;
-            if (valid) {
+            if (s < p.st.n) {
                 x = p.st.x[s];
                 seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
             }
@@ -270,114 +286,85 @@ __global__ void __launch_bounds__(W * 32)
             L.q0[r] = 0.0;
             L.q1[r] = mant;
             L.k[r] = k;
-            // degree offset 0 term: a_mm * P_mm (c_0 = 1), only when already at k == 0
+            // degree offset 0 term: a_mm P_mm (c_0 = 1), only when the seed is already at k == 0
             L.ae[r] = (k == 0) ? make_double2(a0.x * mant, a0.y * mant) : make_double2(0.0, 0.0);
             L.ao[r] = make_double2(0.0, 0.0);
         }
-        bool fast_entered = false;
+        bool fast = false;
 
-        // stage chunk 0
-        if (nchunks > 0) {
-            for (int j = threadIdx.x; j < CL; j += W * 32) {
-                const int i = 1 + j;
-                const bool in = i <= n;
-                sm.A[0][j] = in ? gA[i] : 0.0;
-                sm.T[0][j] = in ? gT[i] : 0x1p1000;
-                if (in) {
-                    const double c = gC[i];
-                    const double2 v = galm[i];
-                    sm.al[0][j] = make_double2(v.x * c, v.y * c);
-                } else {
-                    sm.al[0][j] = make_double2(0.0, 0.0);
-                }
+        // chunk c covers degree offsets i = 1 + c*CL .. ; lane j stages entry j
+        auto fetch = [&](int c, Coef& cf) {
+            const int i = 1 + c * LEG_CL + lane;
+            if (i <= n) {
+                const double cc = gC[i];
+                const double2 v = galm[i];
+                cf.A = gA[i];
+                cf.T = gT[i];
+                cf.ar = v.x * cc;
+                cf.ai = v.y * cc;
+            } else {
+                cf.A = 0.0;
+                cf.T = 0x1p1000;
+                cf.ar = cf.ai = 0.0;
             }
-        }
-        __syncthreads();
-
+        };
+        const int nchunks = (n + LEG_CL - 1) / LEG_CL;
+        Coef nxt;
+        if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            // prefetch chunk c+1 into registers
-            constexpr int PER = (CL + W * 32 - 1) / (W * 32);
-            double pA[PER], pT[PER];
-            double2 pal[PER];
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = threadIdx.x + u * W * 32;
-                const int i = 1 + (c + 1) * CL + j;
-                pA[u] = 0.0;
-                pT[u] = 0x1p1000;
-                pal[u] = make_double2(0.0, 0.0);
-                if (j < CL && i <= n) {
-                    pA[u] = gA[i];
-                    pT[u] = gT[i];
-                    const double cc = gC[i];
-                    const double2 v = galm[i];
-                    pal[u] = make_double2(v.x * cc, v.y * cc);
-                }
-            }
-
-            if (has) {
-                const int i0 = 1 + c * CL;
-                const int cnt = min(CL, n - i0 + 1);
-                int j = 0;
+            __syncwarp();
+            sm[lane] = nxt;
+            __syncwarp();
+            if (c + 1 < nchunks) fetch(c + 1, nxt);
+            const int i0 = 1 + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
+            const int cnt = min(LEG_CL, n - i0 + 1);
+            int j = 0;
+            if (!fast) {
                 for (; j + 1 < cnt; j += 2) {
-                    const int i = i0 + j;  // odd degree offset, i+1 even
-                    const double A1 = sm.A[buf][j], A2 = sm.A[buf][j + 1];
-                    const double2 l1 = sm.al[buf][j], l2 = sm.al[buf][j + 1];
+                    const int i = i0 + j;
+                    if (i > ie) break;
+                    const Coef c1 = sm[j], c2 = sm[j + 1];
                     if (i + 1 < is) {
-                        const double T1 = sm.T[buf][j], T2 = sm.T[buf][j + 1];
-                        a2m_step<R, PREFIX, true>(L, A1, T1, l1);
-                        a2m_step<R, PREFIX, false>(L, A2, T2, l2);
-                    } else if (i > ie) {
-                        if (!fast_entered) {
-                            fast_entered = true;
-#pragma unroll
-                            for (int r = 0; r < R; ++r)
-                                if (L.k[r] != 0) L.q0[r] = L.q1[r] = 0.0;  // dead lanes
-                        }
-                        a2m_step<R, FAST, true>(L, A1, 0.0, l1);
-                        a2m_step<R, FAST, false>(L, A2, 0.0, l2);
+                        a2m_step<R, PREFIX, true>(L, c1);
+                        a2m_step<R, PREFIX, false>(L, c2);
                     } else {
-                        const double T1 = sm.T[buf][j], T2 = sm.T[buf][j + 1];
-                        a2m_step<R, CHECKED, true>(L, A1, T1, l1);
-                        a2m_step<R, CHECKED, false>(L, A2, T2, l2);
+                        a2m_step<R, CHECKED, true>(L, c1);
+                        a2m_step<R, CHECKED, false>(L, c2);
                     }
                 }
-                if (j < cnt) {  // trailing odd step (last chunk only)
-                    const int i = i0 + j;
-                    const double A1 = sm.A[buf][j], T1 = sm.T[buf][j];
-                    const double2 l1 = sm.al[buf][j];
-                    if (i > ie && fast_entered)
-                        a2m_step<R, FAST, true>(L, A1, 0.0, l1);
-                    else
-                        a2m_step<R, CHECKED, true>(L, A1, T1, l1);
+                if (j < cnt && i0 + j > ie) {
+                    fast = true;
+                    a2m_enter_fast<R>(L);
                 }
             }
-
-            // publish the prefetched chunk into the other buffer
+            if (fast) {
+                for (; j + 8 <= cnt; j += 8) {
 #pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = threadIdx.x + u * W * 32;
-                if (j < CL && c + 1 < nchunks) {
-                    sm.A[buf ^ 1][j] = pA[u];
-                    sm.T[buf ^ 1][j] = pT[u];
-                    sm.al[buf ^ 1][j] = pal[u];
+                    for (int u = 0; u < 8; u += 2) {
+                        a2m_step<R, FAST, true>(L, sm[j + u]);
+                        a2m_step<R, FAST, false>(L, sm[j + u + 1]);
+                    }
+                }
+                for (; j + 1 < cnt; j += 2) {
+                    a2m_step<R, FAST, true>(L, sm[j]);
+                    a2m_step<R, FAST, false>(L, sm[j + 1]);
                 }
             }
-            __syncthreads();
+            if (j < cnt) {  // trailing odd step (last chunk only)
+                if (fast) a2m_step<R, FAST, true>(L, sm[j]);
+                else a2m_step<R, CHECKED, true>(L, sm[j]);
+            }
         }
 
-        if (has) {
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int s = tile * (32 * R) + r * 32 + lane;
-                if (s >= p.st.n) continue;
-                double2 e = L.ae[r], o = L.ao[r];
-                if (L.k[r] != 0) e = o = make_double2(0.0, 0.0);
-                const int north = p.st.north[s], south = p.st.south[s];
-                delta[row_off[north] + mi] = cadd(e, o);
-                if (south >= 0) delta[row_off[south] + mi] = csub(e, o);
-            }
+        for (int r = 0; r < R; ++r) {
+            const int s = tile * (32 * R) + r * 32 + lane;
+            if (s >= p.st.n) continue;
+            double2 e = L.ae[r], o = L.ao[r];
+            if (L.k[r] != 0) e = o = make_double2(0.0, 0.0);
+            const int north = p.st.north[s], south = p.st.south[s];
+            delta[row_off[north] + mi] = cadd(e, o);
+            if (south >= 0) delta[row_off[south] + mi] = csub(e, o);
         }
     }
 }
@@ -396,16 +383,34 @@ __global__ void leg_zero_dead_kernel(LegPlanView p, double2* __restrict__ delta,
     if (south >= 0) delta[row_off[south] + mi] = z;
 }
 
+int leg_persistent_blocks(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_alm2map_kernel<LEG_R>, LEG_WARPS * 32, 0);
+    const int v = sms * (per > 0 ? per : 1);
+    if (device >= 0 && device < 64) cached[device] = v;
+    return v;
+}
+
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
-                        const int64_t* row_off, cudaStream_t s) {
+                        const int64_t* row_off, int* counters, cudaStream_t s) {
     if (p.n_m == 0) return;
     dim3 zg((p.st.n + 127) / 128, p.n_m);
     leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off);
-    leg_alm2map_kernel<LEG_R, LEG_W, 64><<<p.n_m, LEG_W * 32, 0, s>>>(p, alm, delta, row_off);
+    if (p.n_a2m_items == 0) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int blocks = leg_persistent_blocks(dev);
+    const int need = (p.n_a2m_items + LEG_WARPS - 1) / LEG_WARPS;
+    if (need < blocks) blocks = need;
+    cudaMemsetAsync(counters, 0, sizeof(int), s);
+    leg_alm2map_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, alm, delta, row_off, counters);
 }
 
 // ---------------------------------------------------------------------------------------
-// map2alm: a_lm = sum_r Delta^S_m(r) P_lm(x_r), mirror paired
+// map2alm: a_lm = c_l sum_r Delta^S_m(r) Q_lm(x_r), mirror paired
 // ---------------------------------------------------------------------------------------
 namespace {
 
@@ -416,40 +421,37 @@ struct M2ALane {
     int k[R];
 };
 
-template <int R>
-__device__ __forceinline__ void m2a_load_d(M2ALane<R>& L, int r, int s, const LegPlanView& p,
+__device__ __forceinline__ void m2a_load_d(double2& ds, double2& dd, int s, const LegPlanView& p,
                                            const double2* __restrict__ delta,
                                            const int64_t* __restrict__ row_off, int mi) {
     const double2 dn = delta[row_off[p.st.north[s]] + mi];
     const int south = p.st.south[s];
     if (south >= 0) {
-        const double2 dsouth = delta[row_off[south] + mi];
-        L.ds[r] = cadd(dn, dsouth);
-        L.dd[r] = csub(dn, dsouth);
+        const double2 dso = delta[row_off[south] + mi];
+        ds = cadd(dn, dso);
+        dd = csub(dn, dso);
     } else {
-        L.ds[r] = dn;  // self-paired / unpaired row: alm_accumulate with dn (transforms.cpp:200-201)
-        L.dd[r] = dn;
+        ds = dn;  // self-paired / unpaired row: alm_accumulate with dn (transforms.cpp:200-201)
+        dd = dn;
     }
 }
 
 // One step; returns the lane's contribution (re, im) summed over its R streams.
 template <int R, int PH, bool ODD>
-__device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, double A, double T, const LegPlanView& p,
+__device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, const Coef& cf, const LegPlanView& p,
                                             const double2* __restrict__ delta,
                                             const int64_t* __restrict__ row_off, int mi,
                                             int tile, int lane) {
     double2 part = make_double2(0.0, 0.0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
+        double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
         if (PH != FAST) {
-            if (fabs(q2) >= T) {
+            if (fabs(q2) >= cf.T) {
                 q2 *= SCALE_DOWN;
                 L.q1[r] *= SCALE_DOWN;
-                if (++L.k[r] == 0) {
-                    const int s = tile * (32 * R) + r * 32 + lane;
-                    m2a_load_d<R>(L, r, s, p, delta, row_off, mi);
-                }
+                if (++L.k[r] == 0)
+                    m2a_load_d(L.ds[r], L.dd[r], tile * (32 * R) + r * 32 + lane, p, delta, row_off, mi);
             }
         }
         if (PH != PREFIX) {
@@ -463,238 +465,217 @@ __device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, double A, double T, c
     return part;
 }
 
-template <int W, int CL>
-struct M2AStage {
-    double A[2][CL];
-    double T[2][CL];
-    double C[2][CL];
-    double red[W][32][17];      // per-warp lane transpose
-    double res[2][W][CL][2];    // per-warp reduced chunk results
+template <int R>
+__device__ __forceinline__ void m2a_enter_fast(M2ALane<R>& L) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (L.k[r] != 0) {
+            L.q0[r] = L.q1[r] = 0.0;
+            L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
+        }
+}
+
+struct M2AWarpSmem {
+    Coef cf[LEG_CL];
+    double red[32][17];  // lane transpose for the 16-value reduction
 };
 
 }  // namespace
 
-template <int R, int W, int CL>
-__global__ void __launch_bounds__(W * 32)
+template <int R>
+__global__ void __launch_bounds__(LEG_WARPS * 32, 3)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
-                       int accumulate) {
-    static_assert(CL % 8 == 0, "chunk must hold whole 8-step reduction groups");
-    extern __shared__ __align__(16) unsigned char smraw[];
-    M2AStage<W, CL>& sm = *reinterpret_cast<M2AStage<W, CL>*>(smraw);
-    const int mi = p.m_order[blockIdx.x];
-    const int m = p.ms[mi];
-    const int n = p.lmax - m;
+                       int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
+    static_assert(LEG_CL % 8 == 0, "chunk must hold whole 8-step reduction groups");
+    __shared__ M2AWarpSmem sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t toff = p.tab.tab_off[mi];
-    const double* __restrict__ gA = p.tab.A + toff;
-    const double* __restrict__ gC = p.tab.C + toff;
-    const double* __restrict__ gT = p.tab.T + toff;
-    double2* __restrict__ out = alm + alm_offset(m, p.lmax);
-    const int tbeg = p.tile_list_off[mi], tcnt = p.tile_list_cnt[mi];
-    const double lmu = p.log_mu[m];
-    const int nchunks = (n + 1 + CL - 1) / CL;  // steps i = 0..n
+    M2AWarpSmem& sm = sm_all[warp];
+    int* m_done = counters + 1;
 
-    if (tcnt == 0) {  // every stream of this order is dropped: a_lm = 0 (or unchanged)
-        if (!accumulate)
-            for (int i = threadIdx.x; i <= n; i += W * 32) out[i] = make_double2(0.0, 0.0);
-        return;
-    }
+    for (;;) {
+        const int it = warp_next_item(counters);
+        if (it >= p.n_m2a_items) return;
+        const LegItem item = p.m2a_items[it];
+        const int mi = item.mi;
+        const int m = p.ms[mi];
+        const int n = p.lmax - m;
+        const int64_t toff = p.tab.tab_off[mi];
+        const double* __restrict__ gA = p.tab.A + toff;
+        const double* __restrict__ gT = p.tab.T + toff;
+        const double lmu = p.log_mu[m];
+        double2* __restrict__ part_out = scratch + p.m2a_slot_base[mi] + (int64_t)item.g * (n + 1);
+        const int nchunks = (n + 1 + LEG_CL - 1) / LEG_CL;  // degree offsets 0..n
 
-    for (int r0 = 0; r0 < tcnt; r0 += W) {
-        const bool first_round = (r0 == 0);
-        const int ti = r0 + warp;
-        const bool has = ti < tcnt;
-        const int tile = has ? p.tile_list[tbeg + ti] : 0;
-        const int2 info = has ? p.tile_info[(size_t)mi * p.n_tiles + tile] : make_int2(INT_MAX, -1);
-        const int is = info.x, ie = info.y;
-
-        M2ALane<R> L;
+        for (int tt = 0; tt < item.b; ++tt) {
+            const int tile = p.tile_list[item.a + tt];
+            const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
+            const int is = info.x, ie = info.y;
+            M2ALane<R> L;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int s = tile * (32 * R) + r * 32 + lane;
-            const bool valid = has && s < p.st.n;
-            double mant = 0.0, x = 0.0;
-            int k = 1;  // invalid lanes: never active
-            if (valid) {
-                x = p.st.x[s];
-                seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
-            }
-            L.x[r] = x;
-            L.q0[r] = 0.0;
-            L.q1[r] = valid ? mant : 0.0;
-            L.k[r] = k;
-            L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-            if (valid && k == 0) m2a_load_d<R>(L, r, s, p, delta, row_off, mi);
-        }
-        bool fast_entered = false;
-
-        // stage chunk 0 (degree offsets 0..CL-1)
-        for (int j = threadIdx.x; j < CL; j += W * 32) {
-            const bool in = j <= n;
-            sm.A[0][j] = in ? gA[j] : 0.0;
-            sm.T[0][j] = in ? gT[j] : 0x1p1000;
-            sm.C[0][j] = in ? gC[j] : 0.0;
-        }
-        __syncthreads();
-
-        for (int c = 0; c < nchunks; ++c) {
-            const int buf = c & 1;
-            constexpr int PER = (CL + W * 32 - 1) / (W * 32);
-            double pA[PER], pT[PER], pC[PER];
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = threadIdx.x + u * W * 32;
-                const int i = (c + 1) * CL + j;
-                const bool in = j < CL && i <= n;
-                pA[u] = in ? gA[i] : 0.0;
-                pT[u] = in ? gT[i] : 0x1p1000;
-                pC[u] = in ? gC[i] : 0.0;
-            }
-            // reduce the previous chunk's per-warp results (fixed warp order) into a_lm
-            if (c > 0) {
-                for (int t = threadIdx.x; t < 2 * CL; t += W * 32) {
-                    const int j = t >> 1, comp = t & 1;
-                    const int i = (c - 1) * CL + j;
-                    if (i <= n) {
-                        double v = 0.0;
-#pragma unroll
-                        for (int w = 0; w < W; ++w) v += sm.res[buf ^ 1][w][j][comp];
-                        v *= sm.C[buf ^ 1][j];
-                        double* o = reinterpret_cast<double*>(out + i) + comp;
-                        *o = (first_round && !accumulate) ? v : *o + v;
-                    }
+            for (int r = 0; r < R; ++r) {
+                const int s = tile * (32 * R) + r * 32 + lane;
+                const bool valid = s < p.st.n;
+                double mant = 0.0, x = 0.0;
+                int k = 1;  // invalid lanes: never active
+                if (valid) {
+                    x = p.st.x[s];
+                    seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
                 }
+                L.x[r] = x;
+                L.q0[r] = 0.0;
+                L.q1[r] = valid ? mant : 0.0;
+                L.k[r] = k;
+                L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
+                if (valid && k == 0) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
             }
+            bool fast = false;
 
-            const int i0 = c * CL;
-            const int cnt = min(CL, n - i0 + 1);
-            for (int g = 0; g < CL; g += 8) {
-                double part[16];
-#pragma unroll
-                for (int u = 0; u < 16; ++u) part[u] = 0.0;
-                bool any = false;
-                if (has && g < cnt) {
-#pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
-                        const int j = g + u;
-                        if (j >= cnt) break;
-                        const int i = i0 + j;  // even degree offset
-                        const double A1 = sm.A[buf][j], T1 = sm.T[buf][j];
-                        const bool two = j + 1 < cnt;
-                        const double A2 = two ? sm.A[buf][j + 1] : 0.0;
-                        const double T2 = two ? sm.T[buf][j + 1] : 0x1p1000;
-                        double2 c1 = make_double2(0.0, 0.0), c2 = make_double2(0.0, 0.0);
-                        if (i == 0) {
-                            // seed term (degree offset 0): no recurrence step
-#pragma unroll
-                            for (int r = 0; r < R; ++r) {
-                                c1.x = __fma_rn(L.ds[r].x, L.q1[r], c1.x);
-                                c1.y = __fma_rn(L.ds[r].y, L.q1[r], c1.y);
-                            }
-                            any = true;
-                            if (two) {
-                                if (1 > ie && !fast_entered) {
-                                    fast_entered = true;
-#pragma unroll
-                                    for (int r = 0; r < R; ++r)
-                                        if (L.k[r] != 0) {
-                                            L.q0[r] = L.q1[r] = 0.0;
-                                            L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-                                        }
-                                }
-                                if (fast_entered)
-                                    c2 = m2a_step<R, FAST, true>(L, A2, T2, p, delta, row_off, mi, tile, lane);
-                                else
-                                    c2 = m2a_step<R, CHECKED, true>(L, A2, T2, p, delta, row_off, mi, tile, lane);
-                            }
-                        } else if (i + 1 < is) {
-                            m2a_step<R, PREFIX, false>(L, A1, T1, p, delta, row_off, mi, tile, lane);
-                            if (two) m2a_step<R, PREFIX, true>(L, A2, T2, p, delta, row_off, mi, tile, lane);
-                        } else if (i > ie) {
-                            if (!fast_entered) {
-                                fast_entered = true;
-#pragma unroll
-                                for (int r = 0; r < R; ++r)
-                                    if (L.k[r] != 0) {
-                                        L.q0[r] = L.q1[r] = 0.0;
-                                        L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-                                    }
-                            }
-                            any = true;
-                            c1 = m2a_step<R, FAST, false>(L, A1, T1, p, delta, row_off, mi, tile, lane);
-                            if (two) c2 = m2a_step<R, FAST, true>(L, A2, T2, p, delta, row_off, mi, tile, lane);
-                        } else {
-                            any = true;
-                            c1 = m2a_step<R, CHECKED, false>(L, A1, T1, p, delta, row_off, mi, tile, lane);
-                            if (two) c2 = m2a_step<R, CHECKED, true>(L, A2, T2, p, delta, row_off, mi, tile, lane);
-                        }
-                        part[2 * u + 0] = c1.x;
-                        part[2 * u + 1] = c1.y;
-                        part[2 * u + 2] = c2.x;
-                        part[2 * u + 3] = c2.y;
-                    }
-                }
-                // reduce the 16 values over the 32 lanes of the warp (fixed order)
-                double v = 0.0;
-                if (__any_sync(0xffffffffu, any)) {
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) sm.red[warp][lane][u] = part[u];
-                    __syncwarp();
-                    const int col = lane & 15, half = lane >> 4;
-#pragma unroll
-                    for (int row = 0; row < 16; ++row) v += sm.red[warp][half * 16 + row][col];
-                    v += __shfl_xor_sync(0xffffffffu, v, 16);
-                    __syncwarp();
-                }
-                if (lane < 16) sm.res[buf][warp][g + (lane >> 1)][lane & 1] = v;
-            }
-
-#pragma unroll
-            for (int u = 0; u < PER; ++u) {
-                const int j = threadIdx.x + u * W * 32;
-                if (j < CL && c + 1 < nchunks) {
-                    sm.A[buf ^ 1][j] = pA[u];
-                    sm.T[buf ^ 1][j] = pT[u];
-                    sm.C[buf ^ 1][j] = pC[u];
-                }
-            }
-            __syncthreads();
-        }
-        // reduce the final chunk
-        {
-            const int c = nchunks;
-            const int buf = c & 1;
-            for (int t = threadIdx.x; t < 2 * CL; t += W * 32) {
-                const int j = t >> 1, comp = t & 1;
-                const int i = (c - 1) * CL + j;
+            auto fetch = [&](int c, Coef& cf) {
+                const int i = c * LEG_CL + lane;
                 if (i <= n) {
-                    double v = 0.0;
+                    cf.A = gA[i];
+                    cf.T = gT[i];
+                } else {
+                    cf.A = 0.0;
+                    cf.T = 0x1p1000;
+                }
+                cf.ar = cf.ai = 0.0;
+            };
+            Coef nxt;
+            fetch(0, nxt);
+            for (int c = 0; c < nchunks; ++c) {
+                __syncwarp();
+                sm.cf[lane] = nxt;
+                __syncwarp();
+                if (c + 1 < nchunks) fetch(c + 1, nxt);
+                const int i0 = c * LEG_CL;
+                const int cnt = min(LEG_CL, n - i0 + 1);
+                for (int g = 0; g < cnt; g += 8) {
+                    const int gc = min(8, cnt - g);
+                    const int ig = i0 + g;  // even degree offset
+                    double part[16];
 #pragma unroll
-                    for (int w = 0; w < W; ++w) v += sm.res[buf ^ 1][w][j][comp];
-                    v *= sm.C[buf ^ 1][j];
-                    double* o = reinterpret_cast<double*>(out + i) + comp;
-                    *o = (first_round && !accumulate) ? v : *o + v;
+                    for (int u = 0; u < 16; ++u) part[u] = 0.0;
+                    bool any = true;
+                    if (!fast && ig > ie && ig > 0) {
+                        fast = true;
+                        m2a_enter_fast<R>(L);
+                    }
+                    if (fast && gc == 8) {
+                        // straight-line 8 steps, no checks
+#pragma unroll
+                        for (int u = 0; u < 8; u += 2) {
+                            const double2 v1 = m2a_step<R, FAST, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                            const double2 v2 = m2a_step<R, FAST, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                            part[2 * u + 0] = v1.x;
+                            part[2 * u + 1] = v1.y;
+                            part[2 * u + 2] = v2.x;
+                            part[2 * u + 3] = v2.y;
+                        }
+                    } else if (ig > 0 && ig + gc < is) {
+                        // whole group before the tile's first activation: recurrence only
+                        any = false;
+                        for (int u = 0; u < gc; u += 2) {
+                            m2a_step<R, PREFIX, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                            if (u + 1 < gc)
+                                m2a_step<R, PREFIX, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                        }
+                    } else {
+                        // generic (checked) path: activation window, the seed group, partial groups
+#pragma unroll
+                        for (int u = 0; u < 8; u += 2) {
+                            if (u < gc) {
+                                double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+                                if (ig + u == 0) {
+                                    // seed term (degree offset 0): no recurrence step
+#pragma unroll
+                                    for (int r = 0; r < R; ++r) {
+                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
+                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
+                                    }
+                                } else {
+                                    v1 = m2a_step<R, CHECKED, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                                }
+                                if (u + 1 < gc)
+                                    v2 = m2a_step<R, CHECKED, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                                part[2 * u + 0] = v1.x;
+                                part[2 * u + 1] = v1.y;
+                                part[2 * u + 2] = v2.x;
+                                part[2 * u + 3] = v2.y;
+                            }
+                        }
+                    }
+                    // reduce the 16 values over the 32 lanes (fixed order), accumulate the
+                    // warp's partial sums for degree offsets i0+g .. i0+g+7 in its scratch slot
+                    double v = 0.0;
+                    if (any) {
+#pragma unroll
+                        for (int u = 0; u < 16; ++u) sm.red[lane][u] = part[u];
+                        __syncwarp();
+                        const int col = lane & 15, half = lane >> 4;
+#pragma unroll
+                        for (int row = 0; row < 16; ++row) v += sm.red[half * 16 + row][col];
+                        v += __shfl_xor_sync(0xffffffffu, v, 16);
+                        __syncwarp();
+                    }
+                    const int i = i0 + g + (lane >> 1);
+                    if (lane < 16 && i <= n) {
+                        double* o = reinterpret_cast<double*>(part_out + i) + (lane & 1);
+                        *o = (tt == 0) ? v : *o + v;
+                    }
                 }
             }
         }
-        __syncthreads();
+
+        // last item of this order to finish reduces the order's partial slots (fixed order)
+        __threadfence();
+        int last = 0;
+        if (lane == 0) last = (atomicAdd(m_done + mi, 1) == p.m2a_items_per_m[mi] - 1);
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+            __threadfence();
+            const double* __restrict__ gC = p.tab.C + toff;
+            const int G = p.m2a_items_per_m[mi];
+            const double2* base = scratch + p.m2a_slot_base[mi];
+            double2* out = alm + alm_offset(m, p.lmax);
+            for (int i = lane; i <= n; i += 32) {
+                double2 v = make_double2(0.0, 0.0);
+                for (int g = 0; g < G; ++g) v = cadd(v, __ldcg(base + (int64_t)g * (n + 1) + i));
+                const double c = gC[i];
+                v = make_double2(v.x * c, v.y * c);
+                out[i] = accumulate ? cadd(out[i], v) : v;
+            }
+        }
     }
 }
 
+// orders without any alive tile: every term is dropped, a_lm = 0 (or unchanged when +=)
+__global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm) {
+    const int mi = blockIdx.x;
+    if (p.m2a_items_per_m[mi] > 0) return;
+    const int m = p.ms[mi];
+    double2* out = alm + alm_offset(m, p.lmax);
+    for (int i = threadIdx.x; i <= p.lmax - m; i += blockDim.x) out[i] = make_double2(0.0, 0.0);
+}
+
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
-                        double2* alm, int accumulate, cudaStream_t s) {
+                        double2* alm, int accumulate, int* counters, double2* scratch,
+                        cudaStream_t s) {
     if (p.n_m == 0) return;
-    constexpr int CL = 64;
-    const size_t smem = sizeof(M2AStage<LEG_W, CL>);
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(leg_map2alm_kernel<LEG_R, LEG_W, CL>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
-    leg_map2alm_kernel<LEG_R, LEG_W, CL><<<p.n_m, LEG_W * 32, smem, s>>>(p, delta, row_off, alm,
-                                                                         accumulate);
+    if (!accumulate) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
+    if (p.n_m2a_items == 0) return;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_map2alm_kernel<LEG_R>, LEG_WARPS * 32, 0);
+    int blocks = sms * (per > 0 ? per : 1);
+    const int need = (p.n_m2a_items + LEG_WARPS - 1) / LEG_WARPS;
+    if (need < blocks) blocks = need;
+    cudaMemsetAsync(counters, 0, sizeof(int) * (1 + p.n_m), s);
+    leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, alm, accumulate,
+                                                                counters, scratch);
 }
 
 }  // namespace shtk

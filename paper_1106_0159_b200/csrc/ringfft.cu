@@ -107,26 +107,43 @@ __device__ __forceinline__ void dft(double2 (&v)[R], int sign) {
     }
 }
 
+// b / Ns and b % Ns for b < 2^24 through a float reciprocal (exact after one correction).
+__device__ __forceinline__ void divmod_small(int b, int Ns, float inv, int& q, int& r) {
+    q = __float2int_rz(__int2float_rn(b) * inv);
+    r = b - q * Ns;
+    if (r >= Ns) { ++q; r -= Ns; }
+    if (r < 0) { --q; r += Ns; }
+}
+
 // One in-place Stockham pass (register staged): all inputs of the pass are read into
 // registers, then the CTA synchronises and writes the outputs.
+// e^{-2 pi i k / B} = lo[k & 63] * hi[k >> 6] from exact table entries (shared memory)
+struct TwTab {
+    const double2* lo;
+    const double2* hi;
+    __device__ __forceinline__ double2 at(int k) const { return cmul(lo[k & 63], hi[k >> 6]); }
+};
+
 template <int R, int T, int BMAX>
 __device__ __forceinline__ void stockham_pass(double2* buf, int B, int Ns, int sign,
-                                              const double2* __restrict__ tw) {
+                                              const TwTab& tw) {
     constexpr int Q = (BMAX + R * T - 1) / (R * T);
     const int nb = B / R;
     const int tstride = B / (Ns * R);
+    const float inv = 1.0f / (float)Ns;
     double2 v[Q][R];
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
         const int b = threadIdx.x + q * T;
         if (b < nb) {
-            const int k = b % Ns;
 #pragma unroll
             for (int r = 0; r < R; ++r) v[q][r] = buf[b + r * nb];
             if (Ns > 1) {
+                int bq, k;
+                divmod_small(b, Ns, inv, bq, k);
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    double2 w = __ldg(&tw[r * k * tstride]);
+                    double2 w = tw.at(r * k * tstride);
                     if (sign > 0) w.y = -w.y;
                     v[q][r] = cmul(v[q][r], w);
                 }
@@ -139,8 +156,9 @@ __device__ __forceinline__ void stockham_pass(double2* buf, int B, int Ns, int s
     for (int q = 0; q < Q; ++q) {
         const int b = threadIdx.x + q * T;
         if (b < nb) {
-            const int k = b % Ns;
-            const int base = (b / Ns) * Ns * R + k;
+            int bq, k;
+            divmod_small(b, Ns, inv, bq, k);
+            const int base = bq * Ns * R + k;
 #pragma unroll
             for (int r = 0; r < R; ++r) buf[base + r * Ns] = v[q][r];
         }
@@ -149,85 +167,129 @@ __device__ __forceinline__ void stockham_pass(double2* buf, int B, int Ns, int s
 }
 
 template <int T, int BMAX>
-__device__ void fft_run(double2* buf, const RingDesc& d, int B, int sign,
-                        const double2* __restrict__ tw) {
+__device__ __forceinline__ void fft_run(double2* buf, int npass, unsigned long long radices, int B,
+                                     int sign, const TwTab& tw) {
     int Ns = 1;
-    for (int pidx = 0; pidx < d.npass; ++pidx) {
-        const int R = d.radix[pidx];
+    for (int pidx = 0; pidx < npass; ++pidx) {
+        const int R = (int)((radices >> (4 * pidx)) & 0xF);
         switch (R) {
             case 8: stockham_pass<8, T, BMAX>(buf, B, Ns, sign, tw); break;
             case 4: stockham_pass<4, T, BMAX>(buf, B, Ns, sign, tw); break;
             case 2: stockham_pass<2, T, BMAX>(buf, B, Ns, sign, tw); break;
-            case 3: stockham_pass<3, T, BMAX>(buf, B, Ns, sign, tw); break;
-            case 5: stockham_pass<5, T, BMAX>(buf, B, Ns, sign, tw); break;
-            case 7: stockham_pass<7, T, BMAX>(buf, B, Ns, sign, tw); break;
-            default: break;
+            default:
+                // odd radices only in the small classes (register budget of the in-place
+                // staging); the planner sends larger non-power-of-two lengths to Bluestein
+                if constexpr (BMAX <= 1024) {
+                    if (R == 3) stockham_pass<3, T, BMAX>(buf, B, Ns, sign, tw);
+                    else if (R == 5) stockham_pass<5, T, BMAX>(buf, B, Ns, sign, tw);
+                    else if (R == 7) stockham_pass<7, T, BMAX>(buf, B, Ns, sign, tw);
+                }
+                break;
         }
         Ns *= R;
     }
 }
 
-// Length-N DFT (sign) of buf[0..N) in place; Bluestein rings use the whole B-length buffer.
+// Length-N DFT (sign) of buf[0..N) in place; Bluestein rings use the whole B-length buffer
+// (chirp, forward FFT_B, multiply by FFT_B(conj chirp), inverse FFT_B, chirp / B).
+// Stage the two-level twiddle table of length B (64 + B/64 entries) into twsm.
+template <int T>
+__device__ __forceinline__ TwTab stage_twiddles(double2* twsm, const double2* __restrict__ tw, int B) {
+    const int nhi = (B + 63) >> 6;
+    for (int j = threadIdx.x; j < 64 + nhi; j += T) {
+        if (j < 64) twsm[j] = (j < B) ? __ldg(&tw[j]) : make_double2(1.0, 0.0);
+        else twsm[j] = __ldg(&tw[(j - 64) << 6]);
+    }
+    return TwTab{twsm, twsm + 64};
+}
+
 template <int T, int BMAX>
 __device__ void ring_dft(double2* buf, const RingDesc& d, int sign,
-                         const double2* __restrict__ tabs) {
-    const double2* __restrict__ tw = tabs + d.tw_off;
-    if (!(d.flags & 2)) {
-        fft_run<T, BMAX>(buf, d, d.B, sign, tw);
-        return;
-    }
+                         const double2* __restrict__ tabs, double2* twsm) {
+    const TwTab tw = stage_twiddles<T>(twsm, tabs + d.tw_off, d.B);  // published by a barrier below
+    const bool blue = d.flags & 2;
     const int N = d.N, M = d.B;
     const double2* __restrict__ chirp = tabs + d.chirp_off;
     const double2* __restrict__ H = tabs + d.h_off;
-    for (int j = threadIdx.x; j < M; j += T) {
-        if (j < N) {
-            double2 c = __ldg(&chirp[j]);
-            if (sign > 0) c.y = -c.y;
-            buf[j] = cmul(buf[j], c);
-        } else {
-            buf[j] = make_double2(0.0, 0.0);
+    if (blue) {
+        for (int j = threadIdx.x; j < M; j += T) {
+            if (j < N) {
+                double2 c = __ldg(&chirp[j]);
+                if (sign > 0) c.y = -c.y;
+                buf[j] = cmul(buf[j], c);
+            } else {
+                buf[j] = make_double2(0.0, 0.0);
+            }
+        }
+        __syncthreads();
+    }
+    if (!blue) __syncthreads();
+    const int nrun = blue ? 2 : 1;
+    for (int run = 0; run < nrun; ++run) {
+        const int sg = blue ? (run == 0 ? -1 : +1) : sign;
+        fft_run<T, BMAX>(buf, d.npass, d.radices, M, sg, tw);
+        if (blue && run == 0) {
+            for (int j = threadIdx.x; j < M; j += T) {
+                double2 h = __ldg(&H[j]);
+                if (sign > 0) h.y = -h.y;
+                buf[j] = cmul(buf[j], h);
+            }
+            __syncthreads();
         }
     }
-    __syncthreads();
-    fft_run<T, BMAX>(buf, d, M, -1, tw);
-    for (int j = threadIdx.x; j < M; j += T) {
-        double2 h = __ldg(&H[j]);
-        if (sign > 0) h.y = -h.y;
-        buf[j] = cmul(buf[j], h);
+    if (blue) {
+        const double inv = 1.0 / (double)M;
+        for (int j = threadIdx.x; j < N; j += T) {
+            double2 c = __ldg(&chirp[j]);
+            if (sign > 0) c.y = -c.y;
+            buf[j] = cscale(cmul(buf[j], c), inv);
+        }
+        __syncthreads();
     }
-    __syncthreads();
-    fft_run<T, BMAX>(buf, d, M, +1, tw);
-    const double inv = 1.0 / (double)M;
-    for (int j = threadIdx.x; j < N; j += T) {
-        double2 c = __ldg(&chirp[j]);
-        if (sign > 0) c.y = -c.y;
-        buf[j] = cscale(cmul(buf[j], c), inv);
-    }
-    __syncthreads();
 }
 
+// e^{i m phi0} = lo[m & 63] * hi[m >> 6]: 64 + (mmax+1)/64 sincos per ring instead of one per
+// order (ring_synthesis_into evaluates polar(1, m*phi0) per order, fourier.cpp:13).
+struct PhaseTab {
+    const double2* lo;
+    const double2* hi;
+    __device__ __forceinline__ double2 at(int m) const { return cmul(lo[m & 63], hi[m >> 6]); }
+};
+
+__device__ __forceinline__ void build_phase(double2* lo, double2* hi, int nhi, double phi0, int T) {
+    for (int j = threadIdx.x; j < 64 + nhi; j += T) {
+        double s, c;
+        if (j < 64) {
+            sincos((double)j * phi0, &s, &c);
+            lo[j] = make_double2(c, s);
+        } else {
+            sincos((double)((j - 64) * 64) * phi0, &s, &c);
+            hi[j - 64] = make_double2(c, s);
+        }
+    }
+}
+
+__device__ __forceinline__ int64_t delta_index(const RingStageArgs& a, int pos, int m) {
+    return a.m_base ? a.m_base[m] + (int64_t)pos * a.m_stride[m] : (int64_t)m + (int64_t)pos * a.ld;
+}
 __device__ __forceinline__ double2 delta_at(const RingStageArgs& a, int pos, int m) {
-    return a.delta_in[a.m_base[m] + (int64_t)pos * a.m_stride[m]];
+    return a.delta_in[delta_index(a, pos, m)];
 }
 
 // v_m = Delta_m e^{i m phi0} as in ring_synthesis_into (fourier.cpp:11-14); m==0 keeps Re only.
 __device__ __forceinline__ double2 folded_value(const RingStageArgs& a, int pos, int m,
-                                                double phi0) {
+                                                bool rot, const PhaseTab& ph) {
     double2 v = delta_at(a, pos, m);
     if (m == 0) return make_double2(v.x, 0.0);
-    if (phi0 != 0.0) {
-        double s, c;
-        sincos((double)m * phi0, &s, &c);
-        v = cmul(v, make_double2(c, s));
-    }
+    if (rot) v = cmul(v, ph.at(m));
     return v;
 }
 
 // Fold sums of bin pair p over the wraps w = g, g+G, ... (ring_synthesis_into's bins,
 // fourier.cpp:17-25): H_p = sum_{m = p mod n} v_m + sum_{m = -p mod n, m >= 1} conj v_m.
 __device__ __forceinline__ void fold_pair(const RingStageArgs& a, int pos, int p, int g, int G,
-                                          int n, int N, bool half, int mmax, double phi0,
-                                          double2& hp, double2& hq) {
+                                          int n, int N, bool half, int mmax, bool rot,
+                                          const PhaseTab& ph, double2& hp, double2& hq) {
     hp = make_double2(0.0, 0.0);
     hq = make_double2(0.0, 0.0);
     const int q = half ? N - p : -1;
@@ -236,19 +298,19 @@ __device__ __forceinline__ void fold_pair(const RingStageArgs& a, int pos, int p
         if (base > mmax) break;
         if (p == 0) {
             // bin 0 (and bin N in half mode): the conjugate lands on the same bin -> 2 Re
-            const double2 v = folded_value(a, pos, base, phi0);
+            const double2 v = folded_value(a, pos, base, rot, ph);
             hp.x += (base == 0) ? v.x : 2.0 * v.x;
-            if (half && base + N <= mmax) hq.x += 2.0 * folded_value(a, pos, base + N, phi0).x;
+            if (half && base + N <= mmax) hq.x += 2.0 * folded_value(a, pos, base + N, rot, ph).x;
         } else {
             int m = base + p;
-            if (m <= mmax) hp = cadd(hp, folded_value(a, pos, m, phi0));
+            if (m <= mmax) hp = cadd(hp, folded_value(a, pos, m, rot, ph));
             m = base + n - p;
-            if (m <= mmax) hp = cadd(hp, cconj(folded_value(a, pos, m, phi0)));
+            if (m <= mmax) hp = cadd(hp, cconj(folded_value(a, pos, m, rot, ph)));
             if (half && q != p) {
                 m = base + q;  // H_q: bin q (v) and bin n - q = N + p (conj v)
-                if (m <= mmax) hq = cadd(hq, folded_value(a, pos, m, phi0));
+                if (m <= mmax) hq = cadd(hq, folded_value(a, pos, m, rot, ph));
                 m = base + N + p;
-                if (m <= mmax) hq = cadd(hq, cconj(folded_value(a, pos, m, phi0)));
+                if (m <= mmax) hq = cadd(hq, cconj(folded_value(a, pos, m, rot, ph)));
             }
         }
     }
@@ -283,14 +345,22 @@ __device__ __forceinline__ void store_z(double2* buf, const double2* __restrict_
 // synthesis: Delta rows -> ring samples
 // ---------------------------------------------------------------------------------------
 template <int T, int BMAX>
-__global__ void __launch_bounds__(T, 1) ring_synth_kernel(RingStageArgs a) {
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) ring_synth_kernel(RingStageArgs a) {
     extern __shared__ __align__(16) double2 smem[];
-    double2* buf = smem;          // BMAX
-    double2* red = smem + BMAX;   // 2T fold partials
+    double2* buf = smem;               // BMAX
+    double2* red = smem + BMAX;        // 2T fold partials
+    double2* twsm = red + 2 * T;       // 64 + BMAX/64 twiddles
+    double2* phlo = twsm + 64 + (BMAX >> 6);  // 64 + (mmax >> 6) + 1 phase factors
     const RingDesc d = a.rings[blockIdx.x];
     const int n = d.n, N = d.N, pos = d.ring_pos, mmax = a.mmax;
     const bool half = d.flags & 1;
     const double phi0 = d.phi0;
+    const bool rot = phi0 != 0.0;
+    const PhaseTab ph{phlo, phlo + 64};
+    if (rot) {
+        build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+        __syncthreads();
+    }
 
     // ---- fold Delta into the Hermitian half spectrum H_k (k = 0..n/2) ----
     // half mode: bin pair p handles H_p and H_{N-p}; full mode: H_p only.  When the pairs fit
@@ -304,7 +374,7 @@ __global__ void __launch_bounds__(T, 1) ring_synth_kernel(RingStageArgs a) {
         if (t < G * np) {
             const int g = t / np, p = t - g * np;
             double2 hp, hq;
-            fold_pair(a, pos, p, g, G, n, N, half, mmax, phi0, hp, hq);
+            fold_pair(a, pos, p, g, G, n, N, half, mmax, rot, ph, hp, hq);
             red[2 * t] = hp;
             red[2 * t + 1] = hq;
         }
@@ -320,13 +390,13 @@ __global__ void __launch_bounds__(T, 1) ring_synth_kernel(RingStageArgs a) {
     } else {
         for (int p = t; p < np; p += T) {
             double2 Hp, Hq;
-            fold_pair(a, pos, p, 0, 1, n, N, half, mmax, phi0, Hp, Hq);
+            fold_pair(a, pos, p, 0, 1, n, N, half, mmax, rot, ph, Hp, Hq);
             store_z(buf, hw, p, Hp, Hq, n, N, half);
         }
     }
     __syncthreads();
 
-    ring_dft<T, BMAX>(buf, d, +1, a.tabs);
+    ring_dft<T, BMAX>(buf, d, +1, a.tabs, twsm);
 
     double* __restrict__ out = a.map_out + d.pix_off;
     if (half) {
@@ -344,16 +414,21 @@ __global__ void __launch_bounds__(T, 1) ring_synth_kernel(RingStageArgs a) {
 // analysis: ring samples -> Delta^S rows
 // ---------------------------------------------------------------------------------------
 template <int T, int BMAX>
-__global__ void __launch_bounds__(T, 1) ring_anal_kernel(RingStageArgs a) {
+__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) ring_anal_kernel(RingStageArgs a) {
     extern __shared__ __align__(16) double2 smem[];
     double2* buf = smem;
     double2* red = smem + BMAX;
+    double2* twsm = red + 2 * T;
+    double2* phlo = twsm + 64 + (BMAX >> 6);
     const RingDesc d = a.rings[blockIdx.x];
     const int n = d.n, N = d.N, pos = d.ring_pos, mmax = a.mmax;
     const bool half = d.flags & 1;
     const double phi0 = d.phi0, wgt = d.weight;
+    const bool rot = phi0 != 0.0;
+    const PhaseTab ph{phlo, phlo + 64};
     const double* __restrict__ in = a.map_in + d.pix_off;
     const int t = threadIdx.x;
+    if (rot) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);  // ordered by later barriers
 
     if (half) {
         for (int j = t; j < N; j += T) buf[j] = make_double2(in[2 * j], in[2 * j + 1]);
@@ -362,7 +437,7 @@ __global__ void __launch_bounds__(T, 1) ring_anal_kernel(RingStageArgs a) {
     }
     __syncthreads();
 
-    ring_dft<T, BMAX>(buf, d, -1, a.tabs);
+    ring_dft<T, BMAX>(buf, d, -1, a.tabs, twsm);
 
     if (half) {
         // B_k = E_k + e^{-2 pi i k/n} O_k, E = (Z_k + conj Z_{N-k})/2, O = -i (Z_k - conj Z_{N-k})/2
@@ -403,12 +478,8 @@ __global__ void __launch_bounds__(T, 1) ring_anal_kernel(RingStageArgs a) {
             val = buf[b];
         }
         double2 v = cscale(val, wgt);
-        if (phi0 != 0.0 && m > 0) {
-            double s, c;
-            sincos(-(double)m * phi0, &s, &c);
-            v = cmul(v, make_double2(c, s));
-        }
-        a.delta_out[a.m_base[m] + (int64_t)pos * a.m_stride[m]] = v;
+        if (rot && m > 0) v = cmul(v, cconj(ph.at(m)));
+        a.delta_out[delta_index(a, pos, m)] = v;
     }
 }
 
@@ -453,7 +524,9 @@ __global__ void __launch_bounds__(T, 1) bluestein_h_kernel(const RingDesc* __res
         buf[j] = v;
     }
     __syncthreads();
-    fft_run<T, BMAX>(buf, d, M, -1, tabs + d.tw_off);
+    const TwTab tw = stage_twiddles<T>(buf + BMAX, tabs + d.tw_off, M);
+    __syncthreads();
+    fft_run<T, BMAX>(buf, d.npass, d.radices, M, -1, tw);
     for (int j = threadIdx.x; j < M; j += T) tabs[d.h_off + j] = buf[j];
 }
 
@@ -462,16 +535,21 @@ __global__ void __launch_bounds__(T, 1) bluestein_h_kernel(const RingDesc* __res
 // ---------------------------------------------------------------------------------------
 namespace {
 constexpr int kBmax[FFT_N_CLASSES] = {256, 1024, 4096, 8192};
-constexpr int kThr[FFT_N_CLASSES] = {64, 128, 256, 512};
+constexpr int kThr[FFT_N_CLASSES] = {64, 256, 512, 1024};
 
+// buffer + fold partials + phase table (orders up to kMaxPhaseM)
+constexpr int kMaxPhaseM = 65535;
 template <int C>
-size_t class_smem() {
-    return (size_t)kBmax[C] * sizeof(double2) + 2 * (size_t)kThr[C] * sizeof(double2);
+size_t class_smem(int mmax) {
+    return (size_t)kBmax[C] * sizeof(double2) + 2 * (size_t)kThr[C] * sizeof(double2) +
+           (size_t)(64 + (kBmax[C] >> 6)) * sizeof(double2) +
+           (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
 }
 
 template <int C, class K>
 void set_smem_attr(K kernel) {
-    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)class_smem<C>());
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)class_smem<C>(kMaxPhaseM));
 }
 
 template <int C>
@@ -482,7 +560,7 @@ void synth_c(const RingStageArgs& a, cudaStream_t s) {
         RingStageArgs b = a;
         b.rings = a.rings + r0;
         const int nr = a.n_rings - r0 < 65535 ? a.n_rings - r0 : 65535;
-        ring_synth_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(), s>>>(b);
+        ring_synth_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(a.mmax), s>>>(b);
     }
 }
 template <int C>
@@ -493,7 +571,7 @@ void anal_c(const RingStageArgs& a, cudaStream_t s) {
         RingStageArgs b = a;
         b.rings = a.rings + r0;
         const int nr = a.n_rings - r0 < 65535 ? a.n_rings - r0 : 65535;
-        ring_anal_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(), s>>>(b);
+        ring_anal_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(a.mmax), s>>>(b);
     }
 }
 template <int C>
@@ -502,7 +580,7 @@ void blue_c(const RingDesc* descs, int n, double2* tabs, cudaStream_t s) {
     (void)once;
     for (int r0 = 0; r0 < n; r0 += 65535) {
         const int nr = n - r0 < 65535 ? n - r0 : 65535;
-        bluestein_h_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(), s>>>(descs + r0, tabs);
+        bluestein_h_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(0), s>>>(descs + r0, tabs);
     }
 }
 }  // namespace

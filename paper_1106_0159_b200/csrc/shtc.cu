@@ -103,7 +103,8 @@ struct LegPlan {
     std::vector<int> ms;
     std::vector<Stream> streams;
     DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
-        tile_cnt, m_order;
+        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters;
+    uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
     double build_ms = 0.0;
@@ -300,36 +301,65 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     CK(cudaStreamSynchronize(s));
     P.useful = useful;
 
-    // alive tile lists per order, orders by cost (descending) for the block schedule
+    // alive tile lists per order and the cost-sorted work queues of the persistent kernels
     std::vector<int> tl, toffs(n_m), tcnt(n_m);
-    std::vector<double> cost(n_m);
-    P.nominal = 0;
-    P.executed = 0;
+    std::vector<LegItem> a2m, m2a;
+    std::vector<int> per_m(n_m);
+    std::vector<int64_t> slot(n_m);
+    int64_t slots = 0;
+    P.nominal = P.executed = P.prefix_steps = P.checked_steps = P.fast_steps = 0;
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
         P.nominal += (uint64_t)(n + 1) * ns;
         toffs[i] = (int)tl.size();
         for (int t = 0; t < v.n_tiles; ++t) {
-            if (info[(size_t)i * v.n_tiles + t].x < 0) continue;
+            const int2 ti = info[(size_t)i * v.n_tiles + t];
+            if (ti.x < 0) continue;
             tl.push_back(t);
+            a2m.push_back(LegItem{i, t, 0, 0});
             const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
             P.executed += (uint64_t)(n + 1) * in_tile;
+            // phase accounting (degree pairs rounded outward, as the kernels run them)
+            const uint64_t pre = (uint64_t)std::max(0, std::min(n, ti.x - 1) & ~1);
+            const uint64_t fst = (uint64_t)std::max(0, n - std::max(ti.y, 0));
+            P.prefix_steps += pre * in_tile;
+            P.fast_steps += std::min<uint64_t>(fst, n - pre) * in_tile;
+            P.checked_steps += (uint64_t)(n + 1 - pre - std::min<uint64_t>(fst, n - pre)) * in_tile;
         }
         tcnt[i] = (int)tl.size() - toffs[i];
-        cost[i] = (double)(n + 1) * std::ceil(tcnt[i] / (double)LEG_W);
+        per_m[i] = (tcnt[i] + LEG_M2A_GROUP - 1) / LEG_M2A_GROUP;
+        slot[i] = slots;
+        slots += (int64_t)per_m[i] * (n + 1);
+        for (int g = 0; g < per_m[i]; ++g)
+            m2a.push_back(LegItem{i, toffs[i] + g * LEG_M2A_GROUP,
+                                  std::min(LEG_M2A_GROUP, tcnt[i] - g * LEG_M2A_GROUP), g});
     }
-    std::vector<int> order(n_m);
-    std::iota(order.begin(), order.end(), 0);
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return cost[a] > cost[b]; });
+    auto steps_of = [&](const LegItem& it) { return (int64_t)(lmax - ms[it.mi] + 1); };
+    std::stable_sort(a2m.begin(), a2m.end(),
+                     [&](const LegItem& a, const LegItem& b) { return steps_of(a) > steps_of(b); });
+    std::stable_sort(m2a.begin(), m2a.end(), [&](const LegItem& a, const LegItem& b) {
+        return steps_of(a) * a.b > steps_of(b) * b.b;
+    });
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
     P.tile_off.upload(toffs, s);
     P.tile_cnt.upload(tcnt, s);
-    P.m_order.upload(order, s);
+    P.a2m_items.upload(a2m, s);
+    P.m2a_items.upload(m2a, s);
+    P.m2a_per_m.upload(per_m, s);
+    P.m2a_slot.upload(slot, s);
+    P.m2a_scratch.ensure((size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
+    P.counters.ensure((size_t)(1 + n_m) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
     v.tile_list_cnt = P.tile_cnt.as<int>();
-    v.m_order = P.m_order.as<int>();
+    v.a2m_items = P.a2m_items.as<LegItem>();
+    v.n_a2m_items = (int)a2m.size();
+    v.m2a_items = P.m2a_items.as<LegItem>();
+    v.n_m2a_items = (int)m2a.size();
+    v.m2a_items_per_m = P.m2a_per_m.as<int>();
+    v.m2a_slot_base = P.m2a_slot.as<int64_t>();
+    v.m2a_scratch_elems = slots;
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float ms_el = 0.f;
@@ -388,7 +418,9 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
         if (d.n < 1) fail(SHTC_EINVAL, "ring_synthesis: ring has no samples");
         const bool half = (d.n % 2 == 0);
         d.N = half ? d.n / 2 : d.n;
-        const bool smooth = is_smooth7(d.N);
+        // 7-smooth lengths run the mixed-radix path; odd radices fit the register-staged
+        // passes only up to 1024 points, longer non-power-of-two lengths go through Bluestein
+        const bool smooth = is_smooth7(d.N) && (d.N <= 1024 || (d.N & (d.N - 1)) == 0);
         d.B = smooth ? d.N : next_pow2(2 * d.N - 1);
         d.flags = (half ? 1 : 0) | (smooth ? 0 : 2);
         d.pix_off = c->pixoff[r];
@@ -401,7 +433,9 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
                                         " needs an FFT buffer beyond the shared-memory classes");
         auto rp = radix_plan(d.B);
         d.npass = (int)rp.size();
-        for (size_t i = 0; i < rp.size(); ++i) d.radix[i] = (unsigned char)rp[i];
+        if (rp.size() > (size_t)FFT_MAX_PASSES) fail(SHTC_EUNSUPPORTED, "radix plan too long");
+        d.radices = 0;
+        for (size_t i = 0; i < rp.size(); ++i) d.radices |= (unsigned long long)rp[i] << (4 * i);
         d.tw_off = table(0, d.B);
         d.hw_off = half ? table(1, d.n) : 0;
         if (!smooth) {
@@ -487,6 +521,7 @@ void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
         a.mmax = c->mmax;
         a.m_base = mb;
         a.m_stride = mst;
+        a.ld = c->mmax + 1;
         a.delta_in = delta;
         a.map_out = map;
         launch_ring_synthesis(k, a, c->stream);
@@ -504,6 +539,7 @@ void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, c
         a.mmax = c->mmax;
         a.m_base = mb;
         a.m_stride = mst;
+        a.ld = c->mmax + 1;
         a.map_in = map;
         a.delta_out = delta;
         launch_ring_analysis(k, a, c->stream);
@@ -532,11 +568,10 @@ void do_alm2map_dev(shtc_ctx* c, const double* alm, double* map, shtc_timing* t,
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev[0], s));
     launch_leg_alm2map(c->leg.view, reinterpret_cast<const double2*>(alm), c->delta.as<double2>(),
-                       c->id_row_off.as<int64_t>(), s);
+                       c->id_row_off.as<int64_t>(), c->leg.counters.as<int>(), s);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[1], s));
-    run_ring_synth(c, c->fft_id, c->delta.as<double2>(), map, c->id_m_base.as<int64_t>(),
-                   c->id_m_stride.as<int64_t>());
+    run_ring_synth(c, c->fft_id, c->delta.as<double2>(), map, nullptr, nullptr);
     CK(cudaEventRecord(c->ev[2], s));
     if (t) {
         CK(cudaEventSynchronize(c->ev[2]));
@@ -553,11 +588,11 @@ void do_map2alm_dev(shtc_ctx* c, const double* map, double* alm, shtc_timing* t,
     c->delta.ensure((size_t)c->n_rings * (c->mmax + 1) * sizeof(double2));
     cudaStream_t s = c->stream;
     CK(cudaEventRecord(c->ev[0], s));
-    run_ring_anal(c, c->fft_id, map, c->delta.as<double2>(), c->id_m_base.as<int64_t>(),
-                  c->id_m_stride.as<int64_t>());
+    run_ring_anal(c, c->fft_id, map, c->delta.as<double2>(), nullptr, nullptr);
     CK(cudaEventRecord(c->ev[1], s));
     launch_leg_map2alm(c->leg.view, c->delta.as<double2>(), c->id_row_off.as<int64_t>(),
-                       reinterpret_cast<double2*>(alm), 0, s);
+                       reinterpret_cast<double2*>(alm), 0, c->leg.counters.as<int>(),
+                       c->leg.m2a_scratch.as<double2>(), s);
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev[2], s));
     if (t) {
@@ -709,6 +744,16 @@ shtc_status shtc_plan_stats(shtc_ctx* ctx, uint64_t* nominal, uint64_t* executed
     });
 }
 
+shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* checked, uint64_t* fast) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        if (prefix) *prefix = ctx->leg.prefix_steps;
+        if (checked) *checked = ctx->leg.checked_steps;
+        if (fast) *fast = ctx->leg.fast_steps;
+    });
+}
+
 shtc_status shtc_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* map_dev, shtc_timing* t) {
     if (!ctx || !alm_dev || !map_dev) return SHTC_EINVAL;
     return guarded(ctx, [&] { do_alm2map_dev(ctx, alm_dev, map_dev, t); });
@@ -822,7 +867,8 @@ shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, doub
         const int64_t* ro = stage_row_off(ctx);
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         launch_leg_alm2map(ctx->leg.view, reinterpret_cast<const double2*>(alm_dev),
-                           reinterpret_cast<double2*>(delta_dev), ro, ctx->stream);
+                           reinterpret_cast<double2*>(delta_dev), ro, ctx->leg.counters.as<int>(),
+                           ctx->stream);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (t) {
@@ -841,7 +887,8 @@ shtc_status shtc_legendre_map2alm_dev(shtc_ctx* ctx, const double* delta_dev, do
         const int64_t* ro = stage_row_off(ctx);
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         launch_leg_map2alm(ctx->leg.view, reinterpret_cast<const double2*>(delta_dev), ro,
-                           reinterpret_cast<double2*>(alm_dev), 0, ctx->stream);
+                           reinterpret_cast<double2*>(alm_dev), 0, ctx->leg.counters.as<int>(),
+                           ctx->leg.m2a_scratch.as<double2>(), ctx->stream);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (t) {
@@ -867,8 +914,8 @@ shtc_status shtc_ring_synthesis_dev(shtc_ctx* ctx, const double* delta_dev, doub
             ensure_fft_id(ctx);
             ensure_id_layout(ctx);
             F = &ctx->fft_id;
-            mb = ctx->id_m_base.as<int64_t>();
-            mst = ctx->id_m_stride.as<int64_t>();
+            mb = nullptr;
+            mst = nullptr;
         }
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         run_ring_synth(ctx, *F, reinterpret_cast<const double2*>(delta_dev), map_dev, mb, mst);
@@ -896,8 +943,8 @@ shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double*
             ensure_fft_id(ctx);
             ensure_id_layout(ctx);
             F = &ctx->fft_id;
-            mb = ctx->id_m_base.as<int64_t>();
-            mst = ctx->id_m_stride.as<int64_t>();
+            mb = nullptr;
+            mst = nullptr;
         }
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         run_ring_anal(ctx, *F, map_dev, reinterpret_cast<double2*>(delta_dev), mb, mst);
@@ -950,7 +997,8 @@ shtc_status shtc_delta_a(shtc_ctx* ctx, const double* alm, int lmax, int mmax, i
         for (int r = 0; r < n_lat; ++r) rov[r] = (int64_t)r * n_m;
         ro.upload(rov, s);
         CK(cudaMemcpyAsync(a.p, alm, na, cudaMemcpyHostToDevice, s));
-        launch_leg_alm2map(ctx->op_leg.view, a.as<double2>(), d.as<double2>(), ro.as<int64_t>(), s);
+        launch_leg_alm2map(ctx->op_leg.view, a.as<double2>(), d.as<double2>(), ro.as<int64_t>(),
+                           ctx->op_leg.counters.as<int>(), s);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(delta, d.p, nd, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));
@@ -982,7 +1030,8 @@ shtc_status shtc_accumulate_alm(shtc_ctx* ctx, const double* delta, int n_lat, c
         ro.upload(rov, s);
         CK(cudaMemcpyAsync(a.p, alm_inout, na, cudaMemcpyHostToDevice, s));
         CK(cudaMemcpyAsync(d.p, delta, nd, cudaMemcpyHostToDevice, s));
-        launch_leg_map2alm(ctx->op_leg.view, d.as<double2>(), ro.as<int64_t>(), a.as<double2>(), 1, s);
+        launch_leg_map2alm(ctx->op_leg.view, d.as<double2>(), ro.as<int64_t>(), a.as<double2>(), 1,
+                           ctx->op_leg.counters.as<int>(), ctx->op_leg.m2a_scratch.as<double2>(), s);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(alm_inout, a.p, na, cudaMemcpyDeviceToHost, s));
         CK(cudaStreamSynchronize(s));

@@ -384,7 +384,10 @@ class Context:
     def plan_stats(self):
         a, b, c = C.c_uint64(), C.c_uint64(), C.c_uint64()
         self._check(lib().shtc_plan_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
-        return {"nominal": a.value, "executed": b.value, "useful": c.value}
+        d, e, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._check(lib().shtc_plan_phase_stats(self._h, C.byref(d), C.byref(e), C.byref(f)))
+        return {"nominal": a.value, "executed": b.value, "useful": c.value,
+                "prefix": d.value, "checked": e.value, "fast": f.value}
 
     # host-buffer transforms ---------------------------------------------------------
     def alm2map(self, alm: np.ndarray, out: np.ndarray | None = None, timing: bool = False):
