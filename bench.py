@@ -1,0 +1,392 @@
+#!/usr/bin/env python
+"""Benchmark driver: alm2map + map2alm on HEALPix nside=2048, lmax=mmax=4096 (BASELINE C4).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one alm2map of a Gaussian a_lm followed by one map2alm of the resulting map
+(both FP64, the paper's two transforms).  `value` = whole-job algorithmic FP64 TFLOP/s
+(8 flops per (l, m, ring-pair) step of the reference's mirror path, both transforms,
+SURVEY.md §8d) over the device-timed step (inputs already in HBM, max over ranks).
+`e2e` runs the same step through the host-buffer C ABI (shtc_alm2map / shtc_map2alm) from
+pinned host memory, host<->device copies inside the timed region.
+
+N > 1 (torchrun, one process per GPU, NCCL): orders are dealt with the reference's
+assign_m, rings with assign_rings; the Legendre stage writes the packed all-to-all send
+buffer directly, one NCCL all-to-all moves Delta, the ring stage reads the receive buffer
+directly (strong scaling: total work fixed).
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, built from
+/root/reference by oracle/build_ref.sh) on the host cores, on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "alm2map/map2alm ms & FP64 TFLOP/s, nside=2048 ℓmax=4096, 1/2/4/8 B200"
+NSIDE, LMAX = 2048, 4096
+SEED_ALM = 12345
+
+
+def falg_flops(lmax: int, mmax: int, n_rings: int) -> float:
+    """F_alg = 8 x n_alm x ceil(R_N / 2) per transform."""
+    n_alm = (mmax + 1) * (lmax + 1) - mmax * (mmax + 1) // 2
+    return 8.0 * n_alm * ((n_rings + 1) // 2)
+
+
+# ----------------------------------------------------------------------------------------
+# clocks
+# ----------------------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        time.sleep(0.15)
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                self.out, _ = self.proc.communicate()
+
+    def summary(self):
+        rows = []
+        for line in (self.out or "").splitlines():
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                rows.append((float(parts[0]), float(parts[1]), parts[4:8]))
+            except ValueError:
+                continue
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = sorted(r[0] for r in rows)
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i, v in enumerate(r[2]) if v.lower() == "active"})
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": max(r[1] for r in rows),
+                "samples": len(rows), "reasons": reasons}
+
+
+# ----------------------------------------------------------------------------------------
+# CPU baseline: the reference itself (oracle/_ref), bounded sample
+# ----------------------------------------------------------------------------------------
+_PROBE = {}
+
+
+def cpu_baseline(max_seconds: float = 30.0):
+    """Reference alm2map+map2alm (distributed_synthesis/analysis, 1 worker, all host threads,
+    mirror pairing = its fastest path) on the largest HEALPix config projected to fit."""
+    from oracle import ref
+    from paper_1106_0159_b200 import sht
+    threads = os.cpu_count() or 1
+    cfgs = [(128, 256), (256, 512), (512, 1024), (1024, 2048), (2048, 4096)]
+    if "rate" not in _PROBE:
+        # probe on C1 to project the cost (the reference's time scales ~ F_alg)
+        g = ref.healpix_grid(128)
+        a = ref.random_alm(256, 256, SEED_ALM)
+        t0 = time.perf_counter()
+        m, _ = ref.distributed_synthesis(a, 256, 256, g, 1, threads, pairing=True)
+        ref.distributed_analysis(m, 256, 256, g, 1, threads, pairing=True)
+        _PROBE["rate"] = 2 * falg_flops(256, 256, g.n_rings) / max(time.perf_counter() - t0, 1e-6)
+    rate = _PROBE["rate"]
+    chosen = cfgs[0]
+    for ns, lm in cfgs:
+        # the small probe over-estimates the rate of large configs (cache effects): margin 3x
+        if 3 * 2 * falg_flops(lm, lm, 4 * ns - 1) / rate <= max_seconds:
+            chosen = (ns, lm)
+    ns, lm = chosen
+    g = ref.healpix_grid(ns)
+    a = sht.gaussian_alm(lm, lm, SEED_ALM)
+    t0 = time.perf_counter()
+    m, st1 = ref.distributed_synthesis(a, lm, lm, g, 1, threads, pairing=True)
+    t1 = time.perf_counter()
+    _, st2 = ref.distributed_analysis(m, lm, lm, g, 1, threads, pairing=True)
+    t2 = time.perf_counter()
+    fl = 2 * falg_flops(lm, lm, g.n_rings)
+    return {
+        "value": fl / (t2 - t0) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
+        "sample": f"one alm2map+map2alm at HEALPix nside={ns}, lmax=mmax={lm} (largest config "
+                  f"projected to fit {max_seconds:.0f}s; same transforms as the workload, rate "
+                  f"normalised by F_alg), reference distributed_synthesis/analysis, 1 worker x "
+                  f"{threads} threads, PairPolicy::mirror",
+        "ms_alm2map": (t1 - t0) * 1e3, "ms_map2alm": (t2 - t1) * 1e3,
+        "stages_alm2map_s": {k: st1[k] for k in ("recurrence_s", "fft_s", "exchange_s")},
+        "stages_map2alm_s": {k: st2[k] for k in ("recurrence_s", "fft_s", "exchange_s")},
+    }
+
+
+# ----------------------------------------------------------------------------------------
+# GPU arm
+# ----------------------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_ours(args):
+    import torch
+    from paper_1106_0159_b200 import sht
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    grid = sht.build_healpix_grid(args.nside)
+    lmax = mmax = args.lmax
+    ctx = sht.Context(local)
+    stream = torch.cuda.current_stream(dev)
+    ctx.set_stream(stream.cuda_stream)
+    ctx.set_grid(grid, mirror=True)
+
+    alm_h = sht.gaussian_alm(lmax, mmax, SEED_ALM)
+    n_alm = alm_h.size
+    layout = sht.WorkerLayout.create(grid, mmax, ws)
+    Mi = layout.m_sets[rank]
+    if ws == 1:
+        ctx.set_band(lmax, mmax)
+    else:
+        ctx.set_band(lmax, mmax, Mi)
+    t0 = time.perf_counter()
+    ctx.plan()
+    plan_s = time.perf_counter() - t0
+    stats = ctx.plan_stats()
+
+    alm = torch.from_numpy(alm_h.view(np.float64)).to(dev)
+    alm_out = torch.zeros_like(alm)
+    launches_per_step = None
+
+    if ws == 1:
+        mp = torch.empty(grid.n_pix, dtype=torch.float64, device=dev)
+
+        def step():
+            t1 = ctx.alm2map_dev(alm.data_ptr(), mp.data_ptr(), timing=True)
+            t2 = ctx.map2alm_dev(mp.data_ptr(), alm_out.data_ptr(), timing=True)
+            return t1, t2
+        ring_classes = None
+    else:
+        import torch.distributed as dist
+        row_off, send_c, recv_c, ring_list, m_base, m_stride = sht.exchange_layout(layout, rank)
+        ctx.set_exchange_layout(row_off, ring_list, m_base, m_stride)
+        send = torch.empty(2 * sum(send_c), dtype=torch.float64, device=dev)
+        recv = torch.empty(2 * sum(recv_c), dtype=torch.float64, device=dev)
+        mp = torch.zeros(grid.n_pix, dtype=torch.float64, device=dev)
+        s_split = [2 * c for c in send_c]
+        r_split = [2 * c for c in recv_c]
+
+        def step():
+            t1 = ctx.legendre_alm2map_dev(alm.data_ptr(), send.data_ptr(), timing=True)
+            dist.all_to_all_single(recv, send, r_split, s_split)
+            t3 = ctx.ring_synthesis_dev(recv.data_ptr(), mp.data_ptr(), timing=True)
+            t4 = ctx.ring_analysis_dev(mp.data_ptr(), recv.data_ptr(), timing=True)
+            dist.all_to_all_single(send, recv, s_split, r_split)
+            t2 = ctx.legendre_map2alm_dev(send.data_ptr(), alm_out.data_ptr(), timing=True)
+            t1["fft_ms"] = t3["fft_ms"]
+            t2["fft_ms"] = t4["fft_ms"]
+            return t1, t2
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    leg_a, leg_s, fft_a, fft_s = [], [], [], []
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            t1, t2 = step()
+            leg_s.append(t1["legendre_ms"]); fft_s.append(t1["fft_ms"])
+            leg_a.append(t2["legendre_ms"]); fft_a.append(t2["fft_ms"])
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+        if ws > 1:
+            dist.barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_total = float(t.item())
+    ms_step = ms_total / args.steps
+
+    # ---- end to end through the host-buffer C ABI (pinned host memory) ----
+    e2e = None
+    if ws == 1:
+        alm_pin = torch.from_numpy(alm_h.view(np.float64)).pin_memory()
+        map_pin = torch.empty(grid.n_pix, dtype=torch.float64).pin_memory()
+        alm_back = torch.empty_like(alm_pin).pin_memory()
+        a_np = alm_pin.numpy().view(np.complex128)
+        m_np = map_pin.numpy()
+        b_np = alm_back.numpy().view(np.complex128)
+        for _ in range(max(1, args.warmup // 2)):
+            ctx.alm2map(a_np, out=m_np)
+            ctx.map2alm(m_np, out=b_np)
+        torch.cuda.synchronize(dev)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            ctx.alm2map(a_np, out=m_np)
+            ctx.map2alm(m_np, out=b_np)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        e2e_ms = e0.elapsed_time(e1) / args.steps
+        bytes_alm = n_alm * 16
+        bytes_map = grid.n_pix * 8
+        e2e = {"value": 2 * falg_flops(lmax, mmax, grid.n_rings) / (e2e_ms * 1e-3) / 1e12,
+               "unit": "TFLOP/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": bytes_alm + bytes_map, "d2h_bytes_per_step": bytes_map + bytes_alm}
+
+    # ---- parity spot check of the timed output (the reference is checked in tests/) ----
+    roundtrip = None
+    if ws == 1:
+        back = alm_out.cpu().numpy().view(np.complex128)
+        roundtrip = float(np.linalg.norm(back - alm_h) / np.linalg.norm(alm_h))
+
+    if rank != 0:
+        if ws > 1:
+            dist.destroy_process_group()
+        return
+
+    fl_step = 2 * falg_flops(lmax, mmax, grid.n_rings)
+    value = fl_step / (ms_step * 1e-3) / 1e12
+    peak_tf, _ = sht.measure_fp64_peak(local)
+    leg_a_ms, leg_s_ms = float(np.mean(leg_a)), float(np.mean(leg_s))
+    fl_leg = falg_flops(lmax, mmax, grid.n_rings) / ws  # per rank, per launch
+    dom_ms, dom_name = (leg_a_ms, "leg_map2alm_kernel") if leg_a_ms >= leg_s_ms else (leg_s_ms, "leg_alm2map_kernel")
+    achieved = fl_leg / (dom_ms * 1e-3) / 1e12
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        try:
+            traffic = json.loads(tf.read_text()).get(dom_name)
+        except Exception:
+            traffic = None
+    roofline = {
+        "bound": "fp64", "kernel": dom_name, "achieved": achieved, "peak": peak_tf,
+        "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+        "peak_source": "measured live: DFMA-loop probe (shtc_measure_fp64_peak); "
+                       "MEASURED_PEAKS.json has no FP64 entry",
+        "flops_per_launch": fl_leg,
+        "flops_basis": "algorithmic 8 x n_alm x ceil(R_N/2) (reference mirror-path steps x 8)",
+        "useful_tflops": 8.0 * stats["useful"] / ws / (dom_ms * 1e-3) / 1e12,
+        "executed_tflops": 8.0 * stats["executed"] / (dom_ms * 1e-3) / 1e12,
+        "alm2map_kernel": {"ms": leg_s_ms, "achieved": fl_leg / (leg_s_ms * 1e-3) / 1e12},
+        "map2alm_kernel": {"ms": leg_a_ms, "achieved": fl_leg / (leg_a_ms * 1e-3) / 1e12},
+    }
+    ms_a2m = float(np.mean(leg_s)) + float(np.mean(fft_s))
+    ms_m2a = float(np.mean(leg_a)) + float(np.mean(fft_a))
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: Gaussian a_lm (splitmix64 counter stream + Box-Muller, seed 12345); "
+                "map2alm input = the step's alm2map output",
+        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={lmax} (C4)",
+                   "grid": "healpix-ring", "nside": args.nside, "lmax": lmax, "mmax": mmax,
+                   "parallelism": f"m-distributed x{ws}" + (" + NCCL all-to-all" if ws > 1 else ""),
+                   "l2": "inputs larger than L2 (a_lm 134 MB, map 403 MB, Delta 537 MB)"},
+        "ms_alm2map": ms_a2m, "ms_map2alm": ms_m2a,
+        "stages_ms": {"alm2map": {"legendre": leg_s_ms, "fft": float(np.mean(fft_s))},
+                      "map2alm": {"legendre": leg_a_ms, "fft": float(np.mean(fft_a))}},
+        "plan_s": plan_s, "steps_accounting": stats,
+        "roundtrip_rel_err": roundtrip,
+        "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
+        "gpu_launches": args.steps * (2 + 2 + 2 * 4),
+    }
+    if ws == 1 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+        except Exception as exc:  # the oracle must exist; report instead of hiding
+            line["cpu_baseline"] = {"error": repr(exc)}
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    # every step is a bounded sample so that the whole --steps/--warmup run stays within a
+    # few minutes (~150 s of reference CPU work in total)
+    per_step = max(2.0, min(args.cpu_seconds, 150.0 / (args.steps + args.warmup)))
+    steps = []
+    for _ in range(args.warmup):
+        cpu_baseline(per_step)
+    for _ in range(args.steps):
+        steps.append(cpu_baseline(per_step))
+    v = float(np.median([s["value"] for s in steps]))
+    cb = dict(steps[-1])
+    cb["value"] = v
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": ws,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": float(np.median([s["ms_alm2map"] + s["ms_map2alm"] for s in steps])),
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic: Gaussian a_lm (seed 12345)",
+        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={args.lmax} (C4)",
+                   "sample": cb["sample"]},
+        "cpu_baseline": cb,
+        "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--nside", type=int, default=NSIDE)
+    p.add_argument("--lmax", type=int, default=LMAX)
+    p.add_argument("--cpu-seconds", type=float, default=30.0)
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    args = p.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
