@@ -477,13 +477,13 @@ __device__ __forceinline__ void m2a_enter_fast(M2ALane<R>& L) {
 
 struct M2AWarpSmem {
     Coef cf[LEG_CL];
-    double red[32][17];  // lane transpose for the 16-value reduction
+    double red[32][18];  // lane transpose for the 16-value reduction (16-byte aligned rows)
 };
 
 }  // namespace
 
 template <int R>
-__global__ void __launch_bounds__(LEG_WARPS * 32, 3)
+__global__ void __launch_bounds__(LEG_WARPS * 32, 4)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
                        int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
@@ -554,9 +554,13 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                 for (int g = 0; g < cnt; g += 8) {
                     const int gc = min(8, cnt - g);
                     const int ig = i0 + g;  // even degree offset
-                    double part[16];
-#pragma unroll
-                    for (int u = 0; u < 16; ++u) part[u] = 0.0;
+                    // previous tiles' partial for this lane's (degree, component): issued now,
+                    // consumed after the group so the load latency hides behind the math
+                    const int iw = ig + (lane >> 1);
+                    double* const wp = reinterpret_cast<double*>(part_out + iw) + (lane & 1);
+                    const double prev = (tt > 0 && lane < 16 && iw <= n) ? *wp : 0.0;
+                    // per-step lane contributions go straight to this lane's transpose row
+                    double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
                     bool any = true;
                     if (!fast && ig > ie && ig > 0) {
                         fast = true;
@@ -566,12 +570,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                         // straight-line 8 steps, no checks
 #pragma unroll
                         for (int u = 0; u < 8; u += 2) {
-                            const double2 v1 = m2a_step<R, FAST, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
-                            const double2 v2 = m2a_step<R, FAST, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
-                            part[2 * u + 0] = v1.x;
-                            part[2 * u + 1] = v1.y;
-                            part[2 * u + 2] = v2.x;
-                            part[2 * u + 3] = v2.y;
+                            row[u] = m2a_step<R, FAST, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                            row[u + 1] = m2a_step<R, FAST, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
                         }
                     } else if (ig > 0 && ig + gc < is) {
                         // whole group before the tile's first activation: recurrence only
@@ -585,8 +585,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                         // generic (checked) path: activation window, the seed group, partial groups
 #pragma unroll
                         for (int u = 0; u < 8; u += 2) {
+                            double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
                             if (u < gc) {
-                                double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
                                 if (ig + u == 0) {
                                     // seed term (degree offset 0): no recurrence step
 #pragma unroll
@@ -599,31 +599,30 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                                 }
                                 if (u + 1 < gc)
                                     v2 = m2a_step<R, CHECKED, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
-                                part[2 * u + 0] = v1.x;
-                                part[2 * u + 1] = v1.y;
-                                part[2 * u + 2] = v2.x;
-                                part[2 * u + 3] = v2.y;
                             }
+                            row[u] = v1;
+                            row[u + 1] = v2;
                         }
                     }
                     // reduce the 16 values over the 32 lanes (fixed order), accumulate the
-                    // warp's partial sums for degree offsets i0+g .. i0+g+7 in its scratch slot
+                    // warp's partial sums for degree offsets ig .. ig+7 in its scratch slot
                     double v = 0.0;
                     if (any) {
-#pragma unroll
-                        for (int u = 0; u < 16; ++u) sm.red[lane][u] = part[u];
                         __syncwarp();
                         const int col = lane & 15, half = lane >> 4;
+                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-                        for (int row = 0; row < 16; ++row) v += sm.red[half * 16 + row][col];
+                        for (int rr = 0; rr < 16; rr += 4) {
+                            s0 += sm.red[half * 16 + rr][col];
+                            s1 += sm.red[half * 16 + rr + 1][col];
+                            s2 += sm.red[half * 16 + rr + 2][col];
+                            s3 += sm.red[half * 16 + rr + 3][col];
+                        }
+                        v = (s0 + s1) + (s2 + s3);
                         v += __shfl_xor_sync(0xffffffffu, v, 16);
-                        __syncwarp();
                     }
-                    const int i = i0 + g + (lane >> 1);
-                    if (lane < 16 && i <= n) {
-                        double* o = reinterpret_cast<double*>(part_out + i) + (lane & 1);
-                        *o = (tt == 0) ? v : *o + v;
-                    }
+                    __syncwarp();
+                    if (lane < 16 && iw <= n) *wp = prev + v;
                 }
             }
         }
