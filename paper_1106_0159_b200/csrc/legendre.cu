@@ -183,6 +183,39 @@ void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* til
                                                               useful_dev);
 }
 
+__global__ void leg_checkpoint_kernel(LegPlanView p, double2* __restrict__ ck_q, int* __restrict__ ck_k) {
+    const int mi = blockIdx.y;
+    const int s = blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= p.st.n) return;
+    const int is = p.tile_info[(size_t)mi * p.n_tiles + s / LEG_TILE].x;
+    const int ic = leg_tile_start(is);
+    if (ic < 2) return;
+    const int m = p.ms[mi];
+    const double x = p.st.x[s];
+    double q1 = 0.0, q0 = 0.0;
+    int k = 0;
+    seed_value(m, p.log_mu[m], p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, q1, k);
+    const double* __restrict__ A = p.tab.A + p.tab.tab_off[mi];
+    const double* __restrict__ T = p.tab.T + p.tab.tab_off[mi];
+    for (int i = 1; i < ic; ++i) {  // the PREFIX steps of the kernels, verbatim
+        double q2 = rec_step(__ldg(A + i), x, q1, q0);
+        if (fabs(q2) >= __ldg(T + i)) {
+            q2 *= SCALE_DOWN;
+            q1 *= SCALE_DOWN;
+            ++k;
+        }
+        q0 = q1;
+        q1 = q2;
+    }
+    ck_q[(size_t)mi * p.st.n + s] = make_double2(q0, q1);
+    ck_k[(size_t)mi * p.st.n + s] = k;
+}
+
+void launch_leg_checkpoint(const LegPlanView& p, double2* ck_q, int* ck_k, cudaStream_t s) {
+    dim3 grid((p.st.n + 127) / 128, p.n_m);
+    leg_checkpoint_kernel<<<grid, 128, 0, s>>>(p, ck_q, ck_k);
+}
+
 // ---------------------------------------------------------------------------------------
 // Persistent, warp-independent Legendre kernels.  Every warp pulls (order, tile) items from a
 // cost-sorted queue, stages the order's coefficients for LEG_CL degrees at a time in its own
@@ -272,29 +305,49 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
         const double lmu = p.log_mu[m];
         const double2 a0 = galm[0];
 
+        const int ic = leg_tile_start(is);  // resume point (0: from the seed)
         A2MLane<R> L;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
             const int s = tile * (32 * R) + r * 32 + lane;
-            double mant = 0.0, x = 0.0;
+            double mant = 0.0, x = 0.0, q0 = 0.0;
             int k = 0;
             if (s < p.st.n) {
                 x = p.st.x[s];
-                seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
+                if (ic) {
+                    const double2 q = p.ck_q[(size_t)mi * p.st.n + s];
+                    q0 = q.x;
+                    mant = q.y;
+                    k = p.ck_k[(size_t)mi * p.st.n + s];
+                } else {
+                    seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
+                }
             }
             L.x[r] = x;
-            L.q0[r] = 0.0;
+            L.q0[r] = q0;
             L.q1[r] = mant;
             L.k[r] = k;
             // degree offset 0 term: a_mm P_mm (c_0 = 1), only when the seed is already at k == 0
-            L.ae[r] = (k == 0) ? make_double2(a0.x * mant, a0.y * mant) : make_double2(0.0, 0.0);
+            L.ae[r] = (k == 0 && !ic) ? make_double2(a0.x * mant, a0.y * mant) : make_double2(0.0, 0.0);
             L.ao[r] = make_double2(0.0, 0.0);
         }
         bool fast = false;
+        if (ic) {
+            // the even step ic on its own, then (odd, even) pairs from ic + 1
+            Coef c0;
+            const double cc = gC[ic];
+            const double2 v = galm[ic];
+            c0.A = gA[ic];
+            c0.T = gT[ic];
+            c0.ar = v.x * cc;
+            c0.ai = v.y * cc;
+            a2m_step<R, CHECKED, false>(L, c0);
+        }
+        const int i_first = ic + 1;
 
-        // chunk c covers degree offsets i = 1 + c*CL .. ; lane j stages entry j
+        // chunk c covers degree offsets i = i_first + c*CL .. ; lane j stages entry j
         auto fetch = [&](int c, Coef& cf) {
-            const int i = 1 + c * LEG_CL + lane;
+            const int i = i_first + c * LEG_CL + lane;
             if (i <= n) {
                 const double cc = gC[i];
                 const double2 v = galm[i];
@@ -308,7 +361,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                 cf.ar = cf.ai = 0.0;
             }
         };
-        const int nchunks = (n + LEG_CL - 1) / LEG_CL;
+        const int nchunks = (n - i_first + 1 + LEG_CL - 1) / LEG_CL;
         Coef nxt;
         if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
@@ -316,7 +369,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
             sm[lane] = nxt;
             __syncwarp();
             if (c + 1 < nchunks) fetch(c + 1, nxt);
-            const int i0 = 1 + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
+            const int i0 = i_first + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
             const int cnt = min(LEG_CL, n - i0 + 1);
             int j = 0;
             if (!fast) {
@@ -505,12 +558,14 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
         const double* __restrict__ gT = p.tab.T + toff;
         const double lmu = p.log_mu[m];
         double2* __restrict__ part_out = scratch + p.m2a_slot_base[mi] + (int64_t)item.g * (n + 1);
-        const int nchunks = (n + 1 + LEG_CL - 1) / LEG_CL;  // degree offsets 0..n
-
         for (int tt = 0; tt < item.b; ++tt) {
             const int tile = p.tile_list[item.a + tt];
             const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
             const int is = info.x, ie = info.y;
+            const int ic = leg_tile_start(is);  // resume point (even; 0: from the seed)
+            const int nchunks = (n + 1 - ic + LEG_CL - 1) / LEG_CL;  // degree offsets ic..n
+            if (tt == 0)  // degrees below the first tile's start get no other first write
+                for (int i = lane; i < ic; i += 32) part_out[i] = make_double2(0.0, 0.0);
             M2ALane<R> L;
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -518,12 +573,20 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 const bool valid = s < p.st.n;
                 double mant = 0.0, x = 0.0;
                 int k = 1;  // invalid lanes: never active
+                double q0 = 0.0;
                 if (valid) {
                     x = p.st.x[s];
-                    seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
+                    if (ic) {
+                        const double2 q = p.ck_q[(size_t)mi * p.st.n + s];
+                        q0 = q.x;
+                        mant = q.y;
+                        k = p.ck_k[(size_t)mi * p.st.n + s];
+                    } else {
+                        seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
+                    }
                 }
                 L.x[r] = x;
-                L.q0[r] = 0.0;
+                L.q0[r] = q0;
                 L.q1[r] = valid ? mant : 0.0;
                 L.k[r] = k;
                 L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
@@ -532,7 +595,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
             bool fast = false;
 
             auto fetch = [&](int c, Coef& cf) {
-                const int i = c * LEG_CL + lane;
+                const int i = ic + c * LEG_CL + lane;
                 if (i <= n) {
                     cf.A = gA[i];
                     cf.T = gT[i];
@@ -549,7 +612,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 sm.cf[lane] = nxt;
                 __syncwarp();
                 if (c + 1 < nchunks) fetch(c + 1, nxt);
-                const int i0 = c * LEG_CL;
+                const int i0 = ic + c * LEG_CL;
                 const int cnt = min(LEG_CL, n - i0 + 1);
                 for (int g = 0; g < cnt; g += 8) {
                     const int gc = min(8, cnt - g);

@@ -103,7 +103,7 @@ struct LegPlan {
     std::vector<int> ms;
     std::vector<Stream> streams;
     DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
-        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters;
+        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_k;
     uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
@@ -318,13 +318,14 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
             tl.push_back(t);
             a2m.push_back(LegItem{i, t, 0, 0});
             const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
-            P.executed += (uint64_t)(n + 1) * in_tile;
-            // phase accounting (degree pairs rounded outward, as the kernels run them)
-            const uint64_t pre = (uint64_t)std::max(0, std::min(n, ti.x - 1) & ~1);
-            const uint64_t fst = (uint64_t)std::max(0, n - std::max(ti.y, 0));
-            P.prefix_steps += pre * in_tile;
-            P.fast_steps += std::min<uint64_t>(fst, n - pre) * in_tile;
-            P.checked_steps += (uint64_t)(n + 1 - pre - std::min<uint64_t>(fst, n - pre)) * in_tile;
+            // the kernels resume at ic (checkpointed state), run the activation window
+            // checked and everything after the last activation unchecked
+            const int ic = leg_tile_start(ti.x);
+            const uint64_t run = (uint64_t)(n + 1 - ic);
+            const uint64_t fst = std::min<uint64_t>(run, (uint64_t)std::max(0, n - std::max(ti.y, ic)));
+            P.executed += run * in_tile;
+            P.fast_steps += fst * in_tile;
+            P.checked_steps += (run - fst) * in_tile;
         }
         tcnt[i] = (int)tl.size() - toffs[i];
         per_m[i] = (tcnt[i] + LEG_M2A_GROUP - 1) / LEG_M2A_GROUP;
@@ -334,12 +335,20 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
             m2a.push_back(LegItem{i, toffs[i] + g * LEG_M2A_GROUP,
                                   std::min(LEG_M2A_GROUP, tcnt[i] - g * LEG_M2A_GROUP), g});
     }
-    auto steps_of = [&](const LegItem& it) { return (int64_t)(lmax - ms[it.mi] + 1); };
+    // cost = degree steps actually run (from the tile's resume point)
+    auto tile_cost = [&](int mi, int t) {
+        return (int64_t)(lmax - ms[mi] + 1 - leg_tile_start(info[(size_t)mi * v.n_tiles + t].x));
+    };
+    auto a2m_cost = [&](const LegItem& it) { return tile_cost(it.mi, it.a); };
+    auto m2a_cost = [&](const LegItem& it) {
+        int64_t c = 0;
+        for (int k = 0; k < it.b; ++k) c += tile_cost(it.mi, tl[it.a + k]);
+        return c;
+    };
     std::stable_sort(a2m.begin(), a2m.end(),
-                     [&](const LegItem& a, const LegItem& b) { return steps_of(a) > steps_of(b); });
-    std::stable_sort(m2a.begin(), m2a.end(), [&](const LegItem& a, const LegItem& b) {
-        return steps_of(a) * a.b > steps_of(b) * b.b;
-    });
+                     [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
+    std::stable_sort(m2a.begin(), m2a.end(),
+                     [&](const LegItem& a, const LegItem& b) { return m2a_cost(a) > m2a_cost(b); });
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
     P.tile_off.upload(toffs, s);
@@ -349,6 +358,14 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.m2a_per_m.upload(per_m, s);
     P.m2a_slot.upload(slot, s);
     P.m2a_scratch.ensure((size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
+    P.ck_q.ensure((size_t)std::max(1, n_m * ns) * sizeof(double2));
+    P.ck_k.ensure((size_t)std::max(1, n_m * ns) * sizeof(int));
+    v.ck_q = P.ck_q.as<double2>();
+    v.ck_k = P.ck_k.as<int>();
+    if (n_m > 0) {
+        launch_leg_checkpoint(v, P.ck_q.as<double2>(), P.ck_k.as<int>(), s);
+        CK(cudaGetLastError());
+    }
     P.counters.ensure((size_t)(1 + n_m) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
