@@ -232,6 +232,21 @@ struct Coef {
     double A, T, ar, ai;  // recurrence coefficient, ladder threshold, staged a_lm * c_l
 };
 
+// Per-warp staging, structure of arrays so a group of steps loads with 16-byte LDS.
+struct __align__(16) CoefSoA {
+    double A[LEG_CL];
+    double T[LEG_CL];
+    double ar[LEG_CL];
+    double ai[LEG_CL];
+    __device__ __forceinline__ void put(int j, const Coef& c) {
+        A[j] = c.A;
+        T[j] = c.T;
+        ar[j] = c.ar;
+        ai[j] = c.ai;
+    }
+    __device__ __forceinline__ Coef get(int j) const { return Coef{A[j], T[j], ar[j], ai[j]}; }
+};
+
 __device__ __forceinline__ int warp_next_item(int* counter) {
     int it = 0;
     if ((threadIdx.x & 31) == 0) it = atomicAdd(counter, 1);
@@ -284,9 +299,9 @@ template <int R>
 __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
     leg_alm2map_kernel(LegPlanView p, const double2* __restrict__ alm, double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, int* __restrict__ counter) {
-    __shared__ Coef sm_all[LEG_WARPS][LEG_CL];
+    __shared__ CoefSoA sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    Coef* sm = sm_all[warp];
+    CoefSoA& sm = sm_all[warp];
 
     for (;;) {
         const int it = warp_next_item(counter);
@@ -366,7 +381,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
         if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
             __syncwarp();
-            sm[lane] = nxt;
+            sm.put(lane, nxt);
             __syncwarp();
             if (c + 1 < nchunks) fetch(c + 1, nxt);
             const int i0 = i_first + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
@@ -376,7 +391,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
                 for (; j + 1 < cnt; j += 2) {
                     const int i = i0 + j;
                     if (i > ie) break;
-                    const Coef c1 = sm[j], c2 = sm[j + 1];
+                    const Coef c1 = sm.get(j), c2 = sm.get(j + 1);
                     if (i + 1 < is) {
                         a2m_step<R, PREFIX, true>(L, c1);
                         a2m_step<R, PREFIX, false>(L, c2);
@@ -392,20 +407,30 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
             }
             if (fast) {
                 for (; j + 8 <= cnt; j += 8) {
+                    // the group's coefficients up front (16-byte loads; j is even)
+                    Coef cg[8];
 #pragma unroll
                     for (int u = 0; u < 8; u += 2) {
-                        a2m_step<R, FAST, true>(L, sm[j + u]);
-                        a2m_step<R, FAST, false>(L, sm[j + u + 1]);
+                        const double2 a = *reinterpret_cast<const double2*>(&sm.A[j + u]);
+                        const double2 xr = *reinterpret_cast<const double2*>(&sm.ar[j + u]);
+                        const double2 xi = *reinterpret_cast<const double2*>(&sm.ai[j + u]);
+                        cg[u] = Coef{a.x, 0.0, xr.x, xi.x};
+                        cg[u + 1] = Coef{a.y, 0.0, xr.y, xi.y};
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        a2m_step<R, FAST, true>(L, cg[u]);
+                        a2m_step<R, FAST, false>(L, cg[u + 1]);
                     }
                 }
                 for (; j + 1 < cnt; j += 2) {
-                    a2m_step<R, FAST, true>(L, sm[j]);
-                    a2m_step<R, FAST, false>(L, sm[j + 1]);
+                    a2m_step<R, FAST, true>(L, sm.get(j));
+                    a2m_step<R, FAST, false>(L, sm.get(j + 1));
                 }
             }
             if (j < cnt) {  // trailing odd step (last chunk only)
-                if (fast) a2m_step<R, FAST, true>(L, sm[j]);
-                else a2m_step<R, CHECKED, true>(L, sm[j]);
+                if (fast) a2m_step<R, FAST, true>(L, sm.get(j));
+                else a2m_step<R, CHECKED, true>(L, sm.get(j));
             }
         }
 
@@ -529,7 +554,7 @@ __device__ __forceinline__ void m2a_enter_fast(M2ALane<R>& L) {
 }
 
 struct M2AWarpSmem {
-    Coef cf[LEG_CL];
+    CoefSoA cf;
     double red[32][18];  // lane transpose for the 16-value reduction (16-byte aligned rows)
 };
 
@@ -609,7 +634,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
             fetch(0, nxt);
             for (int c = 0; c < nchunks; ++c) {
                 __syncwarp();
-                sm.cf[lane] = nxt;
+                sm.cf.put(lane, nxt);
                 __syncwarp();
                 if (c + 1 < nchunks) fetch(c + 1, nxt);
                 const int i0 = ic + c * LEG_CL;
@@ -630,19 +655,26 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                         m2a_enter_fast<R>(L);
                     }
                     if (fast && gc == 8) {
-                        // straight-line 8 steps, no checks
+                        // straight-line 8 steps, no checks; coefficients loaded up front
+                        Coef cg[8];
 #pragma unroll
                         for (int u = 0; u < 8; u += 2) {
-                            row[u] = m2a_step<R, FAST, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
-                            row[u + 1] = m2a_step<R, FAST, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                            const double2 a = *reinterpret_cast<const double2*>(&sm.cf.A[g + u]);
+                            cg[u] = Coef{a.x, 0.0, 0.0, 0.0};
+                            cg[u + 1] = Coef{a.y, 0.0, 0.0, 0.0};
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; u += 2) {
+                            row[u] = m2a_step<R, FAST, false>(L, cg[u], p, delta, row_off, mi, tile, lane);
+                            row[u + 1] = m2a_step<R, FAST, true>(L, cg[u + 1], p, delta, row_off, mi, tile, lane);
                         }
                     } else if (ig > 0 && ig + gc < is) {
                         // whole group before the tile's first activation: recurrence only
                         any = false;
                         for (int u = 0; u < gc; u += 2) {
-                            m2a_step<R, PREFIX, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                            m2a_step<R, PREFIX, false>(L, sm.cf.get(g + u), p, delta, row_off, mi, tile, lane);
                             if (u + 1 < gc)
-                                m2a_step<R, PREFIX, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                                m2a_step<R, PREFIX, true>(L, sm.cf.get(g + u + 1), p, delta, row_off, mi, tile, lane);
                         }
                     } else {
                         // generic (checked) path: activation window, the seed group, partial groups
@@ -658,10 +690,10 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                                         v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
                                     }
                                 } else {
-                                    v1 = m2a_step<R, CHECKED, false>(L, sm.cf[g + u], p, delta, row_off, mi, tile, lane);
+                                    v1 = m2a_step<R, CHECKED, false>(L, sm.cf.get(g + u), p, delta, row_off, mi, tile, lane);
                                 }
                                 if (u + 1 < gc)
-                                    v2 = m2a_step<R, CHECKED, true>(L, sm.cf[g + u + 1], p, delta, row_off, mi, tile, lane);
+                                    v2 = m2a_step<R, CHECKED, true>(L, sm.cf.get(g + u + 1), p, delta, row_off, mi, tile, lane);
                             }
                             row[u] = v1;
                             row[u + 1] = v2;

@@ -141,12 +141,14 @@ __device__ __forceinline__ void stockham_pass(double2* buf, int B, int Ns, int s
             if (Ns > 1) {
                 int bq, k;
                 divmod_small(b, Ns, inv, bq, k);
+                // w^r for r = 1..R-1 from one table lookup: powers by a depth-3 product tree
+                double2 w[R];
+                w[1] = tw.at(k * tstride);
+                if (sign > 0) w[1].y = -w[1].y;
 #pragma unroll
-                for (int r = 1; r < R; ++r) {
-                    double2 w = tw.at(r * k * tstride);
-                    if (sign > 0) w.y = -w.y;
-                    v[q][r] = cmul(v[q][r], w);
-                }
+                for (int r = 2; r < R; ++r) w[r] = cmul(w[r / 2], w[r - r / 2]);
+#pragma unroll
+                for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], w[r]);
             }
             dft<R>(v[q], sign);
         }
