@@ -630,6 +630,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 }
                 cf.ar = cf.ai = 0.0;
             };
+            // this lane's (degree, component) of the 8-degree group in the scratch slot
+            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic + (lane >> 1)) + (lane & 1);
             Coef nxt;
             fetch(0, nxt);
             for (int c = 0; c < nchunks; ++c) {
@@ -645,7 +647,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                     // previous tiles' partial for this lane's (degree, component): issued now,
                     // consumed after the group so the load latency hides behind the math
                     const int iw = ig + (lane >> 1);
-                    double* const wp = reinterpret_cast<double*>(part_out + iw) + (lane & 1);
+                    double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
+                    rmw_ptr += 16;
                     const double prev = (tt > 0 && lane < 16 && iw <= n) ? *wp : 0.0;
                     // per-step lane contributions go straight to this lane's transpose row
                     double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
@@ -734,8 +737,17 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
             const double2* base = scratch + p.m2a_slot_base[mi];
             double2* out = alm + alm_offset(m, p.lmax);
             for (int i = lane; i <= n; i += 32) {
+                // slots summed in order g = 0, 1, ...; loads issued in batches of 4
                 double2 v = make_double2(0.0, 0.0);
-                for (int g = 0; g < G; ++g) v = cadd(v, __ldcg(base + (int64_t)g * (n + 1) + i));
+                int g = 0;
+                for (; g + 4 <= G; g += 4) {
+                    const double2 a0 = __ldcg(base + (int64_t)g * (n + 1) + i);
+                    const double2 a1 = __ldcg(base + (int64_t)(g + 1) * (n + 1) + i);
+                    const double2 a2 = __ldcg(base + (int64_t)(g + 2) * (n + 1) + i);
+                    const double2 a3 = __ldcg(base + (int64_t)(g + 3) * (n + 1) + i);
+                    v = cadd(cadd(cadd(cadd(v, a0), a1), a2), a3);
+                }
+                for (; g < G; ++g) v = cadd(v, __ldcg(base + (int64_t)g * (n + 1) + i));
                 const double c = gC[i];
                 v = make_double2(v.x * c, v.y * c);
                 out[i] = accumulate ? cadd(out[i], v) : v;
