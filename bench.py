@@ -291,13 +291,15 @@ def run_ours(args):
     fl_leg = falg_flops(lmax, mmax, grid.n_rings) / ws  # per rank, per launch
     dom_ms, dom_name = (leg_a_ms, "leg_map2alm_kernel") if leg_a_ms >= leg_s_ms else (leg_s_ms, "leg_alm2map_kernel")
     achieved = fl_leg / (dom_ms * 1e-3) / 1e12
-    traffic = None
-    tf = ROOT / "profiles" / "traffic.json"
+    # DRAM bytes per launch and ncu-executed DP rate from the committed full capture
+    traffic, ncu_rec = None, {}
+    tf = ROOT / "profiles" / "ncu_kernels.json"
     if tf.exists():
         try:
-            traffic = json.loads(tf.read_text()).get(dom_name)
+            ncu_rec = json.loads(tf.read_text()).get(dom_name, {})
+            traffic = ncu_rec.get("dram_bytes")
         except Exception:
-            traffic = None
+            traffic, ncu_rec = None, {}
     roofline = {
         "bound": "fp64", "kernel": dom_name, "achieved": achieved, "peak": peak_tf,
         "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
@@ -307,6 +309,8 @@ def run_ours(args):
         "flops_basis": "algorithmic 8 x n_alm x ceil(R_N/2) (reference mirror-path steps x 8)",
         "useful_tflops": 8.0 * stats["useful"] / ws / (dom_ms * 1e-3) / 1e12,
         "executed_tflops": 8.0 * stats["executed"] / (dom_ms * 1e-3) / 1e12,
+        "ncu": {"executed_dp_tflops": ncu_rec.get("executed_dp_tflops"),
+                "fp64_pipe_pct": ncu_rec.get("fp64_pipe_pct"), "source": ncu_rec.get("source")},
         "alm2map_kernel": {"ms": leg_s_ms, "achieved": fl_leg / (leg_s_ms * 1e-3) / 1e12},
         "map2alm_kernel": {"ms": leg_a_ms, "achieved": fl_leg / (leg_a_ms * 1e-3) / 1e12},
     }
