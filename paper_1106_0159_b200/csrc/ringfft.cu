@@ -141,14 +141,16 @@ __device__ __forceinline__ void stockham_pass(double2* buf, int B, int Ns, int s
             if (Ns > 1) {
                 int bq, k;
                 divmod_small(b, Ns, inv, bq, k);
-                // w^r for r = 1..R-1 from one table lookup: powers by a depth-3 product tree
-                double2 w[R];
-                w[1] = tw.at(k * tstride);
-                if (sign > 0) w[1].y = -w[1].y;
+                // w^r for r = 1..R-1 from one table lookup, as a running product (2 live
+                // complex temporaries; error grows by ~1 ulp per power, <= 7 ulp)
+                double2 w = tw.at(k * tstride);
+                if (sign > 0) w.y = -w.y;
+                double2 wr = w;
 #pragma unroll
-                for (int r = 2; r < R; ++r) w[r] = cmul(w[r / 2], w[r - r / 2]);
-#pragma unroll
-                for (int r = 1; r < R; ++r) v[q][r] = cmul(v[q][r], w[r]);
+                for (int r = 1; r < R; ++r) {
+                    v[q][r] = cmul(v[q][r], wr);
+                    if (r + 1 < R) wr = cmul(wr, w);
+                }
             }
             dft<R>(v[q], sign);
         }
@@ -347,7 +349,7 @@ __device__ __forceinline__ void store_z(double2* buf, const double2* __restrict_
 // synthesis: Delta rows -> ring samples
 // ---------------------------------------------------------------------------------------
 template <int T, int BMAX>
-__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) ring_synth_kernel(RingStageArgs a) {
+__global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_synth_kernel(RingStageArgs a) {
     extern __shared__ __align__(16) double2 smem[];
     double2* buf = smem;               // BMAX
     double2* red = smem + BMAX;        // 2T fold partials
@@ -416,7 +418,7 @@ __global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) ring_synth_kernel
 // analysis: ring samples -> Delta^S rows
 // ---------------------------------------------------------------------------------------
 template <int T, int BMAX>
-__global__ void __launch_bounds__(T, (T >= 512 ? 1 : 512 / T)) ring_anal_kernel(RingStageArgs a) {
+__global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_anal_kernel(RingStageArgs a) {
     extern __shared__ __align__(16) double2 smem[];
     double2* buf = smem;
     double2* red = smem + BMAX;
