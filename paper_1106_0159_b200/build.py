@@ -19,6 +19,7 @@ CSRC = PKG / "csrc"
 OBJ = PKG / "_build"
 LIB = PKG / "libshtc.so"
 DROPIN_LIB = PKG / "libsht_b200.so"
+CLI_BIN = PKG / "sht_b200"
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
@@ -71,16 +72,20 @@ def build(verbose: bool = False, force: bool = False) -> Path:
 
 def build_dropin(force: bool = False) -> Path:
     """C++ drop-in `sht::` API (include/sht/*.hpp) over the C ABI: libsht_b200.so."""
-    srcs = [CSRC / "sht_dropin.cpp"]
+    srcs = [CSRC / "sht_dropin.cpp", CSRC / "sht_edge.cpp"]
     if not srcs[0].exists():
         return DROPIN_LIB
     hdrs = list((ROOT / "include" / "sht").glob("*.hpp")) + [ROOT / "include" / "shtc.h"]
-    newest = max(p.stat().st_mtime for p in srcs + hdrs + [LIB])
-    if not force and DROPIN_LIB.exists() and DROPIN_LIB.stat().st_mtime >= newest:
+    newest = max(p.stat().st_mtime for p in srcs + hdrs + [LIB, CSRC / "sht_cli.cpp"])
+    if not force and DROPIN_LIB.exists() and CLI_BIN.exists() and DROPIN_LIB.stat().st_mtime >= newest:
         return DROPIN_LIB
     _run(["g++", "-std=c++20", "-O2", "-fPIC", "-shared", "-I", str(ROOT / "include"), *map(str, srcs),
           "-o", str(DROPIN_LIB) + ".tmp", f"-L{PKG}", "-lshtc", "-Wl,-rpath,$ORIGIN"])
     os.replace(str(DROPIN_LIB) + ".tmp", DROPIN_LIB)
+    # CLI edge (reference tools/sht_main.cpp subcommands) on the drop-in
+    _run(["g++", "-std=c++20", "-O2", "-I", str(ROOT / "include"), str(CSRC / "sht_cli.cpp"), "-o",
+          str(CLI_BIN) + ".tmp", f"-L{PKG}", "-lsht_b200", "-lshtc", "-Wl,-rpath,$ORIGIN"])
+    os.replace(str(CLI_BIN) + ".tmp", CLI_BIN)
     return DROPIN_LIB
 
 

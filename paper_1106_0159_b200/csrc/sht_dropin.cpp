@@ -656,9 +656,13 @@ AlmSet distributed_analysis(const SkyMap& map, int lmax, int mmax, const WorkerL
 
 // ---- Profiler -----------------------------------------------------------------------------------
 void Profiler::configure(int n_workers, int n_threads) {
+    if (n_workers < 1 || n_threads < 1)
+        throw std::invalid_argument("Profiler: worker and thread counts must be >= 1");
     n_workers_ = n_workers;
     n_threads_ = n_threads;
     steps_.assign(static_cast<size_t>(n_workers) * n_threads, 0);
+    precompute_s = recurrence_s = exchange_s = fft_s = 0.0;
+    exchange_bytes = 0;
 }
 std::uint64_t* Profiler::step_slot(int w, int t) {
     if (w < 0 || w >= n_workers_ || t < 0 || t >= n_threads_) throw std::out_of_range("Profiler::step_slot");
