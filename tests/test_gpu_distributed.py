@@ -24,7 +24,7 @@ def alltoall(sends, send_counts, recv_counts, W):
     return out
 
 
-@pytest.mark.parametrize("nside,lmax,W", [(8, 16, 2), (16, 40, 3), (64, 128, 4), (128, 256, 8)])
+@pytest.mark.parametrize("nside,lmax,W", [(8, 16, 1), (8, 16, 2), (16, 40, 3), (64, 128, 4), (128, 256, 8), (256, 512, 1)])
 def test_stage_path_matches_single_worker(nside, lmax, W):
     dev = torch.device("cuda", 0)
     grid = sht.build_healpix_grid(nside)
