@@ -83,12 +83,16 @@ __host__ __device__ inline int leg_tile_start(int is) { return is >= 2 ? (is & ~
 
 // Delta rows: element (ring r, order index mi) at delta[row_off[r] + mi].
 // counters: >= 1 + n_m ints of device scratch (zeroed by the launcher).
+// phases: bit0 = zero pass (dead tiles / orders without alive tiles), bit1 = the persistent
+// kernel over p's item list (callers may pass a view restricted to one chunk of items).
+constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3;
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
-                        const int64_t* row_off, int* counters, cudaStream_t s);
+                        const int64_t* row_off, int* counters, cudaStream_t s,
+                        int phases = LEG_PHASE_ALL);
 // a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.  scratch: m2a_scratch_elems.
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s);
+                        cudaStream_t s, int phases = LEG_PHASE_ALL);
 int leg_persistent_blocks(int device);
 
 // ---------------------------------------------------------------------------------------

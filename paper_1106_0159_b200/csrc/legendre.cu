@@ -473,11 +473,13 @@ int leg_persistent_blocks(int device) {
 }
 
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
-                        const int64_t* row_off, int* counters, cudaStream_t s) {
+                        const int64_t* row_off, int* counters, cudaStream_t s, int phases) {
     if (p.n_m == 0) return;
-    dim3 zg((p.st.n + 127) / 128, p.n_m);
-    leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off);
-    if (p.n_a2m_items == 0) return;
+    if (phases & LEG_PHASE_ZERO) {
+        dim3 zg((p.st.n + 127) / 128, p.n_m);
+        leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off);
+    }
+    if (!(phases & LEG_PHASE_MAIN) || p.n_a2m_items == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
     int blocks = leg_persistent_blocks(dev);
@@ -767,10 +769,10 @@ __global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm)
 
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s) {
+                        cudaStream_t s, int phases) {
     if (p.n_m == 0) return;
-    if (!accumulate) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
-    if (p.n_m2a_items == 0) return;
+    if (!accumulate && (phases & LEG_PHASE_ZERO)) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
+    if (!(phases & LEG_PHASE_MAIN) || p.n_m2a_items == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
     int sms = 148, per = 1;

@@ -105,15 +105,24 @@ struct LegPlan {
     DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
         tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_k;
     uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
+    // order chunks for the pipelined host-buffer paths: items sorted by (chunk, cost), chunk k
+    // covers order indices [chunk_mi[k], chunk_mi[k+1]) and items [a2m_off[k], a2m_off[k+1])
+    std::vector<int> chunk_mi, a2m_off, m2a_off;
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
     double build_ms = 0.0;
 };
 
+constexpr int kPipeChunks = 4;  // chunks of the pipelined host-buffer entry points
+
 struct FftPlan {
     bool built = false;
     DevBuf descs[FFT_N_CLASSES];
     int count[FFT_N_CLASSES] = {0, 0, 0, 0};
+    // ring ranges (contiguous pixels) for the pipelined paths: class c's descriptors of range k
+    // are [range_start[c][k], range_start[c][k+1]); range k covers pixels [range_pix[k], ..[k+1])
+    std::vector<int> range_start[FFT_N_CLASSES];
+    std::vector<int64_t> range_pix;
     DevBuf tabs;
     double build_ms = 0.0;
 };
@@ -155,6 +164,9 @@ struct shtc_ctx {
     // scratch
     DevBuf delta, alm_buf, map_buf, stats;
     cudaEvent_t ev[8] = {};
+    // pipelined host-buffer paths
+    cudaStream_t h2d = nullptr, d2h = nullptr;
+    cudaEvent_t pev[3][kPipeChunks] = {};
 };
 
 namespace {
@@ -345,10 +357,36 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         for (int k = 0; k < it.b; ++k) c += tile_cost(it.mi, tl[it.a + k]);
         return c;
     };
-    std::stable_sort(a2m.begin(), a2m.end(),
-                     [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
-    std::stable_sort(m2a.begin(), m2a.end(),
-                     [&](const LegItem& a, const LegItem& b) { return m2a_cost(a) > m2a_cost(b); });
+    // order chunks of ~equal coefficient counts (H2D / D2H units of the pipelined paths)
+    std::vector<int> chunk_of(n_m, 0);
+    P.chunk_mi.assign(1, 0);
+    {
+        int64_t total = 0, acc = 0;
+        for (int i = 0; i < n_m; ++i) total += lmax - ms[i] + 1;
+        for (int i = 0; i < n_m; ++i) {
+            const int k = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
+            while ((int)P.chunk_mi.size() <= k) P.chunk_mi.push_back(i);
+            chunk_of[i] = k;
+            acc += lmax - ms[i] + 1;
+        }
+        while ((int)P.chunk_mi.size() <= kPipeChunks) P.chunk_mi.push_back(n_m);
+    }
+    std::stable_sort(a2m.begin(), a2m.end(), [&](const LegItem& a, const LegItem& b) {
+        if (chunk_of[a.mi] != chunk_of[b.mi]) return chunk_of[a.mi] < chunk_of[b.mi];
+        return a2m_cost(a) > a2m_cost(b);
+    });
+    std::stable_sort(m2a.begin(), m2a.end(), [&](const LegItem& a, const LegItem& b) {
+        if (chunk_of[a.mi] != chunk_of[b.mi]) return chunk_of[a.mi] < chunk_of[b.mi];
+        return m2a_cost(a) > m2a_cost(b);
+    });
+    P.a2m_off.assign(kPipeChunks + 1, 0);
+    P.m2a_off.assign(kPipeChunks + 1, 0);
+    for (const auto& it : a2m) P.a2m_off[chunk_of[it.mi] + 1]++;
+    for (const auto& it : m2a) P.m2a_off[chunk_of[it.mi] + 1]++;
+    for (int k = 0; k < kPipeChunks; ++k) {
+        P.a2m_off[k + 1] += P.a2m_off[k];
+        P.m2a_off[k + 1] += P.m2a_off[k];
+    }
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
     P.tile_off.upload(toffs, s);
@@ -485,6 +523,30 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
         F.descs[k].upload(per_class[k], s);
         F.count[k] = (int)per_class[k].size();
     }
+    // ring ranges of ~equal pixel counts (descriptors were appended in ring order)
+    {
+        int64_t total = 0;
+        for (int r : rings) total += c->nphi[r];
+        std::vector<int> range_of_pos(rings.size());
+        std::vector<int> first_pos(kPipeChunks + 1, (int)rings.size());
+        int64_t acc = 0;
+        for (size_t pos = 0; pos < rings.size(); ++pos) {
+            const int k = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
+            range_of_pos[pos] = k;
+            first_pos[k] = std::min(first_pos[k], (int)pos);
+            acc += c->nphi[rings[pos]];
+        }
+        for (int k = kPipeChunks - 1; k >= 0; --k) first_pos[k] = std::min(first_pos[k], first_pos[k + 1]);
+        F.range_pix.assign(kPipeChunks + 1, 0);
+        for (int k = 0; k <= kPipeChunks; ++k)
+            F.range_pix[k] = first_pos[k] < (int)rings.size() ? c->pixoff[rings[first_pos[k]]]
+                                                                 : c->npix;
+        for (int cls = 0; cls < FFT_N_CLASSES; ++cls) {
+            F.range_start[cls].assign(kPipeChunks + 1, 0);
+            for (const RingDesc& d : per_class[cls]) F.range_start[cls][range_of_pos[d.ring_pos] + 1]++;
+            for (int k = 0; k < kPipeChunks; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
+        }
+    }
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float el = 0.f;
@@ -529,11 +591,13 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 }
 
 void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
-                    const int64_t* mb, const int64_t* mst) {
+                    const int64_t* mb, const int64_t* mst, int range = -1) {
     for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
         RingStageArgs a{};
-        a.rings = F.descs[k].as<RingDesc>();
-        a.n_rings = F.count[k];
+        const int b = range < 0 ? 0 : F.range_start[k][range];
+        const int e = range < 0 ? F.count[k] : F.range_start[k][range + 1];
+        a.rings = F.descs[k].as<RingDesc>() + b;
+        a.n_rings = e - b;
         a.tabs = F.tabs.as<double2>();
         a.mmax = c->mmax;
         a.m_base = mb;
@@ -547,11 +611,13 @@ void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
 }
 
 void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
-                   const int64_t* mst) {
+                   const int64_t* mst, int range = -1) {
     for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
         RingStageArgs a{};
-        a.rings = F.descs[k].as<RingDesc>();
-        a.n_rings = F.count[k];
+        const int b = range < 0 ? 0 : F.range_start[k][range];
+        const int e = range < 0 ? F.count[k] : F.range_start[k][range + 1];
+        a.rings = F.descs[k].as<RingDesc>() + b;
+        a.n_rings = e - b;
         a.tabs = F.tabs.as<double2>();
         a.mmax = c->mmax;
         a.m_base = mb;
@@ -669,6 +735,11 @@ void shtc_destroy(shtc_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
+    for (auto& row : ctx->pev)
+        for (auto& e : row)
+            if (e) cudaEventDestroy(e);
+    if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
+    if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
     delete ctx;
 }
@@ -781,30 +852,95 @@ shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_d
     return guarded(ctx, [&] { do_map2alm_dev(ctx, map_dev, alm_dev, t); });
 }
 
+// Host-buffer entry points, pipelined over kPipeChunks chunks on three streams:
+//   alm2map: H2D of a_lm order chunk k || Legendre of chunk k-1 ; ring stage of ring range r
+//            || D2H of the pixels of range r-1
+//   map2alm: H2D of ring range r || ring analysis of range r-1 ; Legendre of order chunk k
+//            || D2H of the a_lm of chunk k-1
+// Same kernels and arithmetic as the device-resident path (results are bit-identical).
+namespace {
+void ensure_pipe(shtc_ctx* c) {
+    if (c->h2d) return;
+    CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    for (auto& row : c->pev)
+        for (auto& e : row) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+}
+
+LegPlanView chunk_view(const LegPlan& P, int k, bool a2m) {
+    LegPlanView v = P.view;
+    if (a2m) {
+        v.a2m_items = P.view.a2m_items + P.a2m_off[k];
+        v.n_a2m_items = P.a2m_off[k + 1] - P.a2m_off[k];
+    } else {
+        v.m2a_items = P.view.m2a_items + P.m2a_off[k];
+        v.n_m2a_items = P.m2a_off[k + 1] - P.m2a_off[k];
+    }
+    return v;
+}
+
+// complex-element range of order chunk k in the m-major a_lm triangle (full band)
+std::pair<size_t, size_t> alm_range(const shtc_ctx* c, const LegPlan& P, int k) {
+    auto off = [&](int mi) {
+        return mi >= (int)c->ms.size() ? alm_count(c->lmax, c->mmax)
+                                       : (size_t)alm_offset(c->ms[mi], c->lmax);
+    };
+    return {off(P.chunk_mi[k]), off(P.chunk_mi[k + 1])};
+}
+}  // namespace
+
 shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_timing* t) {
     if (!ctx || !alm || !map) return SHTC_EINVAL;
     return guarded(ctx, [&] {
         require_full_band(ctx);
-        if (!ctx->grid_set) fail(SHTC_EINVAL, "no grid set");
+        ensure_leg_plan(ctx);
+        ensure_fft_id(ctx);
+        ensure_id_layout(ctx);
+        ensure_pipe(ctx);
         const size_t na = alm_count(ctx->lmax, ctx->mmax) * sizeof(double2);
         const size_t nb = (size_t)ctx->npix * sizeof(double);
         ctx->alm_buf.ensure(na);
         ctx->map_buf.ensure(nb);
+        ctx->delta.ensure((size_t)ctx->n_rings * (ctx->mmax + 1) * sizeof(double2));
         cudaStream_t s = ctx->stream;
+        LegPlan& P = ctx->leg;
+        FftPlan& F = ctx->fft_id;
         CK(cudaEventRecord(ctx->ev[3], s));
-        CK(cudaMemcpyAsync(ctx->alm_buf.p, alm, na, cudaMemcpyHostToDevice, s));
-        CK(cudaEventRecord(ctx->ev[4], s));
-        shtc_timing tt{};
-        do_alm2map_dev(ctx, ctx->alm_buf.as<double>(), ctx->map_buf.as<double>(), &tt);
-        CK(cudaEventRecord(ctx->ev[5], s));
-        CK(cudaMemcpyAsync(map, ctx->map_buf.p, nb, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(ctx->ev[6], s));
+        CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
+        for (int k = 0; k < kPipeChunks; ++k) {
+            auto [b, e] = alm_range(ctx, P, k);
+            if (e > b)
+                CK(cudaMemcpyAsync(ctx->alm_buf.as<double2>() + b, reinterpret_cast<const double2*>(alm) + b,
+                                   (e - b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->h2d));
+            CK(cudaEventRecord(ctx->pev[0][k], ctx->h2d));
+        }
+        const int64_t* ro = ctx->id_row_off.as<int64_t>();
+        launch_leg_alm2map(P.view, ctx->alm_buf.as<double2>(), ctx->delta.as<double2>(), ro,
+                           P.counters.as<int>(), s, LEG_PHASE_ZERO);
+        for (int k = 0; k < kPipeChunks; ++k) {
+            CK(cudaStreamWaitEvent(s, ctx->pev[0][k], 0));
+            if (k == 0) CK(cudaEventRecord(ctx->ev[0], s));
+            launch_leg_alm2map(chunk_view(P, k, true), ctx->alm_buf.as<double2>(), ctx->delta.as<double2>(),
+                               ro, P.counters.as<int>(), s, LEG_PHASE_MAIN);
+            CK(cudaGetLastError());
+        }
+        CK(cudaEventRecord(ctx->ev[1], s));
+        for (int r = 0; r < kPipeChunks; ++r) {
+            run_ring_synth(ctx, F, ctx->delta.as<double2>(), ctx->map_buf.as<double>(), nullptr, nullptr, r);
+            CK(cudaEventRecord(ctx->pev[1][r], s));
+            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][r], 0));
+            const size_t pb = F.range_pix[r], pe = F.range_pix[r + 1];
+            if (pe > pb)
+                CK(cudaMemcpyAsync(map + pb, ctx->map_buf.as<double>() + pb, (pe - pb) * sizeof(double),
+                                   cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
         if (t) {
-            *t = tt;
-            t->h2d_ms = elapsed(ctx->ev[3], ctx->ev[4]);
-            t->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
-            t->total_ms = elapsed(ctx->ev[3], ctx->ev[6]);
+            fill_timing(t, elapsed(ctx->ev[0], ctx->ev[1]), elapsed(ctx->ev[1], ctx->ev[2]),
+                        elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
+                        elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }
@@ -813,26 +949,54 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
     if (!ctx || !alm || !map) return SHTC_EINVAL;
     return guarded(ctx, [&] {
         require_full_band(ctx);
-        if (!ctx->grid_set) fail(SHTC_EINVAL, "no grid set");
+        ensure_leg_plan(ctx);
+        ensure_fft_id(ctx);
+        ensure_id_layout(ctx);
+        ensure_pipe(ctx);
         const size_t na = alm_count(ctx->lmax, ctx->mmax) * sizeof(double2);
         const size_t nb = (size_t)ctx->npix * sizeof(double);
         ctx->alm_buf.ensure(na);
         ctx->map_buf.ensure(nb);
+        ctx->delta.ensure((size_t)ctx->n_rings * (ctx->mmax + 1) * sizeof(double2));
         cudaStream_t s = ctx->stream;
+        LegPlan& P = ctx->leg;
+        FftPlan& F = ctx->fft_id;
         CK(cudaEventRecord(ctx->ev[3], s));
-        CK(cudaMemcpyAsync(ctx->map_buf.p, map, nb, cudaMemcpyHostToDevice, s));
-        CK(cudaEventRecord(ctx->ev[4], s));
-        shtc_timing tt{};
-        do_map2alm_dev(ctx, ctx->map_buf.as<double>(), ctx->alm_buf.as<double>(), &tt);
-        CK(cudaEventRecord(ctx->ev[5], s));
-        CK(cudaMemcpyAsync(alm, ctx->alm_buf.p, na, cudaMemcpyDeviceToHost, s));
-        CK(cudaEventRecord(ctx->ev[6], s));
+        CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
+        for (int r = 0; r < kPipeChunks; ++r) {
+            const size_t pb = F.range_pix[r], pe = F.range_pix[r + 1];
+            if (pe > pb)
+                CK(cudaMemcpyAsync(ctx->map_buf.as<double>() + pb, map + pb, (pe - pb) * sizeof(double),
+                                   cudaMemcpyHostToDevice, ctx->h2d));
+            CK(cudaEventRecord(ctx->pev[0][r], ctx->h2d));
+        }
+        for (int r = 0; r < kPipeChunks; ++r) {
+            CK(cudaStreamWaitEvent(s, ctx->pev[0][r], 0));
+            if (r == 0) CK(cudaEventRecord(ctx->ev[0], s));
+            run_ring_anal(ctx, F, ctx->map_buf.as<double>(), ctx->delta.as<double2>(), nullptr, nullptr, r);
+        }
+        CK(cudaEventRecord(ctx->ev[1], s));
+        const int64_t* ro = ctx->id_row_off.as<int64_t>();
+        launch_leg_map2alm(P.view, ctx->delta.as<double2>(), ro, ctx->alm_buf.as<double2>(), 0,
+                           P.counters.as<int>(), P.m2a_scratch.as<double2>(), s, LEG_PHASE_ZERO);
+        for (int k = 0; k < kPipeChunks; ++k) {
+            launch_leg_map2alm(chunk_view(P, k, false), ctx->delta.as<double2>(), ro, ctx->alm_buf.as<double2>(),
+                               0, P.counters.as<int>(), P.m2a_scratch.as<double2>(), s, LEG_PHASE_MAIN);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(ctx->pev[1][k], s));
+            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][k], 0));
+            auto [b, e] = alm_range(ctx, P, k);
+            if (e > b)
+                CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ctx->alm_buf.as<double2>() + b,
+                                   (e - b) * sizeof(double2), cudaMemcpyDeviceToHost, ctx->d2h));
+        }
+        CK(cudaEventRecord(ctx->ev[2], s));
+        CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
         if (t) {
-            *t = tt;
-            t->h2d_ms = elapsed(ctx->ev[3], ctx->ev[4]);
-            t->d2h_ms = elapsed(ctx->ev[5], ctx->ev[6]);
-            t->total_ms = elapsed(ctx->ev[3], ctx->ev[6]);
+            fill_timing(t, elapsed(ctx->ev[1], ctx->ev[2]), elapsed(ctx->ev[0], ctx->ev[1]),
+                        elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
+                        elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }
