@@ -555,9 +555,11 @@ __device__ __forceinline__ void m2a_enter_fast(M2ALane<R>& L) {
         }
 }
 
+constexpr int M2A_G = 16;  // degrees per cross-lane reduction group
+
 struct M2AWarpSmem {
     CoefSoA cf;
-    double red[32][18];  // lane transpose for the 16-value reduction (16-byte aligned rows)
+    double red[32][2 * M2A_G + 2];  // lane rows of (degree, re/im) partials, 16-byte aligned
 };
 
 }  // namespace
@@ -567,7 +569,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
                        int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
-    static_assert(LEG_CL % 8 == 0, "chunk must hold whole 8-step reduction groups");
+    static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
     __shared__ M2AWarpSmem sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     M2AWarpSmem& sm = sm_all[warp];
@@ -632,8 +634,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 }
                 cf.ar = cf.ai = 0.0;
             };
-            // this lane's (degree, component) of the 8-degree group in the scratch slot
-            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic + (lane >> 1)) + (lane & 1);
+            // this lane's (degree, component) of the group in the scratch slot
+            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
             Coef nxt;
             fetch(0, nxt);
             for (int c = 0; c < nchunks; ++c) {
@@ -643,15 +645,15 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 if (c + 1 < nchunks) fetch(c + 1, nxt);
                 const int i0 = ic + c * LEG_CL;
                 const int cnt = min(LEG_CL, n - i0 + 1);
-                for (int g = 0; g < cnt; g += 8) {
-                    const int gc = min(8, cnt - g);
+                for (int g = 0; g < cnt; g += M2A_G) {
+                    const int gc = min(M2A_G, cnt - g);
                     const int ig = i0 + g;  // even degree offset
                     // previous tiles' partial for this lane's (degree, component): issued now,
                     // consumed after the group so the load latency hides behind the math
                     const int iw = ig + (lane >> 1);
                     double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
-                    rmw_ptr += 16;
-                    const double prev = (tt > 0 && lane < 16 && iw <= n) ? *wp : 0.0;
+                    rmw_ptr += 2 * M2A_G;
+                    const double prev = (tt > 0 && iw <= n) ? *wp : 0.0;
                     // per-step lane contributions go straight to this lane's transpose row
                     double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
                     bool any = true;
@@ -659,19 +661,13 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                         fast = true;
                         m2a_enter_fast<R>(L);
                     }
-                    if (fast && gc == 8) {
-                        // straight-line 8 steps, no checks; coefficients loaded up front
-                        Coef cg[8];
+                    if (fast && gc == M2A_G) {
+                        // straight-line steps, no checks; coefficients loaded in pairs
 #pragma unroll
-                        for (int u = 0; u < 8; u += 2) {
+                        for (int u = 0; u < M2A_G; u += 2) {
                             const double2 a = *reinterpret_cast<const double2*>(&sm.cf.A[g + u]);
-                            cg[u] = Coef{a.x, 0.0, 0.0, 0.0};
-                            cg[u + 1] = Coef{a.y, 0.0, 0.0, 0.0};
-                        }
-#pragma unroll
-                        for (int u = 0; u < 8; u += 2) {
-                            row[u] = m2a_step<R, FAST, false>(L, cg[u], p, delta, row_off, mi, tile, lane);
-                            row[u + 1] = m2a_step<R, FAST, true>(L, cg[u + 1], p, delta, row_off, mi, tile, lane);
+                            row[u] = m2a_step<R, FAST, false>(L, Coef{a.x, 0.0, 0.0, 0.0}, p, delta, row_off, mi, tile, lane);
+                            row[u + 1] = m2a_step<R, FAST, true>(L, Coef{a.y, 0.0, 0.0, 0.0}, p, delta, row_off, mi, tile, lane);
                         }
                     } else if (ig > 0 && ig + gc < is) {
                         // whole group before the tile's first activation: recurrence only
@@ -683,8 +679,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                         }
                     } else {
                         // generic (checked) path: activation window, the seed group, partial groups
-#pragma unroll
-                        for (int u = 0; u < 8; u += 2) {
+                        for (int u = 0; u < M2A_G; u += 2) {
                             double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
                             if (u < gc) {
                                 if (ig + u == 0) {
@@ -704,25 +699,23 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                             row[u + 1] = v2;
                         }
                     }
-                    // reduce the 16 values over the 32 lanes (fixed order), accumulate the
-                    // warp's partial sums for degree offsets ig .. ig+7 in its scratch slot
+                    // lane j reduces column j (degree ig + j/2, component j&1) over the 32 lane
+                    // rows in a fixed order and accumulates it into the warp's scratch slot
                     double v = 0.0;
                     if (any) {
                         __syncwarp();
-                        const int col = lane & 15, half = lane >> 4;
                         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-                        for (int rr = 0; rr < 16; rr += 4) {
-                            s0 += sm.red[half * 16 + rr][col];
-                            s1 += sm.red[half * 16 + rr + 1][col];
-                            s2 += sm.red[half * 16 + rr + 2][col];
-                            s3 += sm.red[half * 16 + rr + 3][col];
+                        for (int rr = 0; rr < 32; rr += 4) {
+                            s0 += sm.red[rr][lane];
+                            s1 += sm.red[rr + 1][lane];
+                            s2 += sm.red[rr + 2][lane];
+                            s3 += sm.red[rr + 3][lane];
                         }
                         v = (s0 + s1) + (s2 + s3);
-                        v += __shfl_xor_sync(0xffffffffu, v, 16);
                     }
                     __syncwarp();
-                    if (lane < 16 && iw <= n) *wp = prev + v;
+                    if (iw <= n) *wp = prev + v;
                 }
             }
         }
