@@ -360,28 +360,33 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 3)
         }
         const int i_first = ic + 1;
 
-        // chunk c covers degree offsets i = i_first + c*CL .. ; lane j stages entry j
-        auto fetch = [&](int c, Coef& cf) {
+        // chunk c covers degree offsets i = i_first + c*CL .. ; lane j stages entry j.  The
+        // raw loads are held in registers across the current chunk's steps; the c_l scaling
+        // happens at staging time so no math waits on the prefetch.
+        struct Raw {
+            double A, T, C;
+            double2 v;
+        };
+        auto fetch = [&](int c, Raw& rw) {
             const int i = i_first + c * LEG_CL + lane;
             if (i <= n) {
-                const double cc = gC[i];
-                const double2 v = galm[i];
-                cf.A = gA[i];
-                cf.T = gT[i];
-                cf.ar = v.x * cc;
-                cf.ai = v.y * cc;
+                rw.C = gC[i];
+                rw.v = galm[i];
+                rw.A = gA[i];
+                rw.T = gT[i];
             } else {
-                cf.A = 0.0;
-                cf.T = 0x1p1000;
-                cf.ar = cf.ai = 0.0;
+                rw.A = 0.0;
+                rw.T = 0x1p1000;
+                rw.C = 0.0;
+                rw.v = make_double2(0.0, 0.0);
             }
         };
         const int nchunks = (n - i_first + 1 + LEG_CL - 1) / LEG_CL;
-        Coef nxt;
+        Raw nxt;
         if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
             __syncwarp();
-            sm.put(lane, nxt);
+            sm.put(lane, Coef{nxt.A, nxt.T, nxt.v.x * nxt.C, nxt.v.y * nxt.C});
             __syncwarp();
             if (c + 1 < nchunks) fetch(c + 1, nxt);
             const int i0 = i_first + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
@@ -648,12 +653,9 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 for (int g = 0; g < cnt; g += M2A_G) {
                     const int gc = min(M2A_G, cnt - g);
                     const int ig = i0 + g;  // even degree offset
-                    // previous tiles' partial for this lane's (degree, component): issued now,
-                    // consumed after the group so the load latency hides behind the math
                     const int iw = ig + (lane >> 1);
                     double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
                     rmw_ptr += 2 * M2A_G;
-                    const double prev = (tt > 0 && iw <= n) ? *wp : 0.0;
                     // per-step lane contributions go straight to this lane's transpose row
                     double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
                     bool any = true;
@@ -715,7 +717,12 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                         v = (s0 + s1) + (s2 + s3);
                     }
                     __syncwarp();
-                    if (iw <= n) *wp = prev + v;
+                    // first tile stores; later tiles add in place (fire-and-forget reduction,
+                    // a single lane owns each word so the order is the tile order)
+                    if (iw <= n) {
+                        if (tt == 0) *wp = v;
+                        else if (any) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
+                    }
                 }
             }
         }
