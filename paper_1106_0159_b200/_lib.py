@@ -6,10 +6,11 @@ The library is built in-tree by `python -m paper_1106_0159_b200.build` (or
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
-LIB_PATH = PKG / "libshtc.so"
+LIB_PATH = Path(os.environ["SHTC_VARIANT_LIB"]) if os.environ.get("SHTC_VARIANT_LIB") else PKG / "libshtc.so"  # variant: tuning experiments only
 
 SHTC_OK, SHTC_EINVAL, SHTC_EDOMAIN, SHTC_ECUDA, SHTC_ENOMEM, SHTC_EUNSUPPORTED = range(6)
 

@@ -89,6 +89,29 @@ def build_dropin(force: bool = False) -> Path:
     return DROPIN_LIB
 
 
+def build_variant(name: str, defines: list[str]) -> Path:
+    """Tuning experiments: libshtc.so rebuilt with extra -D flags into _build/var_<name>/
+    (selected at run time with SHTC_VARIANT_LIB; never the shipped library)."""
+    d = OBJ / f"var_{name}"
+    d.mkdir(parents=True, exist_ok=True)
+    objs = []
+    jobs = []
+    for src in CU_SOURCES:
+        o = d / (src + ".o")
+        objs.append(o)
+        jobs.append([nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", str(ROOT / "include"), "-c",
+                     str(CSRC / src), "-o", str(o)])
+    with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
+        res = list(ex.map(_run, jobs))
+    (d / "ptxas.log").write_text("".join(r.stderr for r in res))
+    lib = d / "libshtc.so"
+    _run([nvcc(), "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lcudart"])
+    return lib
+
+
 if __name__ == "__main__":
+    if len(sys.argv) > 2 and sys.argv[1] == "variant":
+        print(build_variant(sys.argv[2], sys.argv[3:]))
+        sys.exit(0)
     build(verbose="-v" in sys.argv, force="-f" in sys.argv)
     print(LIB)

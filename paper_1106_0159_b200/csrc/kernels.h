@@ -31,10 +31,19 @@ struct LegTables {
 };
 
 // Tile = LEG_TILE consecutive streams handled by one warp (32 lanes x LEG_R streams).
-constexpr int LEG_R = 4;
+#ifndef LEG_R_DEF
+#define LEG_R_DEF 4
+#endif
+constexpr int LEG_R = LEG_R_DEF;
 constexpr int LEG_TILE = 32 * LEG_R;
 constexpr int LEG_WARPS = 4;      // warps per block of the persistent Legendre kernels
 constexpr int LEG_CL = 32;        // degree steps staged per chunk (one entry per lane)
+#ifndef LEG_A2M_MINB
+#define LEG_A2M_MINB 3  // resident CTAs per SM the alm2map kernel is compiled for
+#endif
+#ifndef LEG_M2A_MINB
+#define LEG_M2A_MINB 4
+#endif
 constexpr int LEG_M2A_GROUP = 4;  // tiles per map2alm work item (partials reduce G-fold)
 
 // One warp-sized unit of work of the persistent kernels.

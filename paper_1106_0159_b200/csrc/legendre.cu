@@ -296,7 +296,7 @@ __device__ __forceinline__ void a2m_enter_fast(A2MLane<R>& L) {
 }  // namespace
 
 template <int R>
-__global__ void __launch_bounds__(LEG_WARPS * 32, 3)
+__global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
     leg_alm2map_kernel(LegPlanView p, const double2* __restrict__ alm, double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, int* __restrict__ counter) {
     __shared__ CoefSoA sm_all[LEG_WARPS];
@@ -502,7 +502,7 @@ namespace {
 template <int R>
 struct M2ALane {
     double x[R], q0[R], q1[R];
-    double2 ds[R], dd[R];  // masked (zero until activation) north+south / north-south
+    double2 ds[R], dd[R];  // north+south / north-south ring Delta of the lane's streams
     int k[R];
 };
 
@@ -531,18 +531,19 @@ __device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, const Coef& cf, const
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
+        double qa = q2;  // the term's value: masked to zero while the ladder scale k != 0
         if (PH != FAST) {
             if (fabs(q2) >= cf.T) {
                 q2 *= SCALE_DOWN;
                 L.q1[r] *= SCALE_DOWN;
-                if (++L.k[r] == 0)
-                    m2a_load_d(L.ds[r], L.dd[r], tile * (32 * R) + r * 32 + lane, p, delta, row_off, mi);
+                ++L.k[r];
             }
+            qa = L.k[r] == 0 ? q2 : 0.0;
         }
         if (PH != PREFIX) {
             const double2 d = ODD ? L.dd[r] : L.ds[r];
-            part.x = __fma_rn(d.x, q2, part.x);
-            part.y = __fma_rn(d.y, q2, part.y);
+            part.x = __fma_rn(d.x, qa, part.x);
+            part.y = __fma_rn(d.y, qa, part.y);
         }
         L.q0[r] = L.q1[r];
         L.q1[r] = q2;
@@ -570,7 +571,7 @@ struct M2AWarpSmem {
 }  // namespace
 
 template <int R>
-__global__ void __launch_bounds__(LEG_WARPS * 32, 4)
+__global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
                        int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
@@ -624,7 +625,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                 L.q1[r] = valid ? mant : 0.0;
                 L.k[r] = k;
                 L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-                if (valid && k == 0) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
+                if (valid) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
             }
             bool fast = false;
 
@@ -688,8 +689,9 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, 4)
                                     // seed term (degree offset 0): no recurrence step
 #pragma unroll
                                     for (int r = 0; r < R; ++r) {
-                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
-                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
+                                        const double qa = L.k[r] == 0 ? L.q1[r] : 0.0;
+                                        v1.x = __fma_rn(L.ds[r].x, qa, v1.x);
+                                        v1.y = __fma_rn(L.ds[r].y, qa, v1.y);
                                     }
                                 } else {
                                     v1 = m2a_step<R, CHECKED, false>(L, sm.cf.get(g + u), p, delta, row_off, mi, tile, lane);

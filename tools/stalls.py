@@ -34,9 +34,12 @@ def main():
                           "--kernel-name", "regex:" + a.kernel], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
-    data = [r for r in rows[2:] if len(r) == len(h)]
-    if len(data) % 2 == 0 and data and data[0][1] == data[len(data) // 2][1]:
-        data = data[: len(data) // 2]
+    data = []
+    for r in rows[2:]:  # first captured launch only
+        if r and r[0] == "Kernel Name":
+            break
+        if len(r) == len(h):
+            data.append(r)
     si = h.index("Warp Stall Sampling (All Samples)")
     ei = h.index("Instructions Executed")
     ci = {c: h.index(c) for c in COLS if c in h}
