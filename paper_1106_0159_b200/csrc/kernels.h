@@ -70,24 +70,22 @@ struct LegPlanView {
     int n_a2m_items;
     const LegItem* m2a_items;  // cost-descending
     int n_m2a_items;
-    const double2* ck_q;       // [n_m * st.n] (Q_{ic-2}, Q_{ic-1}) at the tile start ic
-    const int* ck_k;           // [n_m * st.n] ladder scale at the tile start
+    const double2* ck_q;       // [n_m * st.n] (Q_{act-1}, Q_act) at activation, k == 0 scale
+    const int* ck_act;         // [n_m * st.n] activation step (0: seed; INT_MAX: dead)
     const int* m2a_items_per_m;     // [n_m]
     const int64_t* m2a_slot_base;   // [n_m] double2 offset of the order's first partial slot
     int64_t m2a_scratch_elems;
 };
 
 void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s);
-// activation degree offset per (order, stream); INT_MAX = dead stream.
-void launch_leg_scan(const LegPlanView& p, int* act_dev, cudaStream_t s);
+// activation degree offset per (order, stream) (INT_MAX = dead stream) and the recurrence
+// state right after it (same arithmetic as the reference's prefix, so bit-identical).
+void launch_leg_scan(const LegPlanView& p, int* act_dev, double2* ck_dev, cudaStream_t s);
 // per (order, tile) activation window and useful-step totals.
 void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* tile_info_dev,
                              unsigned long long* useful_dev, cudaStream_t s);
 
-// Recurrence state at the first (even) degree offset ic = i_s & ~1 of every tile whose
-// activation window starts at i_s >= 2: the kernels resume there instead of re-running the
-// prefix (same arithmetic as the prefix steps, so the resumed stream is bit-identical).
-void launch_leg_checkpoint(const LegPlanView& p, double2* ck_q, int* ck_k, cudaStream_t s);
+// A tile's run starts at the even step ic = i_s & ~1 (i_s: its first activation).
 __host__ __device__ inline int leg_tile_start(int is) { return is >= 2 ? (is & ~1) : 0; }
 
 // Delta rows: element (ring r, order index mi) at delta[row_off[r] + mi].

@@ -14,18 +14,19 @@
 //     is Q_l = (A_l x) Q_{l-1} - Q_{l-2}: 1 DMUL + 1 DFMA, plus 2 DFMA to accumulate
 //     (8 algorithmic flops in 4 FP64 pipe instructions).  c_l is folded into a_lm when it is
 //     staged (alm2map) or applied once per l after the ring reduction (map2alm).
-//   * the reference ladder is tracked exactly in the Q domain: a lane rescales when
-//     |Q| >= T_l = 2^512 / c_l (== |P mantissa| >= 2^512) and its terms count from the step
-//     where k reaches 0 ("activation").  A plan-time scan records the activation step of every
-//     (order, stream); tiles whose streams never activate are skipped, steps before the first
-//     activation of a tile run without accumulation, steps after the last activation run
-//     without any check.
+//   * the reference ladder is reproduced exactly at plan time: a scan runs every (order,
+//     stream) through the reference's prefix (rescale when |Q| >= T_l = 2^512 / c_l, i.e.
+//     |P mantissa| >= 2^512) and records the step where its scale k reaches 0 ("activation")
+//     and the state (Q_{act-1}, Q_act) there.  Before activation the reference drops every
+//     term, after it no rescale happens, so the kernels keep a lane at zero until its
+//     activation step, inject the recorded state there and never test the ladder.  Tiles with
+//     no activating stream are skipped; a tile's run starts at its first activation.
 //   * persistent, warp-independent kernels: each warp pulls (order, tile of 32 x R
 //     latitude-contiguous streams) items from a cost-sorted queue and stages the order's
 //     coefficients (and c_l-scaled a_lm) in its own shared-memory slice LEG_CL degrees at a
 //     time, so no block-wide barrier couples warps that sit in different phases.
 //   * map2alm reduces over the 32 x R streams of a warp through a shared-memory transpose every
-//     8 degrees, accumulates up to LEG_M2A_GROUP tiles per work item into a scratch slot, and
+//     16 degrees, accumulates up to LEG_M2A_GROUP tiles per work item into a scratch slot, and
 //     the last item of an order to finish sums the order's slots in a fixed order (no atomics
 //     on data, bitwise reproducible).
 
@@ -115,7 +116,7 @@ void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cuda
 // Plan: activation scan.  act = 0 for seeds already at k == 0, i for the step whose value
 // brings k to 0, INT_MAX if the stream never reaches k == 0 (all terms dropped).
 // ---------------------------------------------------------------------------------------
-__global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out) {
+__global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out, double2* __restrict__ ck_out) {
     const int mi = blockIdx.y;
     const int m = p.ms[mi];
     const int n = p.lmax - m;
@@ -128,6 +129,7 @@ __global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out) {
         seed_value(m, p.log_mu[m], p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, q1, k);
     }
     int act = (valid && k == 0) ? 0 : INT_MAX;
+    double2 ck = make_double2(0.0, act == 0 ? q1 : 0.0);  // state at activation (k == 0 scale)
     bool done = !valid || k == 0;
     const double* __restrict__ A = p.tab.A + p.tab.tab_off[mi];
     const double* __restrict__ T = p.tab.T + p.tab.tab_off[mi];
@@ -141,17 +143,21 @@ __global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out) {
             if (k == 0) {
                 act = i;
                 done = true;
+                ck = make_double2(q1, q2);
             }
         }
         q0 = q1;
         q1 = q2;
     }
-    if (valid) act_out[(size_t)mi * p.st.n + s] = act;
+    if (valid) {
+        act_out[(size_t)mi * p.st.n + s] = act;
+        ck_out[(size_t)mi * p.st.n + s] = ck;
+    }
 }
 
-void launch_leg_scan(const LegPlanView& p, int* act_dev, cudaStream_t s) {
+void launch_leg_scan(const LegPlanView& p, int* act_dev, double2* ck_dev, cudaStream_t s) {
     dim3 grid((p.st.n + 127) / 128, p.n_m);
-    leg_scan_kernel<<<grid, 128, 0, s>>>(p, act_dev);
+    leg_scan_kernel<<<grid, 128, 0, s>>>(p, act_dev, ck_dev);
 }
 
 __global__ void leg_tile_summary_kernel(LegPlanView p, const int* __restrict__ act,
@@ -183,68 +189,35 @@ void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* til
                                                               useful_dev);
 }
 
-__global__ void leg_checkpoint_kernel(LegPlanView p, double2* __restrict__ ck_q, int* __restrict__ ck_k) {
-    const int mi = blockIdx.y;
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= p.st.n) return;
-    const int is = p.tile_info[(size_t)mi * p.n_tiles + s / LEG_TILE].x;
-    const int ic = leg_tile_start(is);
-    if (ic < 2) return;
-    const int m = p.ms[mi];
-    const double x = p.st.x[s];
-    double q1 = 0.0, q0 = 0.0;
-    int k = 0;
-    seed_value(m, p.log_mu[m], p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, q1, k);
-    const double* __restrict__ A = p.tab.A + p.tab.tab_off[mi];
-    const double* __restrict__ T = p.tab.T + p.tab.tab_off[mi];
-    for (int i = 1; i < ic; ++i) {  // the PREFIX steps of the kernels, verbatim
-        double q2 = rec_step(__ldg(A + i), x, q1, q0);
-        if (fabs(q2) >= __ldg(T + i)) {
-            q2 *= SCALE_DOWN;
-            q1 *= SCALE_DOWN;
-            ++k;
-        }
-        q0 = q1;
-        q1 = q2;
-    }
-    ck_q[(size_t)mi * p.st.n + s] = make_double2(q0, q1);
-    ck_k[(size_t)mi * p.st.n + s] = k;
-}
-
-void launch_leg_checkpoint(const LegPlanView& p, double2* ck_q, int* ck_k, cudaStream_t s) {
-    dim3 grid((p.st.n + 127) / 128, p.n_m);
-    leg_checkpoint_kernel<<<grid, 128, 0, s>>>(p, ck_q, ck_k);
-}
-
 // ---------------------------------------------------------------------------------------
 // Persistent, warp-independent Legendre kernels.  Every warp pulls (order, tile) items from a
-// cost-sorted queue, stages the order's coefficients for LEG_CL degrees at a time in its own
-// shared-memory slice (no block barriers), and runs the three phases per degree pair:
-//   PREFIX  (both steps before the tile's first activation): recurrence + ladder check
-//   CHECKED (activation window of the tile): + accumulation, + per-lane activation
-//   FAST    (after the tile's last activation): recurrence + accumulation only
+// cost-sorted queue and stages the order's coefficients (and c_l-scaled a_lm) for LEG_CL
+// degrees at a time in its own shared-memory slice (no block barriers).
+//
+// Activation injection: a lane is zero (Q = 0, so it adds nothing) until its activation step
+// act, where its state becomes the plan-time value (Q_{act-1}, Q_act) in the k == 0 scale --
+// exactly the reference's state at the point its terms start to count.  The run of a tile
+// starts at ic = i_s & ~1 (i_s = its first activation); steps up to the tile's last activation
+// i_e test warp-uniformly for the next activation event, later steps are plain recurrence +
+// accumulation.  No ladder check runs in the kernels.
 // ---------------------------------------------------------------------------------------
 namespace {
 
-enum Phase { PREFIX = 0, CHECKED = 1, FAST = 2 };
-
 struct Coef {
-    double A, T, ar, ai;  // recurrence coefficient, ladder threshold, staged a_lm * c_l
+    double A, ar, ai;  // recurrence coefficient, staged a_lm * c_l
 };
 
 // Per-warp staging, structure of arrays so a group of steps loads with 16-byte LDS.
 struct __align__(16) CoefSoA {
     double A[LEG_CL];
-    double T[LEG_CL];
     double ar[LEG_CL];
     double ai[LEG_CL];
     __device__ __forceinline__ void put(int j, const Coef& c) {
         A[j] = c.A;
-        T[j] = c.T;
         ar[j] = c.ar;
         ai[j] = c.ai;
     }
-    __device__ __forceinline__ Coef get(int j) const { return Coef{A[j], T[j], ar[j], ai[j]}; }
+    __device__ __forceinline__ Coef get(int j) const { return Coef{A[j], ar[j], ai[j]}; }
 };
 
 __device__ __forceinline__ int warp_next_item(int* counter) {
@@ -253,44 +226,81 @@ __device__ __forceinline__ int warp_next_item(int* counter) {
     return __shfl_sync(0xffffffffu, it, 0);
 }
 
+// next activation step after i over the warp's lanes and streams (INT_MAX: none)
+template <int R>
+__device__ __forceinline__ int next_activation(const int (&act)[R], int i) {
+    int m = INT_MAX;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+        if (act[r] > i) m = min(m, act[r]);
+    return __reduce_min_sync(0xffffffffu, m);
+}
+
+// Lane setup shared by both kernels: zero state, activation steps, checkpoints staged in smem;
+// seed lanes (act == 0) start from their checkpoint (0, P_mm).
+template <int R>
+__device__ __forceinline__ void lanes_setup(const LegPlanView& p, int mi, int tile, int lane,
+                                            double (&x)[R], double (&q0)[R], double (&q1)[R],
+                                            int (&act)[R], double2 (*ck)[32]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int s = tile * (32 * R) + r * 32 + lane;
+        x[r] = 0.0;
+        q0[r] = q1[r] = 0.0;
+        act[r] = INT_MAX;
+        if (s < p.st.n) {
+            const size_t o = (size_t)mi * p.st.n + s;
+            x[r] = p.st.x[s];
+            act[r] = p.ck_act[o];
+            const double2 c = p.ck_q[o];
+            ck[r][lane] = c;
+            if (act[r] == 0) {
+                q0[r] = c.x;
+                q1[r] = c.y;
+            }
+        }
+    }
+}
+
 template <int R>
 struct A2MLane {
     double x[R], q0[R], q1[R];
     double2 ae[R], ao[R];  // even / odd degree-offset accumulators
-    int k[R];
+    int act[R];
 };
 
-template <int R, int PH, bool ODD>
+// plain step: recurrence + accumulation
+template <int R, bool ODD>
 __device__ __forceinline__ void a2m_step(A2MLane<R>& L, const Coef& cf) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
-        if (PH != FAST) {
-            if (fabs(q2) >= cf.T) {
-                q2 *= SCALE_DOWN;
-                L.q1[r] *= SCALE_DOWN;
-                if (++L.k[r] == 0) {
-                    // activation: every earlier term had k < 0 and is dropped by the reference
-                    L.ae[r] = make_double2(0.0, 0.0);
-                    L.ao[r] = make_double2(0.0, 0.0);
-                }
-            }
-        }
-        if (PH != PREFIX) {
-            double2& acc = ODD ? L.ao[r] : L.ae[r];
-            acc.x = __fma_rn(cf.ar, q2, acc.x);
-            acc.y = __fma_rn(cf.ai, q2, acc.y);
-        }
+        const double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
+        double2& acc = ODD ? L.ao[r] : L.ae[r];
+        acc.x = __fma_rn(cf.ar, q2, acc.x);
+        acc.y = __fma_rn(cf.ai, q2, acc.y);
         L.q0[r] = L.q1[r];
         L.q1[r] = q2;
     }
 }
 
-template <int R>
-__device__ __forceinline__ void a2m_enter_fast(A2MLane<R>& L) {
+// step i where some lanes activate: their (Q_{i-1}, Q_i) come from the checkpoint
+template <int R, bool ODD>
+__device__ __forceinline__ void a2m_step_act(A2MLane<R>& L, const Coef& cf, int i,
+                                             const double2 (*ck)[32], int lane) {
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-        if (L.k[r] != 0) L.q0[r] = L.q1[r] = 0.0;  // dead lanes: keep them finite and silent
+    for (int r = 0; r < R; ++r) {
+        double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
+        if (L.act[r] == i) {
+            const double2 c = ck[r][lane];
+            L.q1[r] = c.x;
+            q2 = c.y;
+        }
+        double2& acc = ODD ? L.ao[r] : L.ae[r];
+        acc.x = __fma_rn(cf.ar, q2, acc.x);
+        acc.y = __fma_rn(cf.ai, q2, acc.y);
+        L.q0[r] = L.q1[r];
+        L.q1[r] = q2;
+    }
 }
 
 }  // namespace
@@ -299,9 +309,14 @@ template <int R>
 __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
     leg_alm2map_kernel(LegPlanView p, const double2* __restrict__ alm, double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, int* __restrict__ counter) {
-    __shared__ CoefSoA sm_all[LEG_WARPS];
+    struct WarpSmem {
+        CoefSoA cf;
+        double2 ck[R][32];
+    };
+    __shared__ WarpSmem sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    CoefSoA& sm = sm_all[warp];
+    CoefSoA& sm = sm_all[warp].cf;
+    double2(*ck)[32] = sm_all[warp].ck;
 
     for (;;) {
         const int it = warp_next_item(counter);
@@ -313,50 +328,34 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
         const int64_t toff = p.tab.tab_off[mi];
         const double* __restrict__ gA = p.tab.A + toff;
         const double* __restrict__ gC = p.tab.C + toff;
-        const double* __restrict__ gT = p.tab.T + toff;
         const double2* __restrict__ galm = alm + alm_offset(m, p.lmax);
         const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
         const int is = info.x, ie = info.y;
-        const double lmu = p.log_mu[m];
-        const double2 a0 = galm[0];
+        const int ic = leg_tile_start(is);  // first step of the run (0: seeds)
 
-        const int ic = leg_tile_start(is);  // resume point (0: from the seed)
         A2MLane<R> L;
+        __syncwarp();
+        lanes_setup<R>(p, mi, tile, lane, L.x, L.q0, L.q1, L.act, ck);
+        const double2 a0 = galm[0];
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int s = tile * (32 * R) + r * 32 + lane;
-            double mant = 0.0, x = 0.0, q0 = 0.0;
-            int k = 0;
-            if (s < p.st.n) {
-                x = p.st.x[s];
-                if (ic) {
-                    const double2 q = p.ck_q[(size_t)mi * p.st.n + s];
-                    q0 = q.x;
-                    mant = q.y;
-                    k = p.ck_k[(size_t)mi * p.st.n + s];
-                } else {
-                    seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
-                }
-            }
-            L.x[r] = x;
-            L.q0[r] = q0;
-            L.q1[r] = mant;
-            L.k[r] = k;
-            // degree offset 0 term: a_mm P_mm (c_0 = 1), only when the seed is already at k == 0
-            L.ae[r] = (k == 0 && !ic) ? make_double2(a0.x * mant, a0.y * mant) : make_double2(0.0, 0.0);
+            // degree offset 0 term: a_mm P_mm (c_0 = 1) of lanes active from the seed
+            L.ae[r] = make_double2(a0.x * L.q1[r], a0.y * L.q1[r]);
             L.ao[r] = make_double2(0.0, 0.0);
         }
-        bool fast = false;
+        __syncwarp();
+        int ev = next_activation<R>(L.act, ic - 1 + (ic == 0));  // ic == 0: seeds are set
         if (ic) {
             // the even step ic on its own, then (odd, even) pairs from ic + 1
-            Coef c0;
             const double cc = gC[ic];
             const double2 v = galm[ic];
-            c0.A = gA[ic];
-            c0.T = gT[ic];
-            c0.ar = v.x * cc;
-            c0.ai = v.y * cc;
-            a2m_step<R, CHECKED, false>(L, c0);
+            const Coef c0{gA[ic], v.x * cc, v.y * cc};
+            if (ic == ev) {
+                a2m_step_act<R, false>(L, c0, ic, ck, lane);
+                ev = next_activation<R>(L.act, ic);
+            } else {
+                a2m_step<R, false>(L, c0);
+            }
         }
         const int i_first = ic + 1;
 
@@ -364,7 +363,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
         // raw loads are held in registers across the current chunk's steps; the c_l scaling
         // happens at staging time so no math waits on the prefetch.
         struct Raw {
-            double A, T, C;
+            double A, C;
             double2 v;
         };
         auto fetch = [&](int c, Raw& rw) {
@@ -373,11 +372,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
                 rw.C = gC[i];
                 rw.v = galm[i];
                 rw.A = gA[i];
-                rw.T = gT[i];
             } else {
-                rw.A = 0.0;
-                rw.T = 0x1p1000;
-                rw.C = 0.0;
+                rw.A = rw.C = 0.0;
                 rw.v = make_double2(0.0, 0.0);
             }
         };
@@ -386,56 +382,58 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
         if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
             __syncwarp();
-            sm.put(lane, Coef{nxt.A, nxt.T, nxt.v.x * nxt.C, nxt.v.y * nxt.C});
+            sm.put(lane, Coef{nxt.A, nxt.v.x * nxt.C, nxt.v.y * nxt.C});
             __syncwarp();
             if (c + 1 < nchunks) fetch(c + 1, nxt);
             const int i0 = i_first + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
             const int cnt = min(LEG_CL, n - i0 + 1);
             int j = 0;
-            if (!fast) {
-                for (; j + 1 < cnt; j += 2) {
-                    const int i = i0 + j;
-                    if (i > ie) break;
-                    const Coef c1 = sm.get(j), c2 = sm.get(j + 1);
-                    if (i + 1 < is) {
-                        a2m_step<R, PREFIX, true>(L, c1);
-                        a2m_step<R, PREFIX, false>(L, c2);
-                    } else {
-                        a2m_step<R, CHECKED, true>(L, c1);
-                        a2m_step<R, CHECKED, false>(L, c2);
-                    }
+            // activation window: pairs with a warp-uniform test for the next activation
+            for (; j + 1 < cnt && i0 + j <= ie; j += 2) {
+                const int i = i0 + j;
+                const Coef c1 = sm.get(j), c2 = sm.get(j + 1);
+                if (i == ev) {
+                    a2m_step_act<R, true>(L, c1, i, ck, lane);
+                    ev = next_activation<R>(L.act, i);
+                } else {
+                    a2m_step<R, true>(L, c1);
                 }
-                if (j < cnt && i0 + j > ie) {
-                    fast = true;
-                    a2m_enter_fast<R>(L);
+                if (i + 1 == ev) {
+                    a2m_step_act<R, false>(L, c2, i + 1, ck, lane);
+                    ev = next_activation<R>(L.act, i + 1);
+                } else {
+                    a2m_step<R, false>(L, c2);
                 }
             }
-            if (fast) {
-                for (; j + 8 <= cnt; j += 8) {
-                    // the group's coefficients up front (16-byte loads; j is even)
-                    Coef cg[8];
+            // after the last activation: groups of 8 steps, coefficients loaded up front
+            for (; j + 8 <= cnt; j += 8) {
+                Coef cg[8];
 #pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
-                        const double2 a = *reinterpret_cast<const double2*>(&sm.A[j + u]);
-                        const double2 xr = *reinterpret_cast<const double2*>(&sm.ar[j + u]);
-                        const double2 xi = *reinterpret_cast<const double2*>(&sm.ai[j + u]);
-                        cg[u] = Coef{a.x, 0.0, xr.x, xi.x};
-                        cg[u + 1] = Coef{a.y, 0.0, xr.y, xi.y};
-                    }
+                for (int u = 0; u < 8; u += 2) {
+                    const double2 a = *reinterpret_cast<const double2*>(&sm.A[j + u]);
+                    const double2 xr = *reinterpret_cast<const double2*>(&sm.ar[j + u]);
+                    const double2 xi = *reinterpret_cast<const double2*>(&sm.ai[j + u]);
+                    cg[u] = Coef{a.x, xr.x, xi.x};
+                    cg[u + 1] = Coef{a.y, xr.y, xi.y};
+                }
 #pragma unroll
-                    for (int u = 0; u < 8; u += 2) {
-                        a2m_step<R, FAST, true>(L, cg[u]);
-                        a2m_step<R, FAST, false>(L, cg[u + 1]);
-                    }
+                for (int u = 0; u < 8; u += 2) {
+                    a2m_step<R, true>(L, cg[u]);
+                    a2m_step<R, false>(L, cg[u + 1]);
                 }
-                for (; j + 1 < cnt; j += 2) {
-                    a2m_step<R, FAST, true>(L, sm.get(j));
-                    a2m_step<R, FAST, false>(L, sm.get(j + 1));
-                }
+            }
+            for (; j + 1 < cnt; j += 2) {
+                a2m_step<R, true>(L, sm.get(j));
+                a2m_step<R, false>(L, sm.get(j + 1));
             }
             if (j < cnt) {  // trailing odd step (last chunk only)
-                if (fast) a2m_step<R, FAST, true>(L, sm.get(j));
-                else a2m_step<R, CHECKED, true>(L, sm.get(j));
+                const int i = i0 + j;
+                if (i == ev) {
+                    a2m_step_act<R, true>(L, sm.get(j), i, ck, lane);
+                    ev = next_activation<R>(L.act, i);
+                } else {
+                    a2m_step<R, true>(L, sm.get(j));
+                }
             }
         }
 
@@ -443,8 +441,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
         for (int r = 0; r < R; ++r) {
             const int s = tile * (32 * R) + r * 32 + lane;
             if (s >= p.st.n) continue;
-            double2 e = L.ae[r], o = L.ao[r];
-            if (L.k[r] != 0) e = o = make_double2(0.0, 0.0);
+            const double2 e = L.ae[r], o = L.ao[r];  // dead lanes stayed zero
             const int north = p.st.north[s], south = p.st.south[s];
             delta[row_off[north] + mi] = cadd(e, o);
             if (south >= 0) delta[row_off[south] + mi] = csub(e, o);
@@ -503,7 +500,7 @@ template <int R>
 struct M2ALane {
     double x[R], q0[R], q1[R];
     double2 ds[R], dd[R];  // north+south / north-south ring Delta of the lane's streams
-    int k[R];
+    int act[R];
 };
 
 __device__ __forceinline__ void m2a_load_d(double2& ds, double2& dd, int s, const LegPlanView& p,
@@ -521,51 +518,51 @@ __device__ __forceinline__ void m2a_load_d(double2& ds, double2& dd, int s, cons
     }
 }
 
-// One step; returns the lane's contribution (re, im) summed over its R streams.
-template <int R, int PH, bool ODD>
-__device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, const Coef& cf, const LegPlanView& p,
-                                            const double2* __restrict__ delta,
-                                            const int64_t* __restrict__ row_off, int mi,
-                                            int tile, int lane) {
+// One plain step; returns the lane's contribution (re, im) summed over its R streams.
+template <int R, bool ODD>
+__device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, double A) {
     double2 part = make_double2(0.0, 0.0);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        double q2 = rec_step(cf.A, L.x[r], L.q1[r], L.q0[r]);
-        double qa = q2;  // the term's value: masked to zero while the ladder scale k != 0
-        if (PH != FAST) {
-            if (fabs(q2) >= cf.T) {
-                q2 *= SCALE_DOWN;
-                L.q1[r] *= SCALE_DOWN;
-                ++L.k[r];
-            }
-            qa = L.k[r] == 0 ? q2 : 0.0;
-        }
-        if (PH != PREFIX) {
-            const double2 d = ODD ? L.dd[r] : L.ds[r];
-            part.x = __fma_rn(d.x, qa, part.x);
-            part.y = __fma_rn(d.y, qa, part.y);
-        }
+        const double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
+        const double2 d = ODD ? L.dd[r] : L.ds[r];
+        part.x = __fma_rn(d.x, q2, part.x);
+        part.y = __fma_rn(d.y, q2, part.y);
         L.q0[r] = L.q1[r];
         L.q1[r] = q2;
     }
     return part;
 }
 
-template <int R>
-__device__ __forceinline__ void m2a_enter_fast(M2ALane<R>& L) {
+// step i where some lanes activate (checkpointed (Q_{i-1}, Q_i))
+template <int R, bool ODD>
+__device__ __forceinline__ double2 m2a_step_act(M2ALane<R>& L, double A, int i, const double2 (*ck)[32],
+                                                int lane) {
+    double2 part = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < R; ++r)
-        if (L.k[r] != 0) {
-            L.q0[r] = L.q1[r] = 0.0;
-            L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
+    for (int r = 0; r < R; ++r) {
+        double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
+        if (L.act[r] == i) {
+            const double2 c = ck[r][lane];
+            L.q1[r] = c.x;
+            q2 = c.y;
         }
+        const double2 d = ODD ? L.dd[r] : L.ds[r];
+        part.x = __fma_rn(d.x, q2, part.x);
+        part.y = __fma_rn(d.y, q2, part.y);
+        L.q0[r] = L.q1[r];
+        L.q1[r] = q2;
+    }
+    return part;
 }
 
 constexpr int M2A_G = 16;  // degrees per cross-lane reduction group
 
+template <int R>
 struct M2AWarpSmem {
-    CoefSoA cf;
+    double A[LEG_CL];
     double red[32][2 * M2A_G + 2];  // lane rows of (degree, re/im) partials, 16-byte aligned
+    double2 ck[R][32];              // activation checkpoints of the current tile
 };
 
 }  // namespace
@@ -576,9 +573,9 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
                        int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
     static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
-    __shared__ M2AWarpSmem sm_all[LEG_WARPS];
+    __shared__ M2AWarpSmem<R> sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    M2AWarpSmem& sm = sm_all[warp];
+    M2AWarpSmem<R>& sm = sm_all[warp];
     int* m_done = counters + 1;
 
     for (;;) {
@@ -590,65 +587,39 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
         const int n = p.lmax - m;
         const int64_t toff = p.tab.tab_off[mi];
         const double* __restrict__ gA = p.tab.A + toff;
-        const double* __restrict__ gT = p.tab.T + toff;
-        const double lmu = p.log_mu[m];
         double2* __restrict__ part_out = scratch + p.m2a_slot_base[mi] + (int64_t)item.g * (n + 1);
         for (int tt = 0; tt < item.b; ++tt) {
             const int tile = p.tile_list[item.a + tt];
             const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
-            const int is = info.x, ie = info.y;
-            const int ic = leg_tile_start(is);  // resume point (even; 0: from the seed)
+            const int ie = info.y;
+            const int ic = leg_tile_start(info.x);  // first step of the run (even; 0: seeds)
             const int nchunks = (n + 1 - ic + LEG_CL - 1) / LEG_CL;  // degree offsets ic..n
             if (tt == 0)  // degrees below the first tile's start get no other first write
                 for (int i = lane; i < ic; i += 32) part_out[i] = make_double2(0.0, 0.0);
             M2ALane<R> L;
+            __syncwarp();
+            lanes_setup<R>(p, mi, tile, lane, L.x, L.q0, L.q1, L.act, sm.ck);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 const int s = tile * (32 * R) + r * 32 + lane;
-                const bool valid = s < p.st.n;
-                double mant = 0.0, x = 0.0;
-                int k = 1;  // invalid lanes: never active
-                double q0 = 0.0;
-                if (valid) {
-                    x = p.st.x[s];
-                    if (ic) {
-                        const double2 q = p.ck_q[(size_t)mi * p.st.n + s];
-                        q0 = q.x;
-                        mant = q.y;
-                        k = p.ck_k[(size_t)mi * p.st.n + s];
-                    } else {
-                        seed_value(m, lmu, p.st.log2s2[s], p.st.s2pos[s], p.exp_lmu0, mant, k);
-                    }
-                }
-                L.x[r] = x;
-                L.q0[r] = q0;
-                L.q1[r] = valid ? mant : 0.0;
-                L.k[r] = k;
                 L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-                if (valid) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
+                if (s < p.st.n) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
             }
-            bool fast = false;
+            __syncwarp();
+            int ev = next_activation<R>(L.act, ic - 1 + (ic == 0));
 
-            auto fetch = [&](int c, Coef& cf) {
+            auto fetch = [&](int c) {
                 const int i = ic + c * LEG_CL + lane;
-                if (i <= n) {
-                    cf.A = gA[i];
-                    cf.T = gT[i];
-                } else {
-                    cf.A = 0.0;
-                    cf.T = 0x1p1000;
-                }
-                cf.ar = cf.ai = 0.0;
+                return i <= n ? gA[i] : 0.0;
             };
             // this lane's (degree, component) of the group in the scratch slot
             double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
-            Coef nxt;
-            fetch(0, nxt);
+            double nxt = fetch(0);
             for (int c = 0; c < nchunks; ++c) {
                 __syncwarp();
-                sm.cf.put(lane, nxt);
+                sm.A[lane] = nxt;
                 __syncwarp();
-                if (c + 1 < nchunks) fetch(c + 1, nxt);
+                if (c + 1 < nchunks) nxt = fetch(c + 1);
                 const int i0 = ic + c * LEG_CL;
                 const int cnt = min(LEG_CL, n - i0 + 1);
                 for (int g = 0; g < cnt; g += M2A_G) {
@@ -659,45 +630,41 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                     rmw_ptr += 2 * M2A_G;
                     // per-step lane contributions go straight to this lane's transpose row
                     double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
-                    bool any = true;
-                    if (!fast && ig > ie && ig > 0) {
-                        fast = true;
-                        m2a_enter_fast<R>(L);
-                    }
-                    if (fast && gc == M2A_G) {
-                        // straight-line steps, no checks; coefficients loaded in pairs
+                    if (ig > ie && gc == M2A_G) {
+                        // after the last activation: straight-line steps, coefficients in pairs
 #pragma unroll
                         for (int u = 0; u < M2A_G; u += 2) {
-                            const double2 a = *reinterpret_cast<const double2*>(&sm.cf.A[g + u]);
-                            row[u] = m2a_step<R, FAST, false>(L, Coef{a.x, 0.0, 0.0, 0.0}, p, delta, row_off, mi, tile, lane);
-                            row[u + 1] = m2a_step<R, FAST, true>(L, Coef{a.y, 0.0, 0.0, 0.0}, p, delta, row_off, mi, tile, lane);
-                        }
-                    } else if (ig > 0 && ig + gc < is) {
-                        // whole group before the tile's first activation: recurrence only
-                        any = false;
-                        for (int u = 0; u < gc; u += 2) {
-                            m2a_step<R, PREFIX, false>(L, sm.cf.get(g + u), p, delta, row_off, mi, tile, lane);
-                            if (u + 1 < gc)
-                                m2a_step<R, PREFIX, true>(L, sm.cf.get(g + u + 1), p, delta, row_off, mi, tile, lane);
+                            const double2 a = *reinterpret_cast<const double2*>(&sm.A[g + u]);
+                            row[u] = m2a_step<R, false>(L, a.x);
+                            row[u + 1] = m2a_step<R, true>(L, a.y);
                         }
                     } else {
-                        // generic (checked) path: activation window, the seed group, partial groups
+                        // activation window (warp-uniform event test per step), seed, partial group
                         for (int u = 0; u < M2A_G; u += 2) {
+                            const int i = ig + u;
                             double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
                             if (u < gc) {
-                                if (ig + u == 0) {
+                                if (i == 0) {
                                     // seed term (degree offset 0): no recurrence step
 #pragma unroll
                                     for (int r = 0; r < R; ++r) {
-                                        const double qa = L.k[r] == 0 ? L.q1[r] : 0.0;
-                                        v1.x = __fma_rn(L.ds[r].x, qa, v1.x);
-                                        v1.y = __fma_rn(L.ds[r].y, qa, v1.y);
+                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
+                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
                                     }
+                                } else if (i == ev) {
+                                    v1 = m2a_step_act<R, false>(L, sm.A[g + u], i, sm.ck, lane);
+                                    ev = next_activation<R>(L.act, i);
                                 } else {
-                                    v1 = m2a_step<R, CHECKED, false>(L, sm.cf.get(g + u), p, delta, row_off, mi, tile, lane);
+                                    v1 = m2a_step<R, false>(L, sm.A[g + u]);
                                 }
-                                if (u + 1 < gc)
-                                    v2 = m2a_step<R, CHECKED, true>(L, sm.cf.get(g + u + 1), p, delta, row_off, mi, tile, lane);
+                                if (u + 1 < gc) {
+                                    if (i + 1 == ev) {
+                                        v2 = m2a_step_act<R, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
+                                        ev = next_activation<R>(L.act, i + 1);
+                                    } else {
+                                        v2 = m2a_step<R, true>(L, sm.A[g + u + 1]);
+                                    }
+                                }
                             }
                             row[u] = v1;
                             row[u + 1] = v2;
@@ -705,25 +672,22 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                     }
                     // lane j reduces column j (degree ig + j/2, component j&1) over the 32 lane
                     // rows in a fixed order and accumulates it into the warp's scratch slot
-                    double v = 0.0;
-                    if (any) {
-                        __syncwarp();
-                        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                    __syncwarp();
+                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-                        for (int rr = 0; rr < 32; rr += 4) {
-                            s0 += sm.red[rr][lane];
-                            s1 += sm.red[rr + 1][lane];
-                            s2 += sm.red[rr + 2][lane];
-                            s3 += sm.red[rr + 3][lane];
-                        }
-                        v = (s0 + s1) + (s2 + s3);
+                    for (int rr = 0; rr < 32; rr += 4) {
+                        s0 += sm.red[rr][lane];
+                        s1 += sm.red[rr + 1][lane];
+                        s2 += sm.red[rr + 2][lane];
+                        s3 += sm.red[rr + 3][lane];
                     }
+                    const double v = (s0 + s1) + (s2 + s3);
                     __syncwarp();
                     // first tile stores; later tiles add in place (fire-and-forget reduction,
                     // a single lane owns each word so the order is the tile order)
                     if (iw <= n) {
                         if (tt == 0) *wp = v;
-                        else if (any) asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
+                        else asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
                     }
                 }
             }

@@ -103,7 +103,7 @@ struct LegPlan {
     std::vector<int> ms;
     std::vector<Stream> streams;
     DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
-        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_k;
+        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_act;
     uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
     // order chunks for the pipelined host-buffer paths: items sorted by (chunk, cost), chunk k
     // covers order indices [chunk_mi[k], chunk_mi[k+1]) and items [a2m_off[k], a2m_off[k+1])
@@ -292,14 +292,17 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     if (n_m > 0) launch_leg_tables(v.ms, n_m, lmax, v.tab, s);
     CK(cudaGetLastError());
 
-    DevBuf act;
-    act.ensure((size_t)n_m * ns * sizeof(int));
+    P.ck_act.ensure((size_t)std::max(1, n_m * ns) * sizeof(int));
+    P.ck_q.ensure((size_t)std::max(1, n_m * ns) * sizeof(double2));
+    v.ck_q = P.ck_q.as<double2>();
+    v.ck_act = P.ck_act.as<int>();
+    DevBuf& act = P.ck_act;
     P.tile_info.ensure((size_t)n_m * v.n_tiles * sizeof(int2));
     c->stats.ensure(sizeof(unsigned long long));
     CK(cudaMemsetAsync(c->stats.p, 0, sizeof(unsigned long long), s));
     v.tile_info = P.tile_info.as<int2>();
     if (n_m > 0) {
-        launch_leg_scan(v, act.as<int>(), s);
+        launch_leg_scan(v, act.as<int>(), P.ck_q.as<double2>(), s);
         CK(cudaGetLastError());
         launch_leg_tile_summary(v, act.as<int>(), P.tile_info.as<int2>(),
                                 c->stats.as<unsigned long long>(), s);
@@ -330,8 +333,8 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
             tl.push_back(t);
             a2m.push_back(LegItem{i, t, 0, 0});
             const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
-            // the kernels resume at ic (checkpointed state), run the activation window
-            // checked and everything after the last activation unchecked
+            // the kernels run from ic; steps up to the last activation test for activation
+            // events ("checked"), later steps are plain recurrence + accumulation
             const int ic = leg_tile_start(ti.x);
             const uint64_t run = (uint64_t)(n + 1 - ic);
             const uint64_t fst = std::min<uint64_t>(run, (uint64_t)std::max(0, n - std::max(ti.y, ic)));
@@ -396,14 +399,6 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.m2a_per_m.upload(per_m, s);
     P.m2a_slot.upload(slot, s);
     P.m2a_scratch.ensure((size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
-    P.ck_q.ensure((size_t)std::max(1, n_m * ns) * sizeof(double2));
-    P.ck_k.ensure((size_t)std::max(1, n_m * ns) * sizeof(int));
-    v.ck_q = P.ck_q.as<double2>();
-    v.ck_k = P.ck_k.as<int>();
-    if (n_m > 0) {
-        launch_leg_checkpoint(v, P.ck_q.as<double2>(), P.ck_k.as<int>(), s);
-        CK(cudaGetLastError());
-    }
     P.counters.ensure((size_t)(1 + n_m) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
