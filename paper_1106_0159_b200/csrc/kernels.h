@@ -92,7 +92,9 @@ __host__ __device__ inline int leg_tile_start(int is) { return is >= 2 ? (is & ~
 // counters: >= 1 + n_m ints of device scratch (zeroed by the launcher).
 // phases: bit0 = zero pass (dead tiles / orders without alive tiles), bit1 = the persistent
 // kernel over p's item list (callers may pass a view restricted to one chunk of items).
-constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3;
+// bit2 (map2alm) = keep the per-order completion counters of an earlier launch (the order's
+// work items are split over several launches; only the first one resets them).
+constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3, LEG_PHASE_KEEP_DONE = 4;
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
                         const int64_t* row_off, int* counters, cudaStream_t s,
                         int phases = LEG_PHASE_ALL);

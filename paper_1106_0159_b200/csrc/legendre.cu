@@ -747,7 +747,7 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
     int blocks = sms * (per > 0 ? per : 1);
     const int need = (p.n_m2a_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
-    cudaMemsetAsync(counters, 0, sizeof(int) * (1 + p.n_m), s);
+    cudaMemsetAsync(counters, 0, sizeof(int) * ((phases & LEG_PHASE_KEEP_DONE) ? 1 : 1 + p.n_m), s);
     leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, alm, accumulate,
                                                                 counters, scratch);
 }

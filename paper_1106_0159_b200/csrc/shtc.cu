@@ -103,11 +103,21 @@ struct LegPlan {
     std::vector<int> ms;
     std::vector<Stream> streams;
     DevBuf ms_d, logmu_d, sx, sl2, spos, sn, ss, tab_off, A, C, T, tile_info, tile_list, tile_off,
-        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_act;
+        tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_act,
+        a2m_items_band, m2a_items_band, m2a_per_m_band, m2a_slot_band;
     uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
-    // order chunks for the pipelined host-buffer paths: items sorted by (chunk, cost), chunk k
-    // covers order indices [chunk_mi[k], chunk_mi[k+1]) and items [a2m_off[k], a2m_off[k+1])
-    std::vector<int> chunk_mi, a2m_off, m2a_off;
+    // Pipelined host-buffer paths (see shtc_alm2map): latitude-band chunks of tiles, numbered
+    // from the equator.  alm2map launches: band tc's items (band 0 also split by order chunk
+    // mc so it can start while a_lm is still arriving); map2alm: band tc's items, after which
+    // the orders whose last item was in band tc are final (runs of order indices).
+    struct PipeLaunch {
+        int tc, mc, begin, end;
+    };
+    std::vector<int> chunk_mi;  // order chunk k = order indices [chunk_mi[k], chunk_mi[k+1])
+    std::vector<PipeLaunch> a2m_launch;  // ranges of the band-ordered item lists
+    LegPlanView band_view{};             // view with the band-ordered item lists
+    std::vector<int> m2a_off;   // band tc = m2a items [m2a_off[tc], m2a_off[tc+1])
+    std::vector<std::vector<std::pair<int, int>>> m2a_done;  // per band: final order-index runs
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
     double build_ms = 0.0;
@@ -119,10 +129,10 @@ struct FftPlan {
     bool built = false;
     DevBuf descs[FFT_N_CLASSES];
     int count[FFT_N_CLASSES] = {0, 0, 0, 0};
-    // ring ranges (contiguous pixels) for the pipelined paths: class c's descriptors of range k
-    // are [range_start[c][k], range_start[c][k+1]); range k covers pixels [range_pix[k], ..[k+1])
+    // latitude bands of the pipelined paths: class c's descriptors of band k are
+    // [range_start[c][k], range_start[c][k+1]); band k covers the pixel intervals band_pix[k]
     std::vector<int> range_start[FFT_N_CLASSES];
-    std::vector<int64_t> range_pix;
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> band_pix;
     DevBuf tabs;
     double build_ms = 0.0;
 };
@@ -166,7 +176,8 @@ struct shtc_ctx {
     cudaEvent_t ev[8] = {};
     // pipelined host-buffer paths
     cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t pev[3][kPipeChunks] = {};
+    cudaEvent_t pev[3][kPipeChunks] = {};  // ordering events of the copy streams
+    cudaEvent_t tev[3][kPipeChunks] = {};  // timing events of the pipelined segments
 };
 
 namespace {
@@ -235,6 +246,46 @@ void check_m_set(const int32_t* ms, int n, int mmax, const char* where) {
 // ---------------------------------------------------------------------------------------
 // Legendre plan
 // ---------------------------------------------------------------------------------------
+// latitude-coherent tiles: streams ordered by |x| descending (polar first)
+void sort_streams(std::vector<Stream>& streams) {
+    std::stable_sort(streams.begin(), streams.end(),
+                     [](const Stream& a, const Stream& b) { return std::fabs(a.x) > std::fabs(b.x); });
+}
+
+// Pipeline band of every tile of the sorted streams: contiguous tile ranges of ~equal pixel
+// counts, band 0 at the equator.
+std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
+    const int ns = (int)st.size();
+    const int nt = (ns + LEG_TILE - 1) / LEG_TILE;
+    std::vector<int64_t> pix(nt, 0);
+    int64_t total = 0;
+    for (int i = 0; i < ns; ++i) {
+        const int64_t p = c->nphi[st[i].north] + (st[i].south >= 0 ? c->nphi[st[i].south] : 0);
+        pix[i / LEG_TILE] += p;
+        total += p;
+    }
+    std::vector<int> band(nt);
+    int64_t acc = 0;
+    for (int t = 0; t < nt; ++t) {
+        const int polar = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
+        band[t] = kPipeChunks - 1 - polar;
+        acc += pix[t];
+    }
+    return band;
+}
+
+// band of every ring (-1: ring in no stream)
+std::vector<int> ring_bands(const shtc_ctx* c, std::vector<Stream> st) {
+    sort_streams(st);
+    const std::vector<int> tb = tile_bands(c, st);
+    std::vector<int> rb(c->n_rings, -1);
+    for (size_t i = 0; i < st.size(); ++i) {
+        rb[st[i].north] = tb[i / LEG_TILE];
+        if (st[i].south >= 0) rb[st[i].south] = tb[i / LEG_TILE];
+    }
+    return rb;
+}
+
 void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vector<int>& ms,
                     std::vector<Stream> streams, const std::vector<double>& log_mu) {
     cudaStream_t s = c->stream;
@@ -243,10 +294,9 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P = LegPlan();  // release previous
     P.lmax = lmax;
     P.ms = ms;
-    // latitude-coherent tiles: streams ordered by |x| descending (polar first)
-    std::stable_sort(streams.begin(), streams.end(),
-                     [](const Stream& a, const Stream& b) { return std::fabs(a.x) > std::fabs(b.x); });
+    sort_streams(streams);
     P.streams = streams;
+    const std::vector<int> tband = tile_bands(c, streams);
     const int ns = (int)streams.size();
     const int n_m = (int)ms.size();
     std::vector<double> sx(ns), sl2(ns);
@@ -317,20 +367,24 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.useful = useful;
 
     // alive tile lists per order and the cost-sorted work queues of the persistent kernels
+    // Two item sets: cost-ordered for the device-resident single launches, band-ordered for
+    // the pipelined host-buffer paths.  Tile lists run in descending tile index, i.e. bands in
+    // ascending order (band 0 = equator).
     std::vector<int> tl, toffs(n_m), tcnt(n_m);
-    std::vector<LegItem> a2m, m2a;
-    std::vector<int> per_m(n_m);
-    std::vector<int64_t> slot(n_m);
-    int64_t slots = 0;
+    std::vector<LegItem> a2m, m2a, m2a_b;
+    std::vector<int> per_m(n_m), per_m_b(n_m);
+    std::vector<int64_t> slot(n_m), slot_b(n_m);
+    int64_t slots = 0, slots_b = 0;
     P.nominal = P.executed = P.prefix_steps = P.checked_steps = P.fast_steps = 0;
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
         P.nominal += (uint64_t)(n + 1) * ns;
         toffs[i] = (int)tl.size();
+        std::vector<int> alive;
         for (int t = 0; t < v.n_tiles; ++t) {
             const int2 ti = info[(size_t)i * v.n_tiles + t];
             if (ti.x < 0) continue;
-            tl.push_back(t);
+            alive.push_back(t);
             a2m.push_back(LegItem{i, t, 0, 0});
             const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
             // the kernels run from ic; steps up to the last activation test for activation
@@ -342,14 +396,22 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
             P.fast_steps += fst * in_tile;
             P.checked_steps += (run - fst) * in_tile;
         }
-        tcnt[i] = (int)tl.size() - toffs[i];
-        per_m[i] = (tcnt[i] + LEG_M2A_GROUP - 1) / LEG_M2A_GROUP;
+        std::reverse(alive.begin(), alive.end());
+        tl.insert(tl.end(), alive.begin(), alive.end());
+        tcnt[i] = (int)alive.size();
+        // map2alm items: up to LEG_M2A_GROUP consecutive alive tiles (both sets share the
+        // grouping, so the summation order and the results are identical)
+        per_m[i] = 0;
+        for (size_t a = 0; a < alive.size(); a += LEG_M2A_GROUP)
+            m2a.push_back(LegItem{i, toffs[i] + (int)a, (int)std::min<size_t>(LEG_M2A_GROUP, alive.size() - a),
+                                  per_m[i]++});
         slot[i] = slots;
         slots += (int64_t)per_m[i] * (n + 1);
-        for (int g = 0; g < per_m[i]; ++g)
-            m2a.push_back(LegItem{i, toffs[i] + g * LEG_M2A_GROUP,
-                                  std::min(LEG_M2A_GROUP, tcnt[i] - g * LEG_M2A_GROUP), g});
     }
+    m2a_b = m2a;
+    per_m_b = per_m;
+    slot_b = slot;
+    slots_b = slots;
     // cost = degree steps actually run (from the tile's resume point)
     auto tile_cost = [&](int mi, int t) {
         return (int64_t)(lmax - ms[mi] + 1 - leg_tile_start(info[(size_t)mi * v.n_tiles + t].x));
@@ -374,21 +436,47 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         }
         while ((int)P.chunk_mi.size() <= kPipeChunks) P.chunk_mi.push_back(n_m);
     }
-    std::stable_sort(a2m.begin(), a2m.end(), [&](const LegItem& a, const LegItem& b) {
-        if (chunk_of[a.mi] != chunk_of[b.mi]) return chunk_of[a.mi] < chunk_of[b.mi];
+    std::stable_sort(a2m.begin(), a2m.end(),
+                     [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
+    std::stable_sort(m2a.begin(), m2a.end(),
+                     [&](const LegItem& a, const LegItem& b) { return m2a_cost(a) > m2a_cost(b); });
+    // alm2map band set: band, then (band 0 only) order chunk, then cost
+    auto a2m_key = [&](const LegItem& it) {
+        const int tc = tband[it.a];
+        return std::make_pair(tc, tc == 0 ? chunk_of[it.mi] : 0);
+    };
+    std::vector<LegItem> a2m_b = a2m;
+    std::stable_sort(a2m_b.begin(), a2m_b.end(), [&](const LegItem& a, const LegItem& b) {
+        if (a2m_key(a) != a2m_key(b)) return a2m_key(a) < a2m_key(b);
         return a2m_cost(a) > a2m_cost(b);
     });
-    std::stable_sort(m2a.begin(), m2a.end(), [&](const LegItem& a, const LegItem& b) {
-        if (chunk_of[a.mi] != chunk_of[b.mi]) return chunk_of[a.mi] < chunk_of[b.mi];
+    P.a2m_launch.clear();
+    for (size_t k = 0; k < a2m_b.size();) {
+        size_t e = k;
+        while (e < a2m_b.size() && a2m_key(a2m_b[e]) == a2m_key(a2m_b[k])) ++e;
+        P.a2m_launch.push_back({a2m_key(a2m_b[k]).first, a2m_key(a2m_b[k]).second, (int)k, (int)e});
+        k = e;
+    }
+    // map2alm band set: an item runs with the last band of its tiles (bands ascend along the
+    // tile list, so every tile's Delta rows are ready), then cost; an order is final after
+    // the band of its last item
+    auto m2a_band = [&](const LegItem& it) { return tband[tl[it.a + it.b - 1]]; };
+    std::stable_sort(m2a_b.begin(), m2a_b.end(), [&](const LegItem& a, const LegItem& b) {
+        if (m2a_band(a) != m2a_band(b)) return m2a_band(a) < m2a_band(b);
         return m2a_cost(a) > m2a_cost(b);
     });
-    P.a2m_off.assign(kPipeChunks + 1, 0);
     P.m2a_off.assign(kPipeChunks + 1, 0);
-    for (const auto& it : a2m) P.a2m_off[chunk_of[it.mi] + 1]++;
-    for (const auto& it : m2a) P.m2a_off[chunk_of[it.mi] + 1]++;
-    for (int k = 0; k < kPipeChunks; ++k) {
-        P.a2m_off[k + 1] += P.a2m_off[k];
-        P.m2a_off[k + 1] += P.m2a_off[k];
+    std::vector<int> last_band(n_m, 0);  // orders without items are final from the start
+    for (const auto& it : m2a_b) {
+        P.m2a_off[m2a_band(it) + 1]++;
+        last_band[it.mi] = std::max(last_band[it.mi], m2a_band(it));
+    }
+    for (int k = 0; k < kPipeChunks; ++k) P.m2a_off[k + 1] += P.m2a_off[k];
+    P.m2a_done.assign(kPipeChunks, {});
+    for (int i = 0; i < n_m; ++i) {
+        auto& runs = P.m2a_done[last_band[i]];
+        if (!runs.empty() && runs.back().second == i) runs.back().second = i + 1;
+        else runs.push_back({i, i + 1});
     }
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
@@ -398,7 +486,11 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.m2a_items.upload(m2a, s);
     P.m2a_per_m.upload(per_m, s);
     P.m2a_slot.upload(slot, s);
-    P.m2a_scratch.ensure((size_t)std::max<int64_t>(slots, 1) * sizeof(double2));
+    P.a2m_items_band.upload(a2m_b, s);
+    P.m2a_items_band.upload(m2a_b, s);
+    P.m2a_per_m_band.upload(per_m_b, s);
+    P.m2a_slot_band.upload(slot_b, s);
+    P.m2a_scratch.ensure((size_t)std::max<int64_t>(std::max(slots, slots_b), 1) * sizeof(double2));
     P.counters.ensure((size_t)(1 + n_m) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
@@ -409,7 +501,13 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     v.n_m2a_items = (int)m2a.size();
     v.m2a_items_per_m = P.m2a_per_m.as<int>();
     v.m2a_slot_base = P.m2a_slot.as<int64_t>();
-    v.m2a_scratch_elems = slots;
+    v.m2a_scratch_elems = std::max(slots, slots_b);
+    P.band_view = v;
+    P.band_view.a2m_items = P.a2m_items_band.as<LegItem>();
+    P.band_view.m2a_items = P.m2a_items_band.as<LegItem>();
+    P.band_view.n_m2a_items = (int)m2a_b.size();
+    P.band_view.m2a_items_per_m = P.m2a_per_m_band.as<int>();
+    P.band_view.m2a_slot_base = P.m2a_slot_band.as<int64_t>();
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float ms_el = 0.f;
@@ -439,7 +537,9 @@ void ensure_leg_plan(shtc_ctx* c) {
 // ---------------------------------------------------------------------------------------
 // Ring FFT plan
 // ---------------------------------------------------------------------------------------
-void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
+// ring_band: pipeline band per grid ring (bands of the host-buffer paths), or empty.
+void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
+                    const std::vector<int>& ring_band = {}) {
     cudaStream_t s = c->stream;
     cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
     CK(cudaEventRecord(e0, s));
@@ -515,30 +615,29 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings) {
             CK(cudaGetLastError());
             CK(cudaStreamSynchronize(s));
         }
-        F.descs[k].upload(per_class[k], s);
         F.count[k] = (int)per_class[k].size();
     }
-    // ring ranges of ~equal pixel counts (descriptors were appended in ring order)
+    // pipeline bands: descriptors of each class grouped by band (ring order inside a band),
+    // pixel intervals of each band for the host copies
     {
-        int64_t total = 0;
-        for (int r : rings) total += c->nphi[r];
-        std::vector<int> range_of_pos(rings.size());
-        std::vector<int> first_pos(kPipeChunks + 1, (int)rings.size());
-        int64_t acc = 0;
+        auto band = [&](const RingDesc& d) {
+            return ring_band.empty() ? 0 : std::max(0, ring_band[rings[d.ring_pos]]);
+        };
+        F.band_pix.assign(kPipeChunks, {});
         for (size_t pos = 0; pos < rings.size(); ++pos) {
-            const int k = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
-            range_of_pos[pos] = k;
-            first_pos[k] = std::min(first_pos[k], (int)pos);
-            acc += c->nphi[rings[pos]];
+            const int r = rings[pos];
+            const int k = ring_band.empty() ? 0 : std::max(0, ring_band[r]);
+            const int64_t b0 = c->pixoff[r], b1 = b0 + c->nphi[r];
+            auto& iv = F.band_pix[k];
+            if (!iv.empty() && iv.back().second == b0) iv.back().second = b1;
+            else iv.push_back({b0, b1});
         }
-        for (int k = kPipeChunks - 1; k >= 0; --k) first_pos[k] = std::min(first_pos[k], first_pos[k + 1]);
-        F.range_pix.assign(kPipeChunks + 1, 0);
-        for (int k = 0; k <= kPipeChunks; ++k)
-            F.range_pix[k] = first_pos[k] < (int)rings.size() ? c->pixoff[rings[first_pos[k]]]
-                                                                 : c->npix;
         for (int cls = 0; cls < FFT_N_CLASSES; ++cls) {
+            std::stable_sort(per_class[cls].begin(), per_class[cls].end(),
+                             [&](const RingDesc& a, const RingDesc& b) { return band(a) < band(b); });
+            F.descs[cls].upload(per_class[cls], s);
             F.range_start[cls].assign(kPipeChunks + 1, 0);
-            for (const RingDesc& d : per_class[cls]) F.range_start[cls][range_of_pos[d.ring_pos] + 1]++;
+            for (const RingDesc& d : per_class[cls]) F.range_start[cls][band(d) + 1]++;
             for (int k = 0; k < kPipeChunks; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
         }
     }
@@ -569,7 +668,7 @@ void ensure_fft_id(shtc_ctx* c) {
     if (!c->fft_id.built) {
         std::vector<int> all(c->n_rings);
         std::iota(all.begin(), all.end(), 0);
-        build_fft_plan(c, c->fft_id, all);
+        build_fft_plan(c, c->fft_id, all, ring_bands(c, grid_streams(c)));
     }
 }
 
@@ -733,6 +832,9 @@ void shtc_destroy(shtc_ctx* ctx) {
     for (auto& row : ctx->pev)
         for (auto& e : row)
             if (e) cudaEventDestroy(e);
+    for (auto& row : ctx->tev)
+        for (auto& e : row)
+            if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
@@ -847,11 +949,14 @@ shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_d
     return guarded(ctx, [&] { do_map2alm_dev(ctx, map_dev, alm_dev, t); });
 }
 
-// Host-buffer entry points, pipelined over kPipeChunks chunks on three streams:
-//   alm2map: H2D of a_lm order chunk k || Legendre of chunk k-1 ; ring stage of ring range r
-//            || D2H of the pixels of range r-1
-//   map2alm: H2D of ring range r || ring analysis of range r-1 ; Legendre of order chunk k
-//            || D2H of the a_lm of chunk k-1
+// Host-buffer entry points, pipelined over latitude bands (contiguous tile ranges of ~equal
+// pixel counts, see tile_bands) on three streams:
+//   alm2map: H2D of a_lm by order chunk || Legendre of band 0 by order chunk; then per band:
+//            Legendre (all orders, the band's rings) -> ring synthesis of the band's rings ->
+//            D2H of the band's pixels || the next band's Legendre
+//   map2alm: per band: H2D of the band's pixels || ring analysis + Legendre of the previous
+//            band; the orders whose last work item was in the band are final -> D2H of their
+//            a_lm || the next band
 // Same kernels and arithmetic as the device-resident path (results are bit-identical).
 namespace {
 void ensure_pipe(shtc_ctx* c) {
@@ -860,27 +965,38 @@ void ensure_pipe(shtc_ctx* c) {
     CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
     for (auto& row : c->pev)
         for (auto& e : row) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& row : c->tev)
+        for (auto& e : row) CK(cudaEventCreate(&e));
 }
 
-LegPlanView chunk_view(const LegPlan& P, int k, bool a2m) {
-    LegPlanView v = P.view;
+// band-ordered items [begin, end) of one pipelined launch
+LegPlanView items_view(const LegPlan& P, int begin, int end, bool a2m) {
+    LegPlanView v = P.band_view;
     if (a2m) {
-        v.a2m_items = P.view.a2m_items + P.a2m_off[k];
-        v.n_a2m_items = P.a2m_off[k + 1] - P.a2m_off[k];
+        v.a2m_items = P.band_view.a2m_items + begin;
+        v.n_a2m_items = end - begin;
     } else {
-        v.m2a_items = P.view.m2a_items + P.m2a_off[k];
-        v.n_m2a_items = P.m2a_off[k + 1] - P.m2a_off[k];
+        v.m2a_items = P.band_view.m2a_items + begin;
+        v.n_m2a_items = end - begin;
     }
     return v;
 }
 
-// complex-element range of order chunk k in the m-major a_lm triangle (full band)
-std::pair<size_t, size_t> alm_range(const shtc_ctx* c, const LegPlan& P, int k) {
+// complex-element range of order indices [mi0, mi1) in the m-major a_lm triangle (full band)
+std::pair<size_t, size_t> alm_span(const shtc_ctx* c, int mi0, int mi1) {
     auto off = [&](int mi) {
         return mi >= (int)c->ms.size() ? alm_count(c->lmax, c->mmax)
                                        : (size_t)alm_offset(c->ms[mi], c->lmax);
     };
-    return {off(P.chunk_mi[k]), off(P.chunk_mi[k + 1])};
+    return {off(mi0), off(mi1)};
+}
+
+void band_timing(shtc_ctx* c, float& first, float& second) {
+    first = second = 0.f;
+    for (int k = 0; k < kPipeChunks; ++k) {
+        first += elapsed(c->tev[0][k], c->tev[1][k]);
+        second += elapsed(c->tev[1][k], c->tev[2][k]);
+    }
 }
 }  // namespace
 
@@ -900,41 +1016,48 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         cudaStream_t s = ctx->stream;
         LegPlan& P = ctx->leg;
         FftPlan& F = ctx->fft_id;
+        double2* ab = ctx->alm_buf.as<double2>();
+        double* mb = ctx->map_buf.as<double>();
         CK(cudaEventRecord(ctx->ev[3], s));
         CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
         for (int k = 0; k < kPipeChunks; ++k) {
-            auto [b, e] = alm_range(ctx, P, k);
+            auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
             if (e > b)
-                CK(cudaMemcpyAsync(ctx->alm_buf.as<double2>() + b, reinterpret_cast<const double2*>(alm) + b,
-                                   (e - b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->h2d));
+                CK(cudaMemcpyAsync(ab + b, reinterpret_cast<const double2*>(alm) + b, (e - b) * sizeof(double2),
+                                   cudaMemcpyHostToDevice, ctx->h2d));
             CK(cudaEventRecord(ctx->pev[0][k], ctx->h2d));
         }
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
-        launch_leg_alm2map(P.view, ctx->alm_buf.as<double2>(), ctx->delta.as<double2>(), ro,
-                           P.counters.as<int>(), s, LEG_PHASE_ZERO);
-        for (int k = 0; k < kPipeChunks; ++k) {
-            CK(cudaStreamWaitEvent(s, ctx->pev[0][k], 0));
-            if (k == 0) CK(cudaEventRecord(ctx->ev[0], s));
-            launch_leg_alm2map(chunk_view(P, k, true), ctx->alm_buf.as<double2>(), ctx->delta.as<double2>(),
-                               ro, P.counters.as<int>(), s, LEG_PHASE_MAIN);
-            CK(cudaGetLastError());
-        }
-        CK(cudaEventRecord(ctx->ev[1], s));
-        for (int r = 0; r < kPipeChunks; ++r) {
-            run_ring_synth(ctx, F, ctx->delta.as<double2>(), ctx->map_buf.as<double>(), nullptr, nullptr, r);
-            CK(cudaEventRecord(ctx->pev[1][r], s));
-            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][r], 0));
-            const size_t pb = F.range_pix[r], pe = F.range_pix[r + 1];
-            if (pe > pb)
-                CK(cudaMemcpyAsync(map + pb, ctx->map_buf.as<double>() + pb, (pe - pb) * sizeof(double),
+        CK(cudaEventRecord(ctx->ev[0], s));
+        launch_leg_alm2map(P.view, ab, ctx->delta.as<double2>(), ro, P.counters.as<int>(), s, LEG_PHASE_ZERO);
+        size_t li = 0;
+        for (int tc = 0; tc < kPipeChunks; ++tc) {
+            CK(cudaEventRecord(ctx->tev[0][tc], s));
+            if (tc == 1) CK(cudaStreamWaitEvent(s, ctx->pev[0][kPipeChunks - 1], 0));
+            for (; li < P.a2m_launch.size() && P.a2m_launch[li].tc == tc; ++li) {
+                const auto& L = P.a2m_launch[li];
+                if (tc == 0) CK(cudaStreamWaitEvent(s, ctx->pev[0][L.mc], 0));
+                launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, ctx->delta.as<double2>(), ro,
+                                   P.counters.as<int>(), s, LEG_PHASE_MAIN);
+                CK(cudaGetLastError());
+            }
+            if (tc == 0) CK(cudaStreamWaitEvent(s, ctx->pev[0][kPipeChunks - 1], 0));
+            CK(cudaEventRecord(ctx->tev[1][tc], s));
+            run_ring_synth(ctx, F, ctx->delta.as<double2>(), mb, nullptr, nullptr, tc);
+            CK(cudaEventRecord(ctx->tev[2][tc], s));
+            CK(cudaEventRecord(ctx->pev[1][tc], s));
+            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][tc], 0));
+            for (const auto& iv : F.band_pix[tc])
+                CK(cudaMemcpyAsync(map + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
                                    cudaMemcpyDeviceToHost, ctx->d2h));
         }
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
         if (t) {
-            fill_timing(t, elapsed(ctx->ev[0], ctx->ev[1]), elapsed(ctx->ev[1], ctx->ev[2]),
-                        elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
+            float leg, fft;
+            band_timing(ctx, leg, fft);
+            fill_timing(t, leg, fft, elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
                         elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
@@ -956,41 +1079,48 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         cudaStream_t s = ctx->stream;
         LegPlan& P = ctx->leg;
         FftPlan& F = ctx->fft_id;
+        double2* ab = ctx->alm_buf.as<double2>();
+        double* mb = ctx->map_buf.as<double>();
         CK(cudaEventRecord(ctx->ev[3], s));
         CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
-        for (int r = 0; r < kPipeChunks; ++r) {
-            const size_t pb = F.range_pix[r], pe = F.range_pix[r + 1];
-            if (pe > pb)
-                CK(cudaMemcpyAsync(ctx->map_buf.as<double>() + pb, map + pb, (pe - pb) * sizeof(double),
+        for (int tc = 0; tc < kPipeChunks; ++tc) {
+            for (const auto& iv : F.band_pix[tc])
+                CK(cudaMemcpyAsync(mb + iv.first, map + iv.first, (iv.second - iv.first) * sizeof(double),
                                    cudaMemcpyHostToDevice, ctx->h2d));
-            CK(cudaEventRecord(ctx->pev[0][r], ctx->h2d));
+            CK(cudaEventRecord(ctx->pev[0][tc], ctx->h2d));
         }
-        for (int r = 0; r < kPipeChunks; ++r) {
-            CK(cudaStreamWaitEvent(s, ctx->pev[0][r], 0));
-            if (r == 0) CK(cudaEventRecord(ctx->ev[0], s));
-            run_ring_anal(ctx, F, ctx->map_buf.as<double>(), ctx->delta.as<double2>(), nullptr, nullptr, r);
-        }
-        CK(cudaEventRecord(ctx->ev[1], s));
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
-        launch_leg_map2alm(P.view, ctx->delta.as<double2>(), ro, ctx->alm_buf.as<double2>(), 0,
-                           P.counters.as<int>(), P.m2a_scratch.as<double2>(), s, LEG_PHASE_ZERO);
-        for (int k = 0; k < kPipeChunks; ++k) {
-            launch_leg_map2alm(chunk_view(P, k, false), ctx->delta.as<double2>(), ro, ctx->alm_buf.as<double2>(),
-                               0, P.counters.as<int>(), P.m2a_scratch.as<double2>(), s, LEG_PHASE_MAIN);
+        CK(cudaEventRecord(ctx->ev[0], s));
+        launch_leg_map2alm(P.view, ctx->delta.as<double2>(), ro, ab, 0, P.counters.as<int>(),
+                           P.m2a_scratch.as<double2>(), s, LEG_PHASE_ZERO);
+        // the order-completion counters run across the band launches: reset them once here
+        CK(cudaMemsetAsync(P.counters.p, 0, (1 + ctx->ms.size()) * sizeof(int), s));
+        for (int tc = 0; tc < kPipeChunks; ++tc) {
+            CK(cudaStreamWaitEvent(s, ctx->pev[0][tc], 0));
+            CK(cudaEventRecord(ctx->tev[0][tc], s));
+            run_ring_anal(ctx, F, mb, ctx->delta.as<double2>(), nullptr, nullptr, tc);
+            CK(cudaEventRecord(ctx->tev[1][tc], s));
+            launch_leg_map2alm(items_view(P, P.m2a_off[tc], P.m2a_off[tc + 1], false), ctx->delta.as<double2>(),
+                               ro, ab, 0, P.counters.as<int>(), P.m2a_scratch.as<double2>(), s,
+                               LEG_PHASE_MAIN | LEG_PHASE_KEEP_DONE);
             CK(cudaGetLastError());
-            CK(cudaEventRecord(ctx->pev[1][k], s));
-            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][k], 0));
-            auto [b, e] = alm_range(ctx, P, k);
-            if (e > b)
-                CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ctx->alm_buf.as<double2>() + b,
-                                   (e - b) * sizeof(double2), cudaMemcpyDeviceToHost, ctx->d2h));
+            CK(cudaEventRecord(ctx->tev[2][tc], s));
+            CK(cudaEventRecord(ctx->pev[1][tc], s));
+            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][tc], 0));
+            for (const auto& run : P.m2a_done[tc]) {
+                auto [b, e] = alm_span(ctx, run.first, run.second);
+                if (e > b)
+                    CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ab + b, (e - b) * sizeof(double2),
+                                       cudaMemcpyDeviceToHost, ctx->d2h));
+            }
         }
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
         if (t) {
-            fill_timing(t, elapsed(ctx->ev[1], ctx->ev[2]), elapsed(ctx->ev[0], ctx->ev[1]),
-                        elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
+            float fft, leg;
+            band_timing(ctx, fft, leg);
+            fill_timing(t, leg, fft, elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
                         elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
