@@ -138,12 +138,20 @@ struct RingStageArgs {
     double2* delta_out;       // analysis
     const double* map_in;     // analysis
     double* map_out;          // synthesis
+    int* counter;             // power-of-two engine: ring queue of this launch (zeroed)
+    const double2* p2_tw;     // power-of-two engine: e^{-2 pi i k/B}, k < B, of the class
 };
 
-// size classes: 0: B<=256 (64 thr), 1: B<=1024 (256), 2: B<=4096 (512), 3: B<=8192 (1024)
-constexpr int FFT_N_CLASSES = 4;
+// size classes.  Generic (any 7-smooth length, in-place mixed radix, odd-length rings):
+//   0: B<=256 (64 thr), 1: B<=1024 (256), 2: B<=4096 (512), 3: B<=8192 (1024).
+// Power-of-two engine (half-mode rings with a power-of-two buffer B = 256, 512, ..., 8192):
+//   4..9 direct FFTs of length B, 10..15 Bluestein convolutions of length B.
+constexpr int FFT_N_GENERIC = 4;
+constexpr int FFT_P2_MIN = 256, FFT_P2_MAX = 8192, FFT_N_P2 = 6;
+constexpr int FFT_N_CLASSES = FFT_N_GENERIC + 2 * FFT_N_P2;
 int fft_class_bmax(int c);
-int fft_class_for(int B);  // -1 if unsupported
+int fft_class_for(int B);     // generic class, -1 if unsupported
+int fft_p2_class_for(int B, bool bluestein);  // power-of-two engine class, -1: not one of its lengths
 
 void launch_ring_synthesis(int cls, const RingStageArgs& a, cudaStream_t s);
 void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s);

@@ -21,6 +21,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "fftcore.cuh"
 #include "kernels.h"
 
 namespace shtk {
@@ -281,12 +282,14 @@ __device__ __forceinline__ double2 delta_at(const RingStageArgs& a, int pos, int
 }
 
 // v_m = Delta_m e^{i m phi0} as in ring_synthesis_into (fourier.cpp:11-14); m==0 keeps Re only.
-__device__ __forceinline__ double2 folded_value(const RingStageArgs& a, int pos, int m,
-                                                bool rot, const PhaseTab& ph) {
-    double2 v = delta_at(a, pos, m);
+__device__ __forceinline__ double2 rot_value(double2 v, int m, bool rot, const PhaseTab& ph) {
     if (m == 0) return make_double2(v.x, 0.0);
     if (rot) v = cmul(v, ph.at(m));
     return v;
+}
+__device__ __forceinline__ double2 folded_value(const RingStageArgs& a, int pos, int m,
+                                                bool rot, const PhaseTab& ph) {
+    return rot_value(delta_at(a, pos, m), m, rot, ph);
 }
 
 // Fold sums of bin pair p over the wraps w = g, g+G, ... (ring_synthesis_into's bins,
@@ -343,7 +346,455 @@ __device__ __forceinline__ void store_z(double2* buf, const double2* __restrict_
     }
 }
 
+// ---------------------------------------------------------------------------------------
+// Power-of-two engine (half-mode rings whose buffer length M is a power of two: direct FFTs of
+// N = M, and Bluestein convolutions of length M).  T = M/E threads; thread t holds the elements
+// t + T j (j < E) in registers.  Every Stockham pass reads its butterfly inputs from the
+// thread's own registers; only the pass outputs go through shared memory (padded one slot per
+// 16 so the stride-R stores of the first pass are conflict-free), and the last pass leaves its
+// outputs in the same register layout.  So a Bluestein ring runs forward FFT -> x FFT(h) ->
+// inverse FFT with no shared-memory round trip between the two transforms, the prologue (fold
+// of Delta into the half spectrum) feeds the first pass from registers and the epilogue writes
+// the ring samples straight from registers.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ int p2pad(int i) { return i + (i >> 4); }
+
+// u[r] *= W_{NS R}^{r k} = W_M^{r e0}, e0 = k M / (NS R); table tw[j] = e^{-2 pi i j / M}
+template <int R, int S>
+__device__ __forceinline__ void p2_twiddle(double2 (&u)[R], int e0, const double2* __restrict__ tw) {
+    // a plain (coherent) load: ptxas may hoist read-only (.nc) loads of every later pass above
+    // the exchange barriers, which keeps all passes' twiddles live at once
+    auto ld = [&](int e) {
+        double2 w;
+        asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(tw + e));
+        if (S > 0) w.y = -w.y;
+        return w;
+    };
+    if constexpr (R == 2) {
+        u[1] = cmul(u[1], ld(e0));
+    } else if constexpr (R == 4) {
+        const double2 w1 = ld(e0), w2 = ld(2 * e0);
+        u[1] = cmul(u[1], w1);
+        u[2] = cmul(u[2], w2);
+        u[3] = cmul(u[3], cmul(w1, w2));
+    } else if constexpr (R == 8) {
+        const double2 w1 = ld(e0), w2 = ld(2 * e0), w4 = ld(4 * e0);
+        const double2 w3 = cmul(w1, w2);
+        u[1] = cmul(u[1], w1);
+        u[2] = cmul(u[2], w2);
+        u[3] = cmul(u[3], w3);
+        u[4] = cmul(u[4], w4);
+        u[5] = cmul(u[5], cmul(w1, w4));
+        u[6] = cmul(u[6], cmul(w2, w4));
+        u[7] = cmul(u[7], cmul(w3, w4));
+    } else {  // R == 16: powers from 4 table entries, product depth <= 3
+        const double2 w1 = ld(e0), w2 = ld(2 * e0), w4 = ld(4 * e0), w8 = ld(8 * e0);
+        const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
+        u[1] = cmul(u[1], w1);
+        u[2] = cmul(u[2], w2);
+        u[3] = cmul(u[3], w3);
+        u[4] = cmul(u[4], w4);
+        u[5] = cmul(u[5], w5);
+        u[6] = cmul(u[6], w6);
+        u[7] = cmul(u[7], w7);
+        u[8] = cmul(u[8], w8);
+        u[9] = cmul(u[9], cmul(w1, w8));
+        u[10] = cmul(u[10], cmul(w2, w8));
+        u[11] = cmul(u[11], cmul(w3, w8));
+        u[12] = cmul(u[12], cmul(w4, w8));
+        u[13] = cmul(u[13], cmul(w5, w8));
+        u[14] = cmul(u[14], cmul(w6, w8));
+        u[15] = cmul(u[15], cmul(w7, w8));
+    }
+}
+
+// Padded position of output r of a butterfly whose output 0 sits at `base`:
+// p2pad(base + r NS) = p2pad(base) + p2off<NS>(r) for every (E, NS) the engine uses (NS = 1 with
+// base a multiple of 8, NS = 8 with base % 16 < 8, NS a multiple of 16), so the compiler sees
+// immediate offsets instead of one live address per element.
+template <int NS>
+__device__ __forceinline__ constexpr int p2off(int r) {
+    return r * NS + (NS >= 16 ? r * (NS / 16) : (NS == 8 ? r / 2 : 0));
+}
+
+// One Stockham pass of radix R after NS points have been combined (butterfly b: inputs
+// b + r M/R, outputs (b/NS) NS R + b%NS + r NS).
+template <int M, int E, int R, int NS, bool LAST, int S>
+__device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw) {
+    constexpr int T = M / E;
+    constexpr int Q = E / R;
+    static_assert(T % 16 == 0, "padded exchange needs T % 16 == 0");
+    int t = threadIdx.x;
+    asm volatile("" : "+r"(t));  // per-pass address arithmetic: nothing hoisted across passes
+#pragma unroll
+    for (int q = 0; q < Q; ++q) {
+        double2 u[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
+        const int b = t + q * T;
+        if constexpr (NS > 1) p2_twiddle<R, S>(u, (b & (NS - 1)) * (M / (NS * R)), tw);
+        dft_pow2<R, S>(u);
+        if constexpr (LAST) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) v[q + r * Q] = u[r];
+        } else {
+            double2* const o = sm + p2pad((b / NS) * (NS * R) + (b & (NS - 1)));
+#pragma unroll
+            for (int r = 0; r < R; ++r) o[p2off<NS>(r)] = u[r];
+        }
+    }
+    if constexpr (!LAST) {
+        __syncthreads();
+        const double2* const in = sm + p2pad(t);
+#pragma unroll
+        for (int j = 0; j < E; ++j) v[j] = in[j * (T + T / 16)];
+        __syncthreads();
+    }
+}
+
+template <int M, int E, int S, int NS = 1>
+__device__ __forceinline__ void p2_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw) {
+    constexpr int REM = M / NS;
+    if constexpr (REM <= E) {
+        p2_pass<M, E, REM, NS, true, S>(v, sm, tw);
+    } else {
+        p2_pass<M, E, E, NS, false, S>(v, sm, tw);
+        p2_fft<M, E, S, NS * E>(v, sm, tw);
+    }
+}
+
 }  // namespace
+
+// L2 prefetch of [p, p + bytes) by the CTA (one prefetch per 128-byte line)
+template <int T>
+__device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
+    const char* c = reinterpret_cast<const char*>(p);
+    for (int64_t o = (int64_t)threadIdx.x * 128; o < bytes; o += (int64_t)T * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(c + o));
+}
+
+// Everything ring `ri` will read from HBM (its Delta row or ring samples and its tables), so
+// the next ring of this persistent CTA streams into L2 while the current one is transformed.
+template <int M, int T, bool SYN>
+__device__ __forceinline__ void p2_prefetch_ring(const RingStageArgs& a, int ri) {
+    if (ri >= a.n_rings) return;
+    const RingDesc d = a.rings[ri];
+    if (SYN) {
+        if (!a.m_base) l2_prefetch<T>(a.delta_in + (int64_t)d.ring_pos * a.ld, (int64_t)(a.mmax + 1) * 16);
+    } else {
+        l2_prefetch<T>(a.map_in + d.pix_off, (int64_t)d.n * 8);
+    }
+    l2_prefetch<T>(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);
+    if (d.flags & 2) {
+        l2_prefetch<T>(a.tabs + d.chirp_off, (int64_t)d.N * 16);
+        l2_prefetch<T>(a.tabs + d.h_off, (int64_t)M * 16);
+    }
+}
+
+// Descriptor fields are read through an index the compiler cannot track, so each read is a
+// fresh (L1-resident) load where it is used rather than a register held across the FFT passes
+// (the ring itself occupies 4E registers per thread).
+__device__ __forceinline__ const RingDesc& desc_at(const RingStageArgs& a, int ri) {
+    asm volatile("" : "+r"(ri));
+    return a.rings[ri];
+}
+
+// Persistent CTAs pull rings from a queue and transform one ring at a time (the ring in
+// registers + one padded shared-memory exchange buffer).
+template <int M, int E, int MINB, bool BLUE>
+__global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArgs a) {
+    constexpr int T = M / E;
+    constexpr int G = E < 8 ? E : 8;  // fold batch: elements whose loads are in flight together
+    extern __shared__ __align__(16) double2 smem[];
+    __shared__ int s_ri;
+    double2* buf = smem;                        // p2pad(M) + 1 (H_N of direct rings)
+    double2* phlo = smem + p2pad(M) + 16;       // 64 + (mmax >> 6) + 1 phase factors
+    const int t = threadIdx.x, mmax = a.mmax;
+    const PhaseTab ph{phlo, phlo + 64};
+    p2_prefetch_ring<M, T, true>(a, blockIdx.x);
+    if (t == 0) s_ri = atomicAdd(a.counter, 1);
+    __syncthreads();
+    for (;;) {
+        // dynamic ring queue: CTAs that become resident late (other classes' kernels run
+        // concurrently on other streams) just take fewer rings; the next index is fetched
+        // while this ring is transformed
+        const int ri = s_ri;
+        if (ri >= a.n_rings) break;
+        int nxt = 0;
+        if (t == 0) nxt = atomicAdd(a.counter, 1);
+        p2_prefetch_ring<M, T, true>(a, ri + gridDim.x);
+        double2 v[E];
+        {
+            const RingDesc& d = desc_at(a, ri);
+            const int n = d.n, N = d.N, pos = d.ring_pos;
+            const double phi0 = d.phi0;
+            const bool rot = phi0 != 0.0;
+            if (rot) {
+                build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                __syncthreads();
+            }
+            // fold (ring_synthesis_into's bins, fourier.cpp:17-25): H_k for 0 <= k <= N, terms
+            // in ascending m as the reference adds them.  k = N of a direct ring (N == M) is an
+            // extra slot of thread 0 in the last batch.
+            if (n > mmax) {
+                // no wraps: H_k = v_k [k <= mmax] + conj v_{n-k} [n-k <= mmax]; loads from
+                // clamped (always valid) positions and masked after, so the G elements' loads
+                // issue back to back
+#pragma unroll
+                for (int j0 = 0; j0 < E; j0 += G) {
+                    constexpr int GX = G + 1;
+                    double2 x1[GX], x2[GX];
+#pragma unroll
+                    for (int u = 0; u < GX; ++u) {
+                        const int k = (u < G) ? t + T * (j0 + u) : N;
+                        const int m1 = k, m2 = (k == 0) ? n : n - k;  // k > N (Bluestein pad): unused
+                        x1[u] = a.delta_in[delta_index(a, pos, (k <= N && m1 <= mmax) ? m1 : 0)];
+                        x2[u] = a.delta_in[delta_index(a, pos, (k <= N && m2 <= mmax) ? m2 : 0)];
+                    }
+#pragma unroll
+                    for (int u = 0; u < GX; ++u) {
+                        const int k = (u < G) ? t + T * (j0 + u) : N;
+                        const bool mine = (u < G) ? (k <= N) : (j0 + G == E && t == 0 && N == M);
+                        const int m1 = k, m2 = (k == 0) ? n : n - k;
+                        if (mine) {
+                            double2 h = make_double2(0.0, 0.0);
+                            if (m1 <= mmax) h = rot_value(x1[u], m1, rot, ph);
+                            if (m2 <= mmax) h = cadd(h, cconj(rot_value(x2[u], m2, rot, ph)));
+                            buf[p2pad(k)] = h;
+                        }
+                    }
+                }
+            } else {
+                // aliasing rings: wraps outer (two per iteration), G elements' loads together
+#pragma unroll
+                for (int j0 = 0; j0 < E; j0 += G) {
+                    constexpr int GX = G + 1;
+                    double2 h[GX];
+                    int kk[GX];
+#pragma unroll
+                    for (int u = 0; u < GX; ++u) {
+                        h[u] = make_double2(0.0, 0.0);
+                        kk[u] = (u < G) ? t + T * (j0 + u) : ((j0 + G == E && t == 0 && N == M) ? N : INT_MAX);
+                    }
+                    for (int base = 0; base <= mmax; base += 2 * n) {
+#pragma unroll
+                        for (int u = 0; u < GX; ++u) {
+                            const int k = kk[u];
+                            if (k <= N) {
+                                const int m1 = base + k, m2 = base + (k == 0 ? n : n - k);
+                                double2 x1 = make_double2(0.0, 0.0), x2 = x1, x3 = x1, x4 = x1;
+                                if (m1 <= mmax) x1 = folded_value(a, pos, m1, rot, ph);
+                                if (m2 <= mmax) x2 = folded_value(a, pos, m2, rot, ph);
+                                if (m1 + n <= mmax) x3 = folded_value(a, pos, m1 + n, rot, ph);
+                                if (m2 + n <= mmax) x4 = folded_value(a, pos, m2 + n, rot, ph);
+                                if (m1 <= mmax) h[u] = cadd(h[u], x1);
+                                if (m2 <= mmax) h[u] = cadd(h[u], cconj(x2));
+                                if (m1 + n <= mmax) h[u] = cadd(h[u], x3);
+                                if (m2 + n <= mmax) h[u] = cadd(h[u], cconj(x4));
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < GX; ++u)
+                        if (kk[u] <= N) buf[p2pad(kk[u])] = h[u];
+                }
+            }
+            __syncthreads();
+            // Z_k = (H_k + conj H_{N-k}) + i (H_k - conj H_{N-k}) e^{+2 pi i k/n}: the C2R of
+            // length n as a complex inverse FFT of length N (chirped for Bluestein)
+            const double2* __restrict__ hw = a.tabs + d.hw_off;
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                const int kc = k < N ? k : 0;  // table loads from valid positions, result masked
+                const double2 w = __ldg(&hw[kc]);
+                double2 c = make_double2(1.0, 0.0);
+                if constexpr (BLUE) c = __ldg(&chirp[kc]);
+                const double2 Hp = buf[p2pad(kc)], Hq = buf[p2pad(N - kc)];
+                const double2 e = cadd(Hp, cconj(Hq));
+                const double2 o = cmul(csub(Hp, cconj(Hq)), cconj(w));
+                double2 z = cadd(e, cmul_si(o, +1));
+                if constexpr (BLUE) z = cmul(z, cconj(c));
+                v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+            }
+        }
+        __syncthreads();  // H is read before the first pass overwrites buf
+        if constexpr (!BLUE) {
+            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+        } else {
+            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+            // fences keep ptxas from hoisting the table loads into the FFT passes
+            __threadfence_block();
+            {
+                const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[j] = cmul(v[j], cconj(__ldg(&H[t + T * j])));
+            }
+            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+            __threadfence_block();
+            const RingDesc& d = desc_at(a, ri);
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            const int N = d.N;
+            const double inv = 1.0 / (double)M;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                const double2 c = __ldg(&chirp[k < N ? k : 0]);
+                v[j] = cscale(cmul(v[j], cconj(c)), inv);  // k >= N: not stored
+            }
+        }
+        {
+            const RingDesc& d = desc_at(a, ri);
+            const int N = d.N;
+            const int64_t po = d.pix_off;
+            double* __restrict__ out = a.map_out + po;
+            if ((po & 1) == 0) {
+                double2* __restrict__ o2 = reinterpret_cast<double2*>(out);
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) o2[k] = v[j];
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) {
+                        out[2 * k] = v[j].x;
+                        out[2 * k + 1] = v[j].y;
+                    }
+                }
+            }
+        }
+        if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
+        __syncthreads();  // buf / phase table / s_ri reuse by the next ring
+    }
+}
+
+template <int M, int E, int MINB, bool BLUE>
+__global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs a) {
+    constexpr int T = M / E;
+    constexpr int U = 8;  // unfold batch
+    extern __shared__ __align__(16) double2 smem[];
+    __shared__ int s_ri;
+    double2* buf = smem;
+    double2* phlo = smem + p2pad(M) + 16;
+    const int t = threadIdx.x, mmax = a.mmax;
+    const PhaseTab ph{phlo, phlo + 64};
+    p2_prefetch_ring<M, T, false>(a, blockIdx.x);
+    if (t == 0) s_ri = atomicAdd(a.counter, 1);
+    __syncthreads();
+    for (;;) {
+        const int ri = s_ri;
+        if (ri >= a.n_rings) break;
+        int nxt = 0;
+        if (t == 0) nxt = atomicAdd(a.counter, 1);
+        p2_prefetch_ring<M, T, false>(a, ri + gridDim.x);
+        double2 v[E];
+        {
+            const RingDesc& d = desc_at(a, ri);
+            const int N = d.N;
+            const double phi0 = d.phi0;
+            if (phi0 != 0.0) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);  // published by later barriers
+            const int64_t po = d.pix_off;
+            const double* __restrict__ in = a.map_in + po;
+            if ((po & 1) == 0) {
+                const double2* __restrict__ i2 = reinterpret_cast<const double2*>(in);
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    const double2 x = i2[k < N ? k : 0];
+                    v[j] = (k < N) ? x : make_double2(0.0, 0.0);
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    v[j] = (k < N) ? make_double2(in[2 * k], in[2 * k + 1]) : make_double2(0.0, 0.0);
+                }
+            }
+            if constexpr (BLUE) {
+                const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    v[j] = cmul(v[j], __ldg(&chirp[k < N ? k : 0]));  // v = 0 beyond N
+                }
+            }
+        }
+        if constexpr (!BLUE) {
+            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+        } else {
+            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+            __threadfence_block();
+            {
+                const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[j] = cmul(v[j], __ldg(&H[t + T * j]));
+            }
+            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+            __threadfence_block();
+            const RingDesc& d = desc_at(a, ri);
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            const int N = d.N;
+            const double inv = 1.0 / (double)M;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                const double2 c = __ldg(&chirp[k < N ? k : 0]);
+                v[j] = cscale(cmul(v[j], c), inv);  // k >= N: not stored
+            }
+        }
+        const RingDesc& d = desc_at(a, ri);
+        const int n = d.n, N = d.N, pos = d.ring_pos;
+        // Z_k (k < N) -> shared memory; the last FFT pass ended after a barrier that followed
+        // every read of buf, so the stores cannot race with it
+#pragma unroll
+        for (int j = 0; j < E; ++j) {
+            const int k = t + T * j;
+            if (k < N) buf[p2pad(k)] = v[j];
+        }
+        __syncthreads();
+        // R2C split B_b = E_b + e^{-2 pi i b/n} O_b and the unfold Delta^S_m = w bins[m mod n]
+        // e^{-i m phi0} (fourier.cpp:42-47); bins above n/2 are conj B_{n-b}.  U orders per
+        // thread per batch so their table loads are in flight together.
+        const double wgt = d.weight;
+        const bool rot = d.phi0 != 0.0;
+        const double2* __restrict__ hw = a.tabs + d.hw_off;
+        const int Tn = T % n;
+        for (int m0 = t; m0 <= mmax; m0 += U * T) {
+            // branch-free batch: indices clamped, table loads issued together, stores masked
+            int bb[U];
+            bool cj[U];
+            double2 w[U];
+            int b = m0 % n;
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                cj[u] = b > N;
+                bb[u] = cj[u] ? n - b : b;
+                w[u] = __ldg(&hw[bb[u]]);
+                b += Tn;
+                if (b >= n) b -= n;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int m = m0 + u * T;
+                const double2 Zp = buf[p2pad(bb[u] == N ? 0 : bb[u])];
+                const double2 Zq = buf[p2pad(bb[u] == 0 ? 0 : N - bb[u])];
+                const double2 e = cscale(cadd(Zp, cconj(Zq)), 0.5);
+                const double2 o = cmul_si(cscale(csub(Zp, cconj(Zq)), 0.5), -1);
+                double2 B = cadd(e, cmul(w[u], o));
+                if (cj[u]) B = cconj(B);
+                double2 val = cscale(B, wgt);
+                if (rot && m > 0) val = cmul(val, cconj(ph.at(m <= mmax ? m : 0)));
+                if (m <= mmax) a.delta_out[delta_index(a, pos, m)] = val;
+            }
+        }
+        if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
+        __syncthreads();  // buf / phase table / s_ri reuse by the next ring
+    }
+}
 
 // ---------------------------------------------------------------------------------------
 // synthesis: Delta rows -> ring samples
@@ -538,8 +989,8 @@ __global__ void __launch_bounds__(T, 1) bluestein_h_kernel(const RingDesc* __res
 // launchers
 // ---------------------------------------------------------------------------------------
 namespace {
-constexpr int kBmax[FFT_N_CLASSES] = {256, 1024, 4096, 8192};
-constexpr int kThr[FFT_N_CLASSES] = {64, 256, 512, 1024};
+constexpr int kBmax[FFT_N_GENERIC] = {256, 1024, 4096, 8192};
+constexpr int kThr[FFT_N_GENERIC] = {64, 256, 512, 1024};
 
 // buffer + fold partials + phase table (orders up to kMaxPhaseM)
 constexpr int kMaxPhaseM = 65535;
@@ -587,13 +1038,115 @@ void blue_c(const RingDesc* descs, int n, double2* tabs, cudaStream_t s) {
         bluestein_h_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(0), s>>>(descs + r0, tabs);
     }
 }
+// power-of-two engine: elements per thread (E, T = M/E threads) and resident CTAs per SM the
+// kernel is compiled for, per buffer length, for direct FFTs (P2D_*) and Bluestein (P2B_*,
+// two FFTs with the table loads between them: more register pressure)
+#ifndef P2D_E_8192
+#define P2D_E_8192 16
+#endif
+#ifndef P2D_MB_8192
+#define P2D_MB_8192 1
+#endif
+#ifndef P2D_E_4096
+#define P2D_E_4096 16
+#endif
+#ifndef P2D_MB_4096
+#define P2D_MB_4096 2
+#endif
+#ifndef P2B_E_8192
+#define P2B_E_8192 16
+#endif
+#ifndef P2B_MB_8192
+#define P2B_MB_8192 1
+#endif
+#ifndef P2B_E_4096
+#define P2B_E_4096 16
+#endif
+#ifndef P2B_MB_4096
+#define P2B_MB_4096 2
+#endif
+#ifndef P2B_E_2048
+#define P2B_E_2048 16
+#endif
+#ifndef P2B_MB_2048
+#define P2B_MB_2048 4
+#endif
+template <int M>
+size_t p2_smem(int mmax) {
+    return (size_t)(M + (M >> 4) + 16) * sizeof(double2) + (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
+}
+// persistent grid: every resident CTA slot of the device (at most one per ring)
+template <class K>
+int p2_grid(K kernel, int threads, size_t smem, int n_rings) {
+    int dev = 0, sms = 148, per = 1;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, smem);
+    const int g = sms * (per > 0 ? per : 1);
+    return n_rings < g ? n_rings : g;
+}
+template <int M, int E, int MINB, bool BLUE>
+void p2_synth(const RingStageArgs& a, cudaStream_t s) {
+    static bool once = (cudaFuncSetAttribute(ring_p2_synth_kernel<M, E, MINB, BLUE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p2_smem<M>(kMaxPhaseM)),
+                        true);
+    (void)once;
+    auto k = ring_p2_synth_kernel<M, E, MINB, BLUE>;
+    const size_t sm = p2_smem<M>(a.mmax);
+    k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
+}
+template <int M, int E, int MINB, bool BLUE>
+void p2_anal(const RingStageArgs& a, cudaStream_t s) {
+    static bool once = (cudaFuncSetAttribute(ring_p2_anal_kernel<M, E, MINB, BLUE>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p2_smem<M>(kMaxPhaseM)),
+                        true);
+    (void)once;
+    auto k = ring_p2_anal_kernel<M, E, MINB, BLUE>;
+    const size_t sm = p2_smem<M>(a.mmax);
+    k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
+}
+// class -> (M, E, resident CTAs per SM, Bluestein)
+template <bool SYN, int M, int E, int MINB, bool BLUE>
+void p2_run(const RingStageArgs& a, cudaStream_t s) {
+    if (SYN) p2_synth<M, E, MINB, BLUE>(a, s);
+    else p2_anal<M, E, MINB, BLUE>(a, s);
+}
+template <bool SYN>
+void p2_dispatch(int cls, const RingStageArgs& a, cudaStream_t s) {
+    const bool blue = cls >= FFT_N_GENERIC + FFT_N_P2;
+    const int c = (cls - FFT_N_GENERIC) % FFT_N_P2;
+#define P2_CASE(C, M, ED, MBD, EB, MBB)                                   \
+    case C:                                                               \
+        if (blue) p2_run<SYN, M, EB, MBB, true>(a, s);                    \
+        else p2_run<SYN, M, ED, MBD, false>(a, s);                        \
+        break;
+    switch (c) {
+        P2_CASE(0, 256, 4, 8, 4, 8)
+        P2_CASE(1, 512, 4, 6, 4, 6)
+        P2_CASE(2, 1024, 4, 3, 4, 3)
+        P2_CASE(3, 2048, 16, 4, P2B_E_2048, P2B_MB_2048)
+        P2_CASE(4, 4096, P2D_E_4096, P2D_MB_4096, P2B_E_4096, P2B_MB_4096)
+        P2_CASE(5, 8192, P2D_E_8192, P2D_MB_8192, P2B_E_8192, P2B_MB_8192)
+    }
+#undef P2_CASE
+}
 }  // namespace
 
-int fft_class_bmax(int c) { return kBmax[c]; }
+int fft_class_bmax(int c) {
+    return c < FFT_N_GENERIC ? kBmax[c] : FFT_P2_MIN << ((c - FFT_N_GENERIC) % FFT_N_P2);
+}
 int fft_class_for(int B) {
-    for (int c = 0; c < FFT_N_CLASSES; ++c)
+    for (int c = 0; c < FFT_N_GENERIC; ++c)
         if (B <= kBmax[c]) return c;
     return -1;
+}
+int fft_p2_class_for(int B, bool bluestein) {
+    if (B < FFT_P2_MIN || B > FFT_P2_MAX || (B & (B - 1))) return -1;
+    int c = FFT_N_GENERIC + (bluestein ? FFT_N_P2 : 0);
+    for (int m = FFT_P2_MIN; m < B; m <<= 1) ++c;
+    return c;
 }
 
 void launch_ring_synthesis(int cls, const RingStageArgs& a, cudaStream_t s) {
@@ -603,6 +1156,7 @@ void launch_ring_synthesis(int cls, const RingStageArgs& a, cudaStream_t s) {
         case 1: synth_c<1>(a, s); break;
         case 2: synth_c<2>(a, s); break;
         case 3: synth_c<3>(a, s); break;
+        default: p2_dispatch<true>(cls, a, s); break;
     }
 }
 void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s) {
@@ -612,6 +1166,7 @@ void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s) {
         case 1: anal_c<1>(a, s); break;
         case 2: anal_c<2>(a, s); break;
         case 3: anal_c<3>(a, s); break;
+        default: p2_dispatch<false>(cls, a, s); break;
     }
 }
 void launch_bluestein_h(int cls, const RingDesc* descs_dev, int n, double2* tabs,

@@ -128,12 +128,14 @@ constexpr int kPipeChunks = 4;  // chunks of the pipelined host-buffer entry poi
 struct FftPlan {
     bool built = false;
     DevBuf descs[FFT_N_CLASSES];
-    int count[FFT_N_CLASSES] = {0, 0, 0, 0};
+    int count[FFT_N_CLASSES] = {};
     // latitude bands of the pipelined paths: class c's descriptors of band k are
     // [range_start[c][k], range_start[c][k+1]); band k covers the pixel intervals band_pix[k]
     std::vector<int> range_start[FFT_N_CLASSES];
     std::vector<std::vector<std::pair<int64_t, int64_t>>> band_pix;
     DevBuf tabs;
+    DevBuf counters;  // ring queues of the power-of-two engine's launches (one per class)
+    int64_t tw_off[FFT_N_CLASSES] = {};  // twiddle table of each power-of-two class
     double build_ms = 0.0;
 };
 
@@ -177,6 +179,9 @@ struct shtc_ctx {
     // pipelined host-buffer paths
     cudaStream_t h2d = nullptr, d2h = nullptr;
     cudaEvent_t pev[3][kPipeChunks] = {};  // ordering events of the copy streams
+    // ring stage: the small-ring classes run on side streams beside the large ones
+    cudaStream_t fft_aux[2] = {};
+    cudaEvent_t fft_fork = nullptr, fft_join[2] = {};
     cudaEvent_t tev[3][kPipeChunks] = {};  // timing events of the pipelined segments
 };
 
@@ -577,8 +582,14 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         d.phi0 = c->phi0[r];
         d.weight = c->weight[r];
         d.ring_pos = (int)pos;
-        const int cls = fft_class_for(d.B);
-        if (cls < 0)
+        // half-mode rings with a power-of-two buffer (direct or Bluestein) run the register
+        // resident power-of-two engine; the rest (odd rings, other 7-smooth lengths, tiny
+        // buffers) the generic in-place mixed-radix kernels.  Bluestein's FFT(conj chirp) is
+        // built by the generic class of the same length at plan time.
+        const int gcls = fft_class_for(d.B);
+        int cls = half ? fft_p2_class_for(d.B, !smooth) : -1;
+        if (cls < 0) cls = gcls;
+        if (gcls < 0)
             fail(SHTC_EUNSUPPORTED, "ring length " + std::to_string(d.n) +
                                         " needs an FFT buffer beyond the shared-memory classes");
         auto rp = radix_plan(d.B);
@@ -595,12 +606,13 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
                 d.h_off = tot;
                 tot += d.B;
                 h_at[d.N] = d.h_off;
-                blue_class[cls].push_back(d);
+                blue_class[gcls].push_back(d);
             } else {
                 d.h_off = it->second;
             }
         }
         per_class[cls].push_back(d);
+        F.tw_off[cls] = d.tw_off;
     }
     F.tabs.ensure((size_t)std::max<int64_t>(tot, 1) * sizeof(double2));
     DevBuf jobs_d;
@@ -684,44 +696,73 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
-void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
-                    const int64_t* mb, const int64_t* mst, int range = -1) {
+// Ring stage launches of one plan (or of one pipeline band of it).  The large power-of-two
+// classes (buffers >= 2048, the belt and the big polar-cap rings) go on the caller's stream;
+// the small-ring classes (latency bound: few CTAs, aliasing folds over many wraps) run on two
+// side streams at the same time, joined back before the stage ends.
+template <class Launch>
+void ring_stage(shtc_ctx* c, FftPlan& F, int range, Launch launch) {
+    if (!c->fft_fork) {
+        for (auto& st : c->fft_aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&c->fft_fork, cudaEventDisableTiming));
+        for (auto& e : c->fft_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    }
+    if (!F.counters.p) F.counters.ensure(FFT_N_CLASSES * sizeof(int));
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(F.counters.p, 0, FFT_N_CLASSES * sizeof(int), s));
+    CK(cudaEventRecord(c->fft_fork, s));
+    bool used[2] = {false, false};
+    int side = 0;
     for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
-        RingStageArgs a{};
         const int b = range < 0 ? 0 : F.range_start[k][range];
         const int e = range < 0 ? F.count[k] : F.range_start[k][range + 1];
+        if (e <= b) continue;
+        const bool big = k >= FFT_N_GENERIC && fft_class_bmax(k) >= 2048;
+        cudaStream_t st = s;
+        if (!big) {
+            const int i = side++ & 1;
+            if (!used[i]) CK(cudaStreamWaitEvent(c->fft_aux[i], c->fft_fork, 0));
+            used[i] = true;
+            st = c->fft_aux[i];
+        }
+        RingStageArgs a{};
         a.rings = F.descs[k].as<RingDesc>() + b;
         a.n_rings = e - b;
         a.tabs = F.tabs.as<double2>();
         a.mmax = c->mmax;
-        a.m_base = mb;
-        a.m_stride = mst;
         a.ld = c->mmax + 1;
-        a.delta_in = delta;
-        a.map_out = map;
-        launch_ring_synthesis(k, a, c->stream);
+        a.counter = F.counters.as<int>() + k;
+        a.p2_tw = a.tabs + F.tw_off[k];
+        launch(k, a, st);
         CK(cudaGetLastError());
     }
+    for (int i = 0; i < 2; ++i)
+        if (used[i]) {
+            CK(cudaEventRecord(c->fft_join[i], c->fft_aux[i]));
+            CK(cudaStreamWaitEvent(s, c->fft_join[i], 0));
+        }
+}
+
+void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
+                    const int64_t* mb, const int64_t* mst, int range = -1) {
+    ring_stage(c, F, range, [&](int k, RingStageArgs& a, cudaStream_t st) {
+        a.m_base = mb;
+        a.m_stride = mst;
+        a.delta_in = delta;
+        a.map_out = map;
+        launch_ring_synthesis(k, a, st);
+    });
 }
 
 void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
                    const int64_t* mst, int range = -1) {
-    for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
-        RingStageArgs a{};
-        const int b = range < 0 ? 0 : F.range_start[k][range];
-        const int e = range < 0 ? F.count[k] : F.range_start[k][range + 1];
-        a.rings = F.descs[k].as<RingDesc>() + b;
-        a.n_rings = e - b;
-        a.tabs = F.tabs.as<double2>();
-        a.mmax = c->mmax;
+    ring_stage(c, F, range, [&](int k, RingStageArgs& a, cudaStream_t st) {
         a.m_base = mb;
         a.m_stride = mst;
-        a.ld = c->mmax + 1;
         a.map_in = map;
         a.delta_out = delta;
-        launch_ring_analysis(k, a, c->stream);
-        CK(cudaGetLastError());
-    }
+        launch_ring_analysis(k, a, st);
+    });
 }
 
 void fill_timing(shtc_timing* t, double leg, double fft, double h2d, double d2h, double total,
@@ -835,6 +876,11 @@ void shtc_destroy(shtc_ctx* ctx) {
     for (auto& row : ctx->tev)
         for (auto& e : row)
             if (e) cudaEventDestroy(e);
+    for (auto& st : ctx->fft_aux)
+        if (st) cudaStreamDestroy(st);
+    if (ctx->fft_fork) cudaEventDestroy(ctx->fft_fork);
+    for (auto& e : ctx->fft_join)
+        if (e) cudaEventDestroy(e);
     if (ctx->h2d) cudaStreamDestroy(ctx->h2d);
     if (ctx->d2h) cudaStreamDestroy(ctx->d2h);
     if (ctx->own_stream) cudaStreamDestroy(ctx->own_stream);
