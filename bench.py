@@ -167,6 +167,8 @@ def run_ours(args):
     from paper_1106_0159_b200 import sht
 
     ws, rank, local = dist_env()
+    if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
+        os.environ["NCCL_DEBUG"] = "WARN"  # rank 0 prints exactly one JSON line on stdout
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
@@ -187,12 +189,21 @@ def run_ours(args):
     n_alm = alm_h.size
     layout = sht.WorkerLayout.create(grid, mmax, ws)
     Mi = layout.m_sets[rank]
-    if ws == 1 and not args.exchange:
+    if args.exchange == "auto":
+        args.exchange = "peer" if ws > 1 else "none"
+    if ws == 1 and args.exchange == "none":
         ctx.set_band(lmax, mmax)
     else:
         ctx.set_band(lmax, mmax, Mi)
         if not dist_ready():
             import torch.distributed as dist
+            if "RANK" not in os.environ:  # N=1 exchange path outside torchrun
+                import socket
+                so = socket.socket()
+                so.bind(("127.0.0.1", 0))
+                os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
+                                  MASTER_PORT=str(so.getsockname()[1]))
+                so.close()
             dist.init_process_group("nccl", device_id=dev)
     t0 = time.perf_counter()
     ctx.plan()
@@ -204,7 +215,7 @@ def run_ours(args):
     launches_per_step = None
     exch_ms, exch_bytes = [], 0
 
-    use_exchange = ws > 1 or args.exchange
+    use_exchange = args.exchange != "none"
     if not use_exchange:
         mp = torch.empty(grid.n_pix, dtype=torch.float64, device=dev)
 
@@ -213,6 +224,39 @@ def run_ours(args):
             t2 = ctx.map2alm_dev(mp.data_ptr(), alm_out.data_ptr(), timing=True)
             return t1, t2
         ring_classes = None
+    elif args.exchange == "peer":
+        # fused exchange: the Legendre (alm2map) and ring-analysis (map2alm) kernels store
+        # Delta straight into the consumers' buffers over NVLink (CUDA IPC peer mappings),
+        # then one device-side barrier; no collective on the data path
+        import torch.distributed as dist
+
+        def all_gather(obj):
+            out = [None] * ws
+            dist.all_gather_object(out, obj)
+            return out
+        px = sht.PeerExchange(ctx, layout, rank, all_gather=all_gather)
+        send_c, recv_c = sht.exchange_sizes(layout, rank)
+        mp = torch.zeros(grid.n_pix, dtype=torch.float64, device=dev)
+        xev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        exch_ms = []
+        _, sc, _, _, _, _ = sht.exchange_layout(layout, rank)
+        exch_bytes = 16 * sum(c for j, c in enumerate(sc) if j != rank)
+
+        def step():
+            t1 = ctx.legendre_alm2map_peer(alm.data_ptr(), timing=True)
+            xev[0].record(stream)
+            px.barrier()
+            xev[1].record(stream)
+            t3 = ctx.ring_synthesis_dev(px.recv, mp.data_ptr(), timing=True)
+            t4 = ctx.ring_analysis_peer(mp.data_ptr(), timing=True)
+            xev[2].record(stream)
+            px.barrier()
+            xev[3].record(stream)
+            t2 = ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr(), timing=True)
+            t1["fft_ms"] = t3["fft_ms"]
+            t2["fft_ms"] = t4["fft_ms"]
+            exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
+            return t1, t2
     else:
         import torch.distributed as dist
         row_off, send_c, recv_c, ring_list, m_base, m_stride = sht.exchange_layout(layout, rank)
@@ -351,13 +395,17 @@ def run_ours(args):
                 "map2alm input = the step's alm2map output",
         "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={lmax} (C4)",
                    "grid": "healpix-ring", "nside": args.nside, "lmax": lmax, "mmax": mmax,
-                   "parallelism": f"m-distributed x{ws}" + (" + NCCL all-to-all" if use_exchange else ""),
+                   "parallelism": f"m-distributed x{ws}" + {"none": "", "peer": " + fused peer-memory exchange",
+                                                            "nccl": " + NCCL all-to-all"}[args.exchange],
                    "l2": "inputs larger than L2 (a_lm 134 MB, map 403 MB, Delta 537 MB)"},
         "ms_alm2map": ms_a2m, "ms_map2alm": ms_m2a,
         "stages_ms": {"alm2map": {"legendre": leg_s_ms, "fft": float(np.mean(fft_s))},
                       "map2alm": {"legendre": leg_a_ms, "fft": float(np.mean(fft_a))}},
         "plan_s": plan_s, "steps_accounting": stats,
-        "exchange": ({"impl": "NCCL all_to_all_single on packed Delta (no pack/unpack kernels)",
+        "exchange": ({"impl": ("Delta stored straight into the owners' buffers by the Legendre / ring-analysis "
+                              "kernels (CUDA IPC peer memory over NVLink) + device-side barrier; "
+                              "ms_per_step = the two barrier waits" if args.exchange == "peer" else
+                              "NCCL all_to_all_single on packed Delta (no pack/unpack kernels)"),
                       "bytes_sent_per_rank_per_transform": exch_bytes,
                       "ms_per_step": float(np.mean(exch_ms[-args.steps:])),
                       "GBps_per_rank": 2 * exch_bytes / (float(np.mean(exch_ms[-args.steps:])) * 1e-3) / 1e9
@@ -416,8 +464,10 @@ def main():
     p.add_argument("--lmax", type=int, default=LMAX)
     p.add_argument("--cpu-seconds", type=float, default=30.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
-    p.add_argument("--exchange", action="store_true",
-                   help="run the multi-GPU stage path (packed NCCL all-to-all) even at N=1")
+    p.add_argument("--exchange", choices=["auto", "none", "peer", "nccl"], default="auto",
+                   help="Delta exchange of the m-distributed path: peer (fused stores over peer "
+                        "memory, the default for N>1), nccl (packed all_to_all_single), none (N=1 "
+                        "whole transforms, the default for N=1); peer/nccl also run at N=1")
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3

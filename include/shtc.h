@@ -22,8 +22,9 @@
  *                                     distributed_synthesis / distributed_analysis stages
  *                                     (distribution.cpp:300-490); the panel transpose
  *                                     exchange_m_to_rings/rings_to_m (distribution.hpp:52-57)
- *                                     becomes the caller's NCCL all-to-all on the packed
- *                                     buffers these calls read and write.
+ *                                     becomes either the caller's NCCL all-to-all on the
+ *                                     packed buffers these calls read and write, or the
+ *                                     fused peer-memory path (shtc_*_peer + shtc_peer_barrier).
  *
  * Error behaviour mirrors the reference: argument/layout violations -> SHTC_EINVAL
  * (std::invalid_argument), beta_lm(l==m) style domain errors -> SHTC_EDOMAIN
@@ -123,6 +124,32 @@ shtc_status shtc_ring_synthesis_dev(shtc_ctx* ctx, const double* delta_dev, doub
                                     shtc_timing* t);
 shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double* delta_dev,
                                    shtc_timing* t);
+
+/* ---- fused exchange over peer memory (multi-GPU, one process per GPU) ----------------- */
+/* exchange_m_to_rings / exchange_rings_to_m (distribution.cpp:233-298) without a collective:
+ * the producing stage kernel stores each Delta entry straight into the consumer's buffer
+ * (NVLink peer memory, mapped through CUDA IPC), then every worker passes one device-side
+ * barrier.  Buffers that other processes map must be allocated with shtc_dev_alloc (an IPC
+ * handle covers an allocation from its base).  Zero-filled. */
+shtc_status shtc_dev_alloc(int device, uint64_t bytes, void** ptr);
+shtc_status shtc_dev_free(void* ptr);
+shtc_status shtc_ipc_handle(const void* ptr, unsigned char* handle64);      /* 64 bytes */
+shtc_status shtc_ipc_open(int device, const unsigned char* handle64, void** ptr);
+shtc_status shtc_ipc_close(void* ptr);
+/* Targets of this worker's stores (device addresses valid on this context's device), on top
+ * of shtc_set_exchange_layout:
+ *   row_ptr[r] (n_rings): ring r's row of this worker's orders in the ring owner's receive
+ *     buffer (alm2map); col_ptr[m] (mmax+1): order m's column for this worker's first ring in
+ *     the order owner's send buffer, rows m_stride[m] apart (map2alm).
+ * NULL clears them. */
+shtc_status shtc_set_exchange_peers(shtc_ctx* ctx, const uint64_t* row_ptr, const uint64_t* col_ptr);
+/* Legendre stage writing Delta through row_ptr; ring analysis writing Delta^S through col_ptr. */
+shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, shtc_timing* t);
+shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_timing* t);
+/* Device-side barrier on the context stream: flags[w] = address of worker w's n_workers-word
+ * uint32 flag array (zeroed at allocation); epoch must increase by one per barrier. */
+shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint64_t* flags,
+                              uint32_t epoch);
 
 /* ---- Legendre-stage operators (transforms.cpp:269-365), host buffers ------------------ */
 /* Delta^A_m(r) for the given latitudes and orders; delta: n_lat x n_m complex, ring-major.

@@ -21,7 +21,9 @@ EXPORTED = [
     "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev", "shtc_set_exchange_layout",
     "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev", "shtc_ring_synthesis_dev",
     "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
-    "shtc_measure_fp64_peak",
+    "shtc_measure_fp64_peak", "shtc_dev_alloc", "shtc_dev_free", "shtc_ipc_handle", "shtc_ipc_open",
+    "shtc_ipc_close", "shtc_set_exchange_peers", "shtc_legendre_alm2map_peer", "shtc_ring_analysis_peer",
+    "shtc_peer_barrier",
 ]
 
 
@@ -70,6 +72,15 @@ def lib():
         L.shtc_accumulate_alm.argtypes = [vp, vp, i32, vp, i32, vp, i32, i32, vp, u64p]
         L.shtc_device_info.argtypes = [i32, C.c_char_p, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]
         L.shtc_measure_fp64_peak.argtypes = [i32, C.POINTER(dbl), C.POINTER(dbl)]
+        L.shtc_dev_alloc.argtypes = [i32, C.c_uint64, C.POINTER(vp)]
+        L.shtc_dev_free.argtypes = [vp]
+        L.shtc_ipc_handle.argtypes = [vp, C.c_char_p]
+        L.shtc_ipc_open.argtypes = [i32, C.c_char_p, C.POINTER(vp)]
+        L.shtc_ipc_close.argtypes = [vp]
+        L.shtc_set_exchange_peers.argtypes = [vp, vp, vp]
+        L.shtc_legendre_alm2map_peer.argtypes = [vp, vp, C.POINTER(Timing)]
+        L.shtc_ring_analysis_peer.argtypes = [vp, vp, C.POINTER(Timing)]
+        L.shtc_peer_barrier.argtypes = [vp, i32, i32, vp, C.c_uint32]
         _LIB = L
     return _LIB
 

@@ -75,6 +75,9 @@ struct LegPlanView {
     const int* m2a_items_per_m;     // [n_m]
     const int64_t* m2a_slot_base;   // [n_m] double2 offset of the order's first partial slot
     int64_t m2a_scratch_elems;
+    // fused exchange (alm2map): ring r's output row is row_ptr[r] (an address in the ring
+    // owner's receive buffer, peer memory) instead of delta + row_off[r]; nullptr: local
+    double2* const* row_ptr;
 };
 
 void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s);
@@ -140,6 +143,9 @@ struct RingStageArgs {
     double* map_out;          // synthesis
     int* counter;             // power-of-two engine: ring queue of this launch (zeroed)
     const double2* p2_tw;     // power-of-two engine: e^{-2 pi i k/B}, k < B, of the class
+    // fused exchange (analysis): Delta^S(ring_pos, m) goes to col_ptr[m] + ring_pos *
+    // m_stride[m] (an address in the order owner's send buffer, peer memory); nullptr: local
+    double2* const* col_ptr;
 };
 
 // size classes.  Generic (any 7-smooth length, in-place mixed radix, odd-length rings):
@@ -166,6 +172,15 @@ void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cud
 // For each Bluestein ring descriptor (deduplicated by N): tabs[h_off..] = FFT_B(h).
 void launch_bluestein_h(int cls, const RingDesc* descs_dev, int n, double2* tabs,
                         cudaStream_t s);
+
+// Device-side barrier of the fused exchange: worker `rank` publishes `epoch` into every
+// worker's flag array (system-scope release) and waits until all workers published it into
+// its own (acquire).  flags[w]: address of worker w's n-word flag array, valid on this device.
+constexpr int PEER_MAX = 64;
+struct PeerFlags {
+    unsigned int* f[PEER_MAX];
+};
+void launch_peer_barrier(const PeerFlags& flags, int rank, int n, unsigned int epoch, cudaStream_t s);
 
 // FP64 peak probe.
 void launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s);

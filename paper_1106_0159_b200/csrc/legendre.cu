@@ -64,6 +64,13 @@ __device__ __forceinline__ double rec_step(double A, double x, double q1, double
     return __fma_rn(__dmul_rn(A, x), q1, -q0);
 }
 
+// Delta row of ring r for the alm2map output: the local panel (delta + row_off[r]) or, on the
+// fused exchange path, ring r's row in its owner's receive buffer (peer memory over NVLink)
+__device__ __forceinline__ double2* leg_row(const LegPlanView& p, double2* delta,
+                                            const int64_t* __restrict__ row_off, int r) {
+    return p.row_ptr ? p.row_ptr[r] : delta + row_off[r];
+}
+
 }  // namespace
 
 // ---------------------------------------------------------------------------------------
@@ -443,8 +450,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
             if (s >= p.st.n) continue;
             const double2 e = L.ae[r], o = L.ao[r];  // dead lanes stayed zero
             const int north = p.st.north[s], south = p.st.south[s];
-            delta[row_off[north] + mi] = cadd(e, o);
-            if (south >= 0) delta[row_off[south] + mi] = csub(e, o);
+            leg_row(p, delta, row_off, north)[mi] = cadd(e, o);
+            if (south >= 0) leg_row(p, delta, row_off, south)[mi] = csub(e, o);
         }
     }
 }
@@ -458,9 +465,9 @@ __global__ void leg_zero_dead_kernel(LegPlanView p, double2* __restrict__ delta,
     const int t = s / LEG_TILE;
     if (p.tile_info[(size_t)mi * p.n_tiles + t].x >= 0) return;
     const double2 z = make_double2(0.0, 0.0);
-    delta[row_off[p.st.north[s]] + mi] = z;
+    leg_row(p, delta, row_off, p.st.north[s])[mi] = z;
     const int south = p.st.south[s];
-    if (south >= 0) delta[row_off[south] + mi] = z;
+    if (south >= 0) leg_row(p, delta, row_off, south)[mi] = z;
 }
 
 int leg_persistent_blocks(int device) {

@@ -277,6 +277,11 @@ __device__ __forceinline__ void build_phase(double2* lo, double2* hi, int nhi, d
 __device__ __forceinline__ int64_t delta_index(const RingStageArgs& a, int pos, int m) {
     return a.m_base ? a.m_base[m] + (int64_t)pos * a.m_stride[m] : (int64_t)m + (int64_t)pos * a.ld;
 }
+// analysis output slot of Delta^S(pos, m): local panel / receive-shaped block, or the order
+// owner's send buffer (fused exchange over peer memory)
+__device__ __forceinline__ double2* delta_out_at(const RingStageArgs& a, int pos, int m) {
+    return a.col_ptr ? a.col_ptr[m] + (int64_t)pos * a.m_stride[m] : a.delta_out + delta_index(a, pos, m);
+}
 __device__ __forceinline__ double2 delta_at(const RingStageArgs& a, int pos, int m) {
     return a.delta_in[delta_index(a, pos, m)];
 }
@@ -788,7 +793,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
                 if (cj[u]) B = cconj(B);
                 double2 val = cscale(B, wgt);
                 if (rot && m > 0) val = cmul(val, cconj(ph.at(m <= mmax ? m : 0)));
-                if (m <= mmax) a.delta_out[delta_index(a, pos, m)] = val;
+                if (m <= mmax) *delta_out_at(a, pos, m) = val;
             }
         }
         if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
@@ -934,7 +939,7 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_anal_kerne
         }
         double2 v = cscale(val, wgt);
         if (rot && m > 0) v = cmul(v, cconj(ph.at(m)));
-        a.delta_out[delta_index(a, pos, m)] = v;
+        *delta_out_at(a, pos, m) = v;
     }
 }
 
@@ -1196,6 +1201,31 @@ __global__ void dfma_peak_kernel(double* out, int iters) {
     }
     const double r = a0 + a1 + a2 + a3 + a4 + a5 + a6 + a7;
     if (r == 1234.5) out[0] = r;  // keep the chains alive
+}
+
+// ---------------------------------------------------------------------------------------
+// fused exchange: device-side barrier over peer flag words (one thread)
+// ---------------------------------------------------------------------------------------
+__global__ void peer_barrier_kernel(PeerFlags fl, int rank, int n, unsigned int epoch) {
+    // the stage kernel before this one on the stream has completed (its peer stores are
+    // ordered before this thread); release them to every worker together with the flag
+    __threadfence_system();
+    for (int w = 0; w < n; ++w)
+        asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(fl.f[w] + rank), "r"(epoch) : "memory");
+    for (int w = 0; w < n; ++w) {
+        unsigned int v = 0;
+        long long spins = 0;
+        for (;;) {
+            asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(fl.f[rank] + w) : "memory");
+            if ((int)(v - epoch) >= 0) break;
+            __nanosleep(64);
+            if (++spins > (1LL << 27)) __trap();  // a worker never arrived (~10 s): fail loudly
+        }
+    }
+}
+
+void launch_peer_barrier(const PeerFlags& flags, int rank, int n, unsigned int epoch, cudaStream_t s) {
+    peer_barrier_kernel<<<1, 1, 0, s>>>(flags, rank, n, epoch);
 }
 
 void launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s) {

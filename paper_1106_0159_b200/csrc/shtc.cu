@@ -164,6 +164,10 @@ struct shtc_ctx {
     std::vector<int> ring_list;
     std::vector<int64_t> m_base, m_stride;
     DevBuf row_off_d, m_base_d, m_stride_d;
+    // fused exchange over peer memory: per-ring row / per-order column addresses in the
+    // owners' buffers (valid on this device: NVLink peer mappings or CUDA IPC)
+    DevBuf peer_row_ptr, peer_col_ptr;
+    bool peers_set = false;
     // identity layout for whole transforms
     DevBuf id_row_off, id_m_base, id_m_stride;
     // plans
@@ -653,6 +657,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
             for (int k = 0; k < kPipeChunks; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
         }
     }
+    F.counters.ensure(FFT_N_CLASSES * sizeof(int));  // no allocation on the transform path
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float el = 0.f;
@@ -755,10 +760,11 @@ void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
 }
 
 void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
-                   const int64_t* mst, int range = -1) {
+                   const int64_t* mst, int range = -1, double2* const* col_ptr = nullptr) {
     ring_stage(c, F, range, [&](int k, RingStageArgs& a, cudaStream_t st) {
         a.m_base = mb;
         a.m_stride = mst;
+        a.col_ptr = col_ptr;
         a.map_in = map;
         a.delta_out = delta;
         launch_ring_analysis(k, a, st);
@@ -1306,6 +1312,122 @@ shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double*
             *t = shtc_timing{};
             t->fft_ms = t->total_ms = elapsed(ctx->ev[0], ctx->ev[1]);
         }
+    });
+}
+
+// ---- fused exchange over peer memory ----------------------------------------------------
+// exchange_m_to_rings / exchange_rings_to_m (distribution.cpp:233-298) as direct stores from
+// the producing kernels into the consumers' buffers, then one device-side barrier.
+shtc_status shtc_dev_alloc(int device, uint64_t bytes, void** ptr) {
+    if (!ptr || bytes == 0) return SHTC_EINVAL;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        void* p = nullptr;
+        if (cudaMalloc(&p, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            fail(SHTC_ENOMEM, "shtc_dev_alloc: cudaMalloc failed");
+        }
+        CK(cudaMemset(p, 0, bytes));
+        *ptr = p;
+    });
+}
+
+shtc_status shtc_dev_free(void* ptr) {
+    return guarded(nullptr, [&] {
+        if (ptr) CK(cudaFree(ptr));
+    });
+}
+
+shtc_status shtc_ipc_handle(const void* ptr, unsigned char* handle64) {
+    if (!ptr || !handle64) return SHTC_EINVAL;
+    return guarded(nullptr, [&] {
+        cudaIpcMemHandle_t h;
+        CK(cudaIpcGetMemHandle(&h, const_cast<void*>(ptr)));
+        static_assert(sizeof(h) == 64, "CUDA IPC handle size");
+        std::memcpy(handle64, &h, 64);
+    });
+}
+
+shtc_status shtc_ipc_open(int device, const unsigned char* handle64, void** ptr) {
+    if (!handle64 || !ptr) return SHTC_EINVAL;
+    return guarded(nullptr, [&] {
+        CK(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle64, 64);
+        CK(cudaIpcOpenMemHandle(ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+shtc_status shtc_ipc_close(void* ptr) {
+    return guarded(nullptr, [&] {
+        if (ptr) CK(cudaIpcCloseMemHandle(ptr));
+    });
+}
+
+shtc_status shtc_set_exchange_peers(shtc_ctx* ctx, const uint64_t* row_ptr, const uint64_t* col_ptr) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (!row_ptr || !col_ptr) {
+            ctx->peers_set = false;
+            return;
+        }
+        if (!ctx->custom_layout) fail(SHTC_EINVAL, "exchange peers: set the exchange layout first");
+        std::vector<uint64_t> rp(row_ptr, row_ptr + ctx->n_rings), cp(col_ptr, col_ptr + ctx->mmax + 1);
+        ctx->peer_row_ptr.upload(rp, ctx->stream);
+        ctx->peer_col_ptr.upload(cp, ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->peers_set = true;
+    });
+}
+
+shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, shtc_timing* t) {
+    if (!ctx || !alm_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->peers_set) fail(SHTC_EINVAL, "exchange peers not set");
+        ensure_leg_plan(ctx);
+        LegPlanView v = ctx->leg.view;
+        v.row_ptr = ctx->peer_row_ptr.as<double2*>();
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        launch_leg_alm2map(v, reinterpret_cast<const double2*>(alm_dev), nullptr,
+                           ctx->row_off_d.as<int64_t>(), ctx->leg.counters.as<int>(), ctx->stream);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+        }
+    });
+}
+
+shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_timing* t) {
+    if (!ctx || !map_dev) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->peers_set) fail(SHTC_EINVAL, "exchange peers not set");
+        CK(cudaEventRecord(ctx->ev[0], ctx->stream));
+        run_ring_anal(ctx, ctx->fft_custom, map_dev, nullptr, ctx->m_base_d.as<int64_t>(),
+                      ctx->m_stride_d.as<int64_t>(), -1, ctx->peer_col_ptr.as<double2*>());
+        CK(cudaEventRecord(ctx->ev[1], ctx->stream));
+        if (t) {
+            CK(cudaEventSynchronize(ctx->ev[1]));
+            *t = shtc_timing{};
+            t->fft_ms = t->total_ms = elapsed(ctx->ev[0], ctx->ev[1]);
+        }
+    });
+}
+
+shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint64_t* flags,
+                              uint32_t epoch) {
+    if (!ctx || !flags || n_workers < 1 || n_workers > PEER_MAX || rank < 0 || rank >= n_workers)
+        return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        PeerFlags f{};
+        for (int w = 0; w < n_workers; ++w) {
+            if (!flags[w]) fail(SHTC_EINVAL, "peer barrier: null flag array");
+            f.f[w] = reinterpret_cast<unsigned int*>(flags[w]);
+        }
+        launch_peer_barrier(f, rank, n_workers, epoch, ctx->stream);
+        CK(cudaGetLastError());
     });
 }
 

@@ -328,6 +328,40 @@ def exchange_layout(layout: WorkerLayout, rank: int):
     return row_off, send_counts, recv_counts, np.asarray(Ri, np.int32), m_base, m_stride
 
 
+def exchange_sizes(layout: WorkerLayout, rank: int):
+    """(send, recv) buffer sizes of one worker in complex elements."""
+    Mi, Ri = len(layout.m_sets[rank]), len(layout.ring_sets[rank])
+    send = sum(len(Rj) for Rj in layout.ring_sets) * Mi
+    recv = Ri * sum(len(Mj) for Mj in layout.m_sets)
+    return send, recv
+
+
+def peer_exchange_pointers(layout: WorkerLayout, rank: int, recv_bases, send_bases):
+    """Store targets of worker `rank` on the fused exchange path (shtc_set_exchange_peers).
+
+    recv_bases[j] / send_bases[j]: device addresses (valid in this process) of worker j's
+    receive / send buffers, laid out as exchange_layout describes.  Returns
+      row_ptr[r]: where ring r's row of this worker's orders goes in the ring owner's receive
+                  buffer (the block from source `rank`, row pos * |M_rank|);
+      col_ptr[m]: order m's column for this worker's ring position 0 in the order owner's send
+                  buffer (the block for destination `rank`), rows |M_owner| apart (m_stride).
+    Byte addresses as uint64 (16-byte complex elements)."""
+    W = layout.n_workers
+    Msz = [len(M) for M in layout.m_sets]
+    Rsz = [len(R) for R in layout.ring_sets]
+    row_ptr = np.zeros(layout.n_rings, np.uint64)
+    for j in range(W):
+        off = sum(Rsz[j] * Msz[s] for s in range(rank))  # block of source `rank` in j's recv
+        for pos, r in enumerate(layout.ring_sets[j]):
+            row_ptr[r] = int(recv_bases[j]) + 16 * (off + pos * Msz[rank])
+    col_ptr = np.zeros(layout.mmax + 1, np.uint64)
+    for i in range(W):
+        soff = sum(Rsz[d] * Msz[i] for d in range(rank))  # block for destination `rank` in i's send
+        for c, m in enumerate(layout.m_sets[i]):
+            col_ptr[m] = int(send_bases[i]) + 16 * (soff + c)
+    return row_ptr, col_ptr
+
+
 # ----------------------------------------------------------------------------------------
 # GPU context
 # ----------------------------------------------------------------------------------------
@@ -455,6 +489,29 @@ class Context:
                                                  C.byref(t) if timing else None))
         return t.as_dict() if timing else None
 
+    # fused exchange over peer memory (see PeerExchange) ---------------------------------
+    def set_exchange_peers(self, row_ptr=None, col_ptr=None):
+        if row_ptr is None:
+            self._check(lib().shtc_set_exchange_peers(self._h, None, None))
+            return
+        rp = np.ascontiguousarray(row_ptr, np.uint64)
+        cp = np.ascontiguousarray(col_ptr, np.uint64)
+        self._check(lib().shtc_set_exchange_peers(self._h, _p(rp), _p(cp)))
+
+    def legendre_alm2map_peer(self, alm_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_legendre_alm2map_peer(self._h, C.c_void_p(alm_ptr), C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def ring_analysis_peer(self, map_ptr, timing=False):
+        t = Timing()
+        self._check(lib().shtc_ring_analysis_peer(self._h, C.c_void_p(map_ptr), C.byref(t) if timing else None))
+        return t.as_dict() if timing else None
+
+    def peer_barrier(self, rank: int, n_workers: int, flag_ptrs, epoch: int):
+        f = np.ascontiguousarray(flag_ptrs, np.uint64)
+        self._check(lib().shtc_peer_barrier(self._h, rank, n_workers, _p(f), C.c_uint32(epoch & 0xFFFFFFFF)))
+
     # Legendre-stage operators ----------------------------------------------------------
     def delta_a(self, alm, lmax, mmax, x, ms):
         alm = np.ascontiguousarray(alm, np.complex128)
@@ -479,6 +536,116 @@ class Context:
 
 
 _DEFAULT = {}
+
+
+# ----------------------------------------------------------------------------------------
+# fused exchange over peer memory
+# ----------------------------------------------------------------------------------------
+def dev_alloc(device: int, nbytes: int) -> int:
+    p = C.c_void_p()
+    check(lib().shtc_dev_alloc(int(device), int(nbytes), C.byref(p)))
+    return int(p.value)
+
+
+def dev_free(ptr: int):
+    check(lib().shtc_dev_free(C.c_void_p(ptr)))
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = C.create_string_buffer(64)
+    check(lib().shtc_ipc_handle(C.c_void_p(ptr), buf))
+    return buf.raw
+
+
+def ipc_open(device: int, handle: bytes) -> int:
+    p = C.c_void_p()
+    check(lib().shtc_ipc_open(int(device), C.c_char_p(handle), C.byref(p)))
+    return int(p.value)
+
+
+def ipc_close(ptr: int):
+    check(lib().shtc_ipc_close(C.c_void_p(ptr)))
+
+
+class PeerExchange:
+    """One worker's side of the fused exchange (distributed_synthesis/analysis, distribution.cpp:
+    300-490, with exchange_m_to_rings / rings_to_m as direct peer stores).
+
+    Owns this worker's send buffer (Legendre side: a_lm orders x all rings), receive buffer
+    (ring side: its rings x all orders) and barrier flags, all from shtc_dev_alloc; maps the
+    other workers' buffers through CUDA IPC (`all_gather(obj) -> list over ranks`, e.g. over
+    torch.distributed) or, for workers of one process, takes their addresses directly.
+
+        alm2map: legendre_alm2map_peer(alm) -> barrier -> ring_synthesis_dev(recv, map)
+        map2alm: ring_analysis_peer(map) -> barrier -> legendre_map2alm_dev(send, alm)
+    """
+
+    def __init__(self, ctx: Context, layout: WorkerLayout, rank: int, all_gather=None, peers=None):
+        self.ctx, self.layout, self.rank = ctx, layout, rank
+        W = layout.n_workers
+        self.n = W
+        send_c, recv_c = exchange_sizes(layout, rank)
+        dev = ctx.device
+        self.send = dev_alloc(dev, 16 * max(send_c, 1))
+        self.recv = dev_alloc(dev, 16 * max(recv_c, 1))
+        self.flags = dev_alloc(dev, 4 * W)
+        self.epoch = 0
+        self._opened = []
+        mine = (self.send, self.recv, self.flags)
+        if peers is not None:                       # workers in one process: plain addresses
+            self._peers = peers
+            self._peers[rank] = mine
+            return
+        hs = all_gather((ipc_handle(self.send), ipc_handle(self.recv), ipc_handle(self.flags)))
+        addrs = []
+        for j, h in enumerate(hs):
+            if j == rank:
+                addrs.append(mine)
+                continue
+            a = tuple(ipc_open(dev, x) for x in h)
+            self._opened += list(a)
+            addrs.append(a)
+        self._peers = addrs
+        self.connect()
+
+    def connect(self):
+        """Set the layout and the peer store targets on the context (after every worker of
+        a single-process group is constructed)."""
+        row_off, send_c, recv_c, ring_list, m_base, m_stride = exchange_layout(self.layout, self.rank)
+        self.ctx.set_exchange_layout(row_off, ring_list, m_base, m_stride)
+        send_b = [p[0] for p in self._peers]
+        recv_b = [p[1] for p in self._peers]
+        row_ptr, col_ptr = peer_exchange_pointers(self.layout, self.rank, recv_b, send_b)
+        self.ctx.set_exchange_peers(row_ptr, col_ptr)
+        self._flag_ptrs = np.array([p[2] for p in self._peers], np.uint64)
+        # build every plan now: no allocation or synchronising call may run once a worker's
+        # barrier kernel is waiting for the others
+        self.ctx.plan()
+
+    def barrier(self):
+        self.epoch += 1
+        self.ctx.peer_barrier(self.rank, self.n, self._flag_ptrs, self.epoch)
+
+    def alm2map(self, alm_ptr: int, map_ptr: int, timing=False):
+        t1 = self.ctx.legendre_alm2map_peer(alm_ptr, timing)
+        self.barrier()
+        t2 = self.ctx.ring_synthesis_dev(self.recv, map_ptr, timing)
+        return (t1, t2) if timing else None
+
+    def map2alm(self, map_ptr: int, alm_ptr: int, timing=False):
+        t1 = self.ctx.ring_analysis_peer(map_ptr, timing)
+        self.barrier()
+        t2 = self.ctx.legendre_map2alm_dev(self.send, alm_ptr, timing)
+        return (t2, t1) if timing else None
+
+    def close(self):
+        for p in self._opened:
+            ipc_close(p)
+        self._opened = []
+        for p in (self.send, self.recv, self.flags):
+            if p:
+                dev_free(p)
+        self.send = self.recv = self.flags = 0
 
 
 def default_context(device: int = 0) -> Context:
