@@ -152,9 +152,11 @@ struct RingStageArgs {
 //   0: B<=256 (64 thr), 1: B<=1024 (256), 2: B<=4096 (512), 3: B<=8192 (1024).
 // Power-of-two engine (half-mode rings with a power-of-two buffer B = 256, 512, ..., 8192):
 //   4..9 direct FFTs of length B, 10..15 Bluestein convolutions of length B.
+// Cluster class: Bluestein buffers of 16384 points, one ring per 2-CTA cluster (class 16).
 constexpr int FFT_N_GENERIC = 4;
 constexpr int FFT_P2_MIN = 256, FFT_P2_MAX = 8192, FFT_N_P2 = 6;
-constexpr int FFT_N_CLASSES = FFT_N_GENERIC + 2 * FFT_N_P2;
+constexpr int FFT_P2C_CLASS = FFT_N_GENERIC + 2 * FFT_N_P2, FFT_P2C_B = 16384;
+constexpr int FFT_N_CLASSES = FFT_P2C_CLASS + 1;
 int fft_class_bmax(int c);
 int fft_class_for(int B);     // generic class, -1 if unsupported
 int fft_p2_class_for(int B, bool bluestein);  // power-of-two engine class, -1: not one of its lengths
@@ -172,6 +174,9 @@ void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cud
 // For each Bluestein ring descriptor (deduplicated by N): tabs[h_off..] = FFT_B(h).
 void launch_bluestein_h(int cls, const RingDesc* descs_dev, int n, double2* tabs,
                         cudaStream_t s);
+// Cluster class: tabs[h_off..] = FFT_16384(h) (tw_off: e^{-2 pi i k/16384}; tw_half: the
+// 8192-point table of the half transforms).
+void launch_p2c_h(const RingDesc* descs_dev, int n, double2* tabs, const double2* tw_half, cudaStream_t s);
 
 // Device-side barrier of the fused exchange: worker `rank` publishes `epoch` into every
 // worker's flag array (system-scope release) and waits until all workers published it into

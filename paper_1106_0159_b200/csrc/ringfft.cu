@@ -20,6 +20,8 @@
 
 #include <climits>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "fftcore.cuh"
 #include "kernels.h"
@@ -802,6 +804,210 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
 }
 
 // ---------------------------------------------------------------------------------------
+// Bluestein buffers of 16384 points (rings of more than 8192 samples whose half length is not
+// a power of two, nside >= 4096): one ring per 2-CTA cluster.  The convolution FFT of length
+// M = 2 MH is split by one decimation-in-frequency step: CTA h transforms the MH-point
+// sequence x_b + (-1)^h x_{b+MH} (twiddled by W_M^b for h = 1), giving the outputs 2k + h.
+// The chirped input lives in [0, N) with N < MH, so both halves start from the same x_b and
+// need no exchange; after the pointwise product and the inverse MH-point transforms, the time
+// samples b < MH are u_b + W_M^{-b} v_b: CTA 1 hands v to CTA 0 through distributed shared
+// memory.  Each CTA keeps its half in registers (E = 16 per thread, 512 threads).
+// ---------------------------------------------------------------------------------------
+namespace cg = cooperative_groups;
+
+template <bool SYN>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_kernel(RingStageArgs a) {
+    constexpr int MH = FFT_P2C_B / 2, E = 16, T = MH / E, G = 8;
+    extern __shared__ __align__(16) double2 smem[];
+    double2* buf = smem;
+    double2* phlo = smem + p2pad(MH) + 16;
+    cg::cluster_group cluster = cg::this_cluster();
+    const int h = (int)cluster.block_rank();
+    const int t = threadIdx.x, mmax = a.mmax;
+    const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
+    const PhaseTab ph{phlo, phlo + 64};
+    for (int ri = cl; ri < a.n_rings; ri += ncl) {
+        if (h == 0) p2_prefetch_ring<FFT_P2C_B, T, SYN>(a, ri + ncl);
+        double2 v[E];
+        {
+            const RingDesc& d = desc_at(a, ri);
+            const int n = d.n, N = d.N, pos = d.ring_pos;
+            const double phi0 = d.phi0;
+            const bool rot = phi0 != 0.0;
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            if (SYN) {
+                if (rot) {
+                    build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                    __syncthreads();
+                }
+                // fold: H_k for 0 <= k <= N (n = 2N > mmax here: no wraps)
+#pragma unroll
+                for (int j0 = 0; j0 < E; j0 += G) {
+                    double2 x1[G], x2[G];
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const int k = t + T * (j0 + u);
+                        const int m1 = k, m2 = (k == 0) ? n : n - k;
+                        x1[u] = a.delta_in[delta_index(a, pos, (k <= N && m1 <= mmax) ? m1 : 0)];
+                        x2[u] = a.delta_in[delta_index(a, pos, (k <= N && m2 <= mmax) ? m2 : 0)];
+                    }
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const int k = t + T * (j0 + u);
+                        if (k <= N) {
+                            const int m1 = k, m2 = (k == 0) ? n : n - k;
+                            double2 hk = make_double2(0.0, 0.0);
+                            if (m1 <= mmax) hk = rot_value(x1[u], m1, rot, ph);
+                            if (m2 <= mmax) hk = cadd(hk, cconj(rot_value(x2[u], m2, rot, ph)));
+                            buf[p2pad(k)] = hk;
+                        }
+                    }
+                }
+                __syncthreads();
+                const double2* __restrict__ hw = a.tabs + d.hw_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    const int kc = k < N ? k : 0;
+                    const double2 w = __ldg(&hw[kc]), c = __ldg(&chirp[kc]);
+                    const double2 Hp = buf[p2pad(kc)], Hq = buf[p2pad(N - kc)];
+                    const double2 e = cadd(Hp, cconj(Hq));
+                    const double2 o = cmul(csub(Hp, cconj(Hq)), cconj(w));
+                    const double2 z = cmul(cadd(e, cmul_si(o, +1)), cconj(c));
+                    v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                }
+                __syncthreads();  // H read before the first pass overwrites buf
+            } else {
+                if (h == 0 && rot) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                const int64_t po = d.pix_off;
+                const double* __restrict__ in = a.map_in + po;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    const int kc = k < N ? k : 0;
+                    const double2 x = ((po & 1) == 0) ? reinterpret_cast<const double2*>(in)[kc]
+                                                      : make_double2(in[2 * kc], in[2 * kc + 1]);
+                    const double2 z = cmul(x, __ldg(&chirp[kc]));
+                    v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                }
+            }
+            if (h == 1) {  // DIF split: odd outputs from x_b W_M^b
+                const double2* __restrict__ twm = a.tabs + d.tw_off;  // e^{-2 pi i b / M}
+#pragma unroll
+                for (int j = 0; j < E; ++j) v[j] = cmul(v[j], __ldg(&twm[t + T * j]));
+            }
+        }
+        p2_fft<MH, E, -1>(v, buf, a.p2_tw);
+        __threadfence_block();
+        {
+            const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const double2 hv = __ldg(&H[2 * (t + T * j) + h]);
+                v[j] = cmul(v[j], SYN ? cconj(hv) : hv);
+            }
+        }
+        p2_fft<MH, E, +1>(v, buf, a.p2_tw);
+        if (h == 1) {
+            const double2* __restrict__ twm = a.tabs + desc_at(a, ri).tw_off;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                v[j] = cmul(v[j], cconj(__ldg(&twm[t + T * j])));
+                buf[p2pad(t + T * j)] = v[j];
+            }
+        }
+        cluster.sync();
+        if (h == 0) {
+            const double2* rb = cluster.map_shared_rank(buf, 1);
+#pragma unroll
+            for (int j = 0; j < E; ++j) v[j] = cadd(v[j], rb[p2pad(t + T * j)]);
+        }
+        cluster.sync();  // CTA 1's buffer is reused by the next ring
+        if (h == 0) {
+            const RingDesc& d = desc_at(a, ri);
+            const int N = d.N;
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            const double inv = 1.0 / (double)FFT_P2C_B;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                const double2 c = __ldg(&chirp[k < N ? k : 0]);
+                v[j] = cscale(cmul(v[j], SYN ? cconj(c) : c), inv);
+            }
+            if (SYN) {
+                const int64_t po = d.pix_off;
+                double* __restrict__ out = a.map_out + po;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) {
+                        if ((po & 1) == 0) {
+                            reinterpret_cast<double2*>(out)[k] = v[j];
+                        } else {
+                            out[2 * k] = v[j].x;
+                            out[2 * k + 1] = v[j].y;
+                        }
+                    }
+                }
+            } else {
+                const int n = d.n, pos = d.ring_pos;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) buf[p2pad(k)] = v[j];
+                }
+                __syncthreads();
+                const double wgt = d.weight;
+                const bool rot = d.phi0 != 0.0;
+                const double2* __restrict__ hw = a.tabs + d.hw_off;
+                for (int m = t; m <= mmax; m += T) {
+                    const int b = m % n;
+                    const bool cj = b > N;
+                    const int bb = cj ? n - b : b;
+                    const double2 Zp = buf[p2pad(bb == N ? 0 : bb)];
+                    const double2 Zq = buf[p2pad(bb == 0 ? 0 : N - bb)];
+                    const double2 e = cscale(cadd(Zp, cconj(Zq)), 0.5);
+                    const double2 o = cmul_si(cscale(csub(Zp, cconj(Zq)), 0.5), -1);
+                    double2 B = cadd(e, cmul(__ldg(&hw[bb]), o));
+                    if (cj) B = cconj(B);
+                    double2 val = cscale(B, wgt);
+                    if (rot && m > 0) val = cmul(val, cconj(ph.at(m)));
+                    *delta_out_at(a, pos, m) = val;
+                }
+            }
+        }
+        __syncthreads();  // buf / phase table reuse by the next ring
+    }
+}
+
+// FFT_M of Bluestein's h (h_d = conj chirp_|d|, cyclic) in natural order, by the same split:
+// block 2i + h writes the outputs 2k + h of descriptor i.
+__global__ void __launch_bounds__(512, 1) p2c_h_kernel(const RingDesc* __restrict__ descs,
+                                                       double2* __restrict__ tabs, const double2* __restrict__ tw_half) {
+    constexpr int M = FFT_P2C_B, MH = M / 2, E = 16, T = MH / E;
+    extern __shared__ __align__(16) double2 smem[];
+    const RingDesc d = descs[blockIdx.x >> 1];
+    const int h = blockIdx.x & 1, N = d.N, t = threadIdx.x;
+    const double2* chirp = tabs + d.chirp_off;
+    const double2* twm = tabs + d.tw_off;
+    auto hval = [&](int i) {
+        if (i < N) return cconj(chirp[i]);
+        if (i > M - N) return cconj(chirp[M - i]);
+        return make_double2(0.0, 0.0);
+    };
+    double2 v[E];
+#pragma unroll
+    for (int j = 0; j < E; ++j) {
+        const int b = t + T * j;
+        const double2 lo = hval(b), hi = hval(b + MH);
+        v[j] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), twm[b]);
+    }
+    p2_fft<MH, E, -1>(v, smem, tw_half);
+#pragma unroll
+    for (int j = 0; j < E; ++j) tabs[d.h_off + 2 * (t + T * j) + h] = v[j];
+}
+
+// ---------------------------------------------------------------------------------------
 // synthesis: Delta rows -> ring samples
 // ---------------------------------------------------------------------------------------
 template <int T, int BMAX>
@@ -1139,8 +1345,48 @@ void p2_dispatch(int cls, const RingStageArgs& a, cudaStream_t s) {
 }
 }  // namespace
 
+namespace {
+size_t p2c_smem(int mmax) {
+    return (size_t)(FFT_P2C_B / 2 + FFT_P2C_B / 32 + 16) * sizeof(double2) +
+           (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
+}
+template <bool SYN>
+void p2c_run(const RingStageArgs& a, cudaStream_t s) {
+    auto k = ring_p2c_kernel<SYN>;
+    static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p2c_smem(kMaxPhaseM)),
+                        true);
+    (void)once;
+    const size_t sm = p2c_smem(a.mmax);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(2, 1, 1);
+    cfg.blockDim = dim3(512, 1, 1);
+    cfg.dynamicSmemBytes = sm;
+    int ncl = 0;
+    if (cudaOccupancyMaxActiveClusters(&ncl, k, &cfg) != cudaSuccess || ncl < 1) {
+        cudaGetLastError();
+        ncl = 64;
+    }
+    if (ncl > a.n_rings) ncl = a.n_rings;
+    k<<<2 * ncl, 512, sm, s>>>(a);
+}
+}  // namespace
+
 int fft_class_bmax(int c) {
+    if (c == FFT_P2C_CLASS) return FFT_P2C_B;
     return c < FFT_N_GENERIC ? kBmax[c] : FFT_P2_MIN << ((c - FFT_N_GENERIC) % FFT_N_P2);
+}
+
+void launch_p2c_h(const RingDesc* descs_dev, int n, double2* tabs, const double2* tw_half, cudaStream_t s) {
+    if (n == 0) return;
+    static bool once = (cudaFuncSetAttribute(p2c_h_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p2c_smem(0)),
+                        true);
+    (void)once;
+    for (int r0 = 0; r0 < n; r0 += 32767) {
+        const int nr = n - r0 < 32767 ? n - r0 : 32767;
+        p2c_h_kernel<<<2 * nr, 512, p2c_smem(0), s>>>(descs_dev + r0, tabs, tw_half);
+    }
 }
 int fft_class_for(int B) {
     for (int c = 0; c < FFT_N_GENERIC; ++c)
@@ -1161,6 +1407,7 @@ void launch_ring_synthesis(int cls, const RingStageArgs& a, cudaStream_t s) {
         case 1: synth_c<1>(a, s); break;
         case 2: synth_c<2>(a, s); break;
         case 3: synth_c<3>(a, s); break;
+        case FFT_P2C_CLASS: p2c_run<true>(a, s); break;
         default: p2_dispatch<true>(cls, a, s); break;
     }
 }
@@ -1171,6 +1418,7 @@ void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s) {
         case 1: anal_c<1>(a, s); break;
         case 2: anal_c<2>(a, s); break;
         case 3: anal_c<3>(a, s); break;
+        case FFT_P2C_CLASS: p2c_run<false>(a, s); break;
         default: p2_dispatch<false>(cls, a, s); break;
     }
 }

@@ -268,8 +268,11 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     const int nt = (ns + LEG_TILE - 1) / LEG_TILE;
     std::vector<int64_t> pix(nt, 0);
     int64_t total = 0;
+    // pixel weight of a stream's rings; operator plans (latitudes without a grid) weigh 1 each
+    const int nr = (int)c->nphi.size();
+    auto w = [&](int r) -> int64_t { return r < 0 ? 0 : (r < nr ? c->nphi[r] : 1); };
     for (int i = 0; i < ns; ++i) {
-        const int64_t p = c->nphi[st[i].north] + (st[i].south >= 0 ? c->nphi[st[i].south] : 0);
+        const int64_t p = w(st[i].north) + w(st[i].south);
         pix[i / LEG_TILE] += p;
         total += p;
     }
@@ -570,6 +573,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
     std::map<int, int64_t> h_at;  // Bluestein N -> H offset
     std::vector<RingDesc> per_class[FFT_N_CLASSES];
     std::vector<RingDesc> blue_class[FFT_N_CLASSES];
+    std::vector<RingDesc> blue_clus;
     for (size_t pos = 0; pos < rings.size(); ++pos) {
         const int r = rings[pos];
         RingDesc d{};
@@ -591,16 +595,19 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         // buffers) the generic in-place mixed-radix kernels.  Bluestein's FFT(conj chirp) is
         // built by the generic class of the same length at plan time.
         const int gcls = fft_class_for(d.B);
-        int cls = half ? fft_p2_class_for(d.B, !smooth) : -1;
+        const bool clus = half && d.B == FFT_P2C_B;  // 16384-point Bluestein: 2-CTA clusters
+        int cls = clus ? FFT_P2C_CLASS : (half ? fft_p2_class_for(d.B, !smooth) : -1);
         if (cls < 0) cls = gcls;
-        if (gcls < 0)
+        if (cls < 0)
             fail(SHTC_EUNSUPPORTED, "ring length " + std::to_string(d.n) +
                                         " needs an FFT buffer beyond the shared-memory classes");
-        auto rp = radix_plan(d.B);
-        d.npass = (int)rp.size();
-        if (rp.size() > (size_t)FFT_MAX_PASSES) fail(SHTC_EUNSUPPORTED, "radix plan too long");
-        d.radices = 0;
-        for (size_t i = 0; i < rp.size(); ++i) d.radices |= (unsigned long long)rp[i] << (4 * i);
+        if (gcls >= 0) {
+            auto rp = radix_plan(d.B);
+            d.npass = (int)rp.size();
+            if (rp.size() > (size_t)FFT_MAX_PASSES) fail(SHTC_EUNSUPPORTED, "radix plan too long");
+            d.radices = 0;
+            for (size_t i = 0; i < rp.size(); ++i) d.radices |= (unsigned long long)rp[i] << (4 * i);
+        }
         d.tw_off = table(0, d.B);
         d.hw_off = half ? table(1, d.n) : 0;
         if (!smooth) {
@@ -610,13 +617,14 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
                 d.h_off = tot;
                 tot += d.B;
                 h_at[d.N] = d.h_off;
-                blue_class[gcls].push_back(d);
+                if (clus) blue_clus.push_back(d);
+                else blue_class[gcls].push_back(d);
             } else {
                 d.h_off = it->second;
             }
         }
         per_class[cls].push_back(d);
-        F.tw_off[cls] = d.tw_off;
+        F.tw_off[cls] = clus ? table(0, FFT_P2C_B / 2) : d.tw_off;
     }
     F.tabs.ensure((size_t)std::max<int64_t>(tot, 1) * sizeof(double2));
     DevBuf jobs_d;
@@ -632,6 +640,14 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
             CK(cudaStreamSynchronize(s));
         }
         F.count[k] = (int)per_class[k].size();
+    }
+    if (!blue_clus.empty()) {
+        DevBuf bd;
+        bd.upload(blue_clus, s);
+        launch_p2c_h(bd.as<RingDesc>(), (int)blue_clus.size(), F.tabs.as<double2>(),
+                     F.tabs.as<double2>() + F.tw_off[FFT_P2C_CLASS], s);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(s));
     }
     // pipeline bands: descriptors of each class grouped by band (ring order inside a band),
     // pixel intervals of each band for the host copies
@@ -1106,6 +1122,7 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
+        CK(cudaEventSynchronize(ctx->ev[2]));  // the two streams end independently
         if (t) {
             float leg, fft;
             band_timing(ctx, leg, fft);
@@ -1169,6 +1186,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         CK(cudaEventRecord(ctx->ev[2], s));
         CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
         CK(cudaEventSynchronize(ctx->ev[6]));
+        CK(cudaEventSynchronize(ctx->ev[2]));  // the two streams end independently
         if (t) {
             float fft, leg;
             band_timing(ctx, fft, leg);

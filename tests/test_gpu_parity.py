@@ -115,3 +115,23 @@ def test_c2_alm2map_and_map2alm(gpu_ctx):
     back_ref, _ = ref.distributed_analysis(want, lmax, lmax, g, n_workers=1, n_threads=8, pairing=True)
     back = gpu_ctx.map2alm(want)
     assert rel_rms(back, back_ref) <= RMS_TOL, (rel_rms(back, back_ref), worst(back, back_ref))
+
+
+def test_c5_recurrence_depth(gpu_ctx):
+    """C5 band (lmax = mmax = 8192) through the Legendre operator on the most polar HEALPix
+    nside-4096 rings (deepest underflow ladder, k ~ -200), equatorial rings and high orders,
+    against the reference's compute_delta_a.  The whole C5 transforms' parity (4.3e-14 /
+    3.9e-14 rel-RMS) is recorded by tools/parity_large.py in profiles/r01_c5_parity.json."""
+    lmax = 8192
+    g = ref.healpix_grid(4096)
+    idx = list(range(0, 24)) + [2047, 4095, 8190, 8191, 8192]
+    x = np.asarray(g.cos_theta)[idx]
+    ms = [0, 1, 2, 1000, 4096, 6000, 8000, 8191, 8192]
+    alm = ref.random_alm(lmax, lmax, 4242)
+    want, wsteps = ref.compute_delta_a(alm, lmax, lmax, x, ms)
+    got, steps = gpu_ctx.delta_a(alm, lmax, lmax, x, ms)
+    assert steps == wsteps
+    # the recurrence's own conditioning at x -> 1 and l ~ 8000 (measured 1.2e-11 here; the
+    # reference itself is ~2e-11 off a long-double recurrence at lmax 2048): the north-star gate
+    assert rel_rms(got, want) <= RMS_TOL, (rel_rms(got, want), worst(got, want))
+    assert worst(got, want) <= RMS_TOL

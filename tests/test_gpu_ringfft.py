@@ -2,7 +2,8 @@
 
 One grid per case holds rings of many different lengths, so a single alm2map / map2alm touches
 the generic mixed-radix classes (tiny, odd and 7-smooth rings), the power-of-two engine's direct
-classes (N = 256 ... 8192) and its Bluestein classes (buffers 256 ... 8192), with phi_0 = 0 and
+classes (N = 256 ... 8192), its Bluestein classes (buffers 256 ... 8192) and the 2-CTA cluster
+class (Bluestein buffers of 16384), with phi_0 = 0 and
 phi_0 != 0 rings and with orders above n/2 (aliasing folds).  Oracle: the reference's
 synthesis / analysis (fourier.cpp:10-56 + fft.cpp) on the same grid and a_lm.
 """
@@ -26,6 +27,7 @@ NPHI = [
     6000,                       # 7-smooth N = 3000 > 1024: Bluestein buffer 8192
     8188, 8192,                 # Bluestein N = 4094 (8192), direct N = 4096
     16384,                      # direct N = 8192
+    8200, 12000, 16380,         # Bluestein N = 4100, 6000 (7-smooth), 8190: 16384-point, 2-CTA cluster
 ]
 
 
@@ -46,7 +48,7 @@ def rel_max(a, b):
 
 @pytest.mark.parametrize("lmax,phase", [(40, 0.0), (40, 0.5), (700, 0.5), (4200, 0.25)])
 def test_ring_classes_match_reference(gpu_ctx, lmax, phase):
-    nphi = NPHI if lmax < 4000 else [4, 130, 1030, 4100, 8188, 8192, 16384]
+    nphi = NPHI if lmax < 4000 else [4, 130, 1030, 4100, 8188, 8192, 16384, 8200, 16380]
     g = mixed_grid(nphi, phase)
     alm = ref.random_alm(lmax, lmax, 4242)
     want, _ = ref.synthesis(alm, lmax, lmax, g, pairing=True)
