@@ -366,26 +366,56 @@ __device__ __forceinline__ void store_z(double2* buf, const double2* __restrict_
 // ---------------------------------------------------------------------------------------
 __device__ __forceinline__ int p2pad(int i) { return i + (i >> 4); }
 
-// u[r] *= W_{NS R}^{r k} = W_M^{r e0}, e0 = k M / (NS R); table tw[j] = e^{-2 pi i j / M}
-template <int R, int S>
-__device__ __forceinline__ void p2_twiddle(double2 (&u)[R], int e0, const double2* __restrict__ tw) {
-    // a plain (coherent) load: ptxas may hoist read-only (.nc) loads of every later pass above
-    // the exchange barriers, which keeps all passes' twiddles live at once
-    auto ld = [&](int e) {
-        double2 w;
-        asm("ld.global.v2.f64 {%0, %1}, [%2];" : "=d"(w.x), "=d"(w.y) : "l"(tw + e));
+constexpr int p2_ilog2(int v) { return v <= 1 ? 0 : 1 + p2_ilog2(v >> 1); }
+
+// Pass plan of an M-point transform with E elements per thread: pass 0 has the remainder radix
+// R0 = M / E^(P-1) and no twiddles (NS = 1); passes 1..P-1 have radix E after NS_i = R0 E^(i-1)
+// points.  Putting the small radix first keeps the twiddle tables small: pass i needs
+// W_{NS_i E}^{k j} for k < NS_i and j in {1, 2, 4, 8} (the other powers are products), held in
+// shared memory for the whole persistent CTA.
+template <int M, int E>
+struct P2Plan {
+    static constexpr int LOGE = p2_ilog2(E);
+    static constexpr int P = (p2_ilog2(M) + LOGE - 1) / LOGE;
+    static constexpr int R0 = M >> (LOGE * (P - 1));
+    static constexpr int NW = E == 16 ? 4 : (E == 8 ? 3 : (E == 4 ? 2 : 1));  // tabled powers
+    static constexpr int ns(int i) { return i == 0 ? 1 : R0 * (i == 1 ? 1 : E * (ns(i - 1) / R0)); }
+    static constexpr int off(int i) { return i <= 1 ? 0 : off(i - 1) + NW * ns(i - 1); }
+    static constexpr int TW = P > 1 ? off(P - 1) + NW * ns(P - 1) : 0;  // table entries
+};
+
+// tws[off(i) + jj NS_i + k] = W_M^{2^jj k M / (NS_i E)} (sign -1), from the global W_M table
+template <int M, int E>
+__device__ __forceinline__ void p2_twsm_build(double2* tws, const double2* __restrict__ tw) {
+    using PL = P2Plan<M, E>;
+    constexpr int T = M / E;
+    for (int i = 1; i < PL::P; ++i) {
+        const int ns = PL::ns(i), o = PL::off(i), stride = M / (ns * E);
+        for (int x = threadIdx.x; x < PL::NW * ns; x += T) {
+            const int jj = x / ns, k = x - jj * ns;
+            tws[o + x] = tw[(1 << jj) * k * stride];
+        }
+    }
+}
+
+// u[r] *= W_{NS R}^{r k} with R = E: powers 1, 2, 4, 8 from the table, the rest as products
+// (depth <= 3)
+template <int R, int S, int NS>
+__device__ __forceinline__ void p2_twiddle(double2 (&u)[R], int k, const double2* tws) {
+    auto ld = [&](int jj) {
+        double2 w = tws[jj * NS + k];
         if (S > 0) w.y = -w.y;
         return w;
     };
     if constexpr (R == 2) {
-        u[1] = cmul(u[1], ld(e0));
+        u[1] = cmul(u[1], ld(0));
     } else if constexpr (R == 4) {
-        const double2 w1 = ld(e0), w2 = ld(2 * e0);
+        const double2 w1 = ld(0), w2 = ld(1);
         u[1] = cmul(u[1], w1);
         u[2] = cmul(u[2], w2);
         u[3] = cmul(u[3], cmul(w1, w2));
     } else if constexpr (R == 8) {
-        const double2 w1 = ld(e0), w2 = ld(2 * e0), w4 = ld(4 * e0);
+        const double2 w1 = ld(0), w2 = ld(1), w4 = ld(2);
         const double2 w3 = cmul(w1, w2);
         u[1] = cmul(u[1], w1);
         u[2] = cmul(u[2], w2);
@@ -394,8 +424,8 @@ __device__ __forceinline__ void p2_twiddle(double2 (&u)[R], int e0, const double
         u[5] = cmul(u[5], cmul(w1, w4));
         u[6] = cmul(u[6], cmul(w2, w4));
         u[7] = cmul(u[7], cmul(w3, w4));
-    } else {  // R == 16: powers from 4 table entries, product depth <= 3
-        const double2 w1 = ld(e0), w2 = ld(2 * e0), w4 = ld(4 * e0), w8 = ld(8 * e0);
+    } else {
+        const double2 w1 = ld(0), w2 = ld(1), w4 = ld(2), w8 = ld(3);
         const double2 w3 = cmul(w1, w2), w5 = cmul(w1, w4), w6 = cmul(w2, w4), w7 = cmul(w3, w4);
         u[1] = cmul(u[1], w1);
         u[2] = cmul(u[2], w2);
@@ -415,19 +445,17 @@ __device__ __forceinline__ void p2_twiddle(double2 (&u)[R], int e0, const double
     }
 }
 
-// Padded position of output r of a butterfly whose output 0 sits at `base`:
-// p2pad(base + r NS) = p2pad(base) + p2off<NS>(r) for every (E, NS) the engine uses (NS = 1 with
-// base a multiple of 8, NS = 8 with base % 16 < 8, NS a multiple of 16), so the compiler sees
-// immediate offsets instead of one live address per element.
+// Padded position of output r of a butterfly whose output 0 sits at `base` (base % 16 < NS
+// when NS < 16): p2pad(base + r NS) = p2pad(base) + p2off<NS>(r), an immediate offset.
 template <int NS>
 __device__ __forceinline__ constexpr int p2off(int r) {
-    return r * NS + (NS >= 16 ? r * (NS / 16) : (NS == 8 ? r / 2 : 0));
+    return r * NS + ((r * NS) >> 4);
 }
 
 // One Stockham pass of radix R after NS points have been combined (butterfly b: inputs
 // b + r M/R, outputs (b/NS) NS R + b%NS + r NS).
 template <int M, int E, int R, int NS, bool LAST, int S>
-__device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const double2* __restrict__ tw) {
+__device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const double2* tws) {
     constexpr int T = M / E;
     constexpr int Q = E / R;
     static_assert(T % 16 == 0, "padded exchange needs T % 16 == 0");
@@ -439,7 +467,7 @@ __device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const doub
 #pragma unroll
         for (int r = 0; r < R; ++r) u[r] = v[q + r * Q];
         const int b = t + q * T;
-        if constexpr (NS > 1) p2_twiddle<R, S>(u, (b & (NS - 1)) * (M / (NS * R)), tw);
+        if constexpr (NS > 1) p2_twiddle<R, S, NS>(u, b & (NS - 1), tws);
         dft_pow2<R, S>(u);
         if constexpr (LAST) {
 #pragma unroll
@@ -459,15 +487,16 @@ __device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const doub
     }
 }
 
-template <int M, int E, int S, int NS = 1>
-__device__ __forceinline__ void p2_fft(double2 (&v)[E], double2* sm, const double2* __restrict__ tw) {
-    constexpr int REM = M / NS;
-    if constexpr (REM <= E) {
-        p2_pass<M, E, REM, NS, true, S>(v, sm, tw);
+template <int M, int E, int S, int I = 0>
+__device__ __forceinline__ void p2_fft(double2 (&v)[E], double2* sm, const double2* tws) {
+    using PL = P2Plan<M, E>;
+    constexpr bool LAST = I == PL::P - 1;
+    if constexpr (I == 0) {
+        p2_pass<M, E, PL::R0, 1, LAST, S>(v, sm, tws);
     } else {
-        p2_pass<M, E, E, NS, false, S>(v, sm, tw);
-        p2_fft<M, E, S, NS * E>(v, sm, tw);
+        p2_pass<M, E, E, PL::ns(I), LAST, S>(v, sm, tws + PL::off(I));
     }
+    if constexpr (!LAST) p2_fft<M, E, S, I + 1>(v, sm, tws);
 }
 
 }  // namespace
@@ -515,9 +544,11 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
     extern __shared__ __align__(16) double2 smem[];
     __shared__ int s_ri;
     double2* buf = smem;                        // p2pad(M) + 1 (H_N of direct rings)
-    double2* phlo = smem + p2pad(M) + 16;       // 64 + (mmax >> 6) + 1 phase factors
+    double2* tws = smem + p2pad(M) + 16;        // pass twiddles (P2Plan<M, E>::TW)
+    double2* phlo = tws + P2Plan<M, E>::TW;     // 64 + (mmax >> 6) + 1 phase factors
     const int t = threadIdx.x, mmax = a.mmax;
     const PhaseTab ph{phlo, phlo + 64};
+    p2_twsm_build<M, E>(tws, a.p2_tw);
     p2_prefetch_ring<M, T, true>(a, blockIdx.x);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -628,9 +659,9 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
         }
         __syncthreads();  // H is read before the first pass overwrites buf
         if constexpr (!BLUE) {
-            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+            p2_fft<M, E, +1>(v, buf, tws);
         } else {
-            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+            p2_fft<M, E, -1>(v, buf, tws);
             // fences keep ptxas from hoisting the table loads into the FFT passes
             __threadfence_block();
             {
@@ -638,7 +669,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], cconj(__ldg(&H[t + T * j])));
             }
-            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+            p2_fft<M, E, +1>(v, buf, tws);
             __threadfence_block();
             const RingDesc& d = desc_at(a, ri);
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
@@ -686,9 +717,11 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
     extern __shared__ __align__(16) double2 smem[];
     __shared__ int s_ri;
     double2* buf = smem;
-    double2* phlo = smem + p2pad(M) + 16;
+    double2* tws = smem + p2pad(M) + 16;
+    double2* phlo = tws + P2Plan<M, E>::TW;
     const int t = threadIdx.x, mmax = a.mmax;
     const PhaseTab ph{phlo, phlo + 64};
+    p2_twsm_build<M, E>(tws, a.p2_tw);
     p2_prefetch_ring<M, T, false>(a, blockIdx.x);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
@@ -731,16 +764,16 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
             }
         }
         if constexpr (!BLUE) {
-            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+            p2_fft<M, E, -1>(v, buf, tws);
         } else {
-            p2_fft<M, E, -1>(v, buf, a.p2_tw);
+            p2_fft<M, E, -1>(v, buf, tws);
             __threadfence_block();
             {
                 const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], __ldg(&H[t + T * j]));
             }
-            p2_fft<M, E, +1>(v, buf, a.p2_tw);
+            p2_fft<M, E, +1>(v, buf, tws);
             __threadfence_block();
             const RingDesc& d = desc_at(a, ri);
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
@@ -820,8 +853,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
     constexpr int MH = FFT_P2C_B / 2, E = 16, T = MH / E, G = 8;
     extern __shared__ __align__(16) double2 smem[];
     double2* buf = smem;
-    double2* phlo = smem + p2pad(MH) + 16;
+    double2* tws = smem + p2pad(MH) + 16;
+    double2* phlo = tws + P2Plan<MH, E>::TW;
     cg::cluster_group cluster = cg::this_cluster();
+    p2_twsm_build<MH, E>(tws, a.p2_tw);
     const int h = (int)cluster.block_rank();
     const int t = threadIdx.x, mmax = a.mmax;
     const int cl = blockIdx.x >> 1, ncl = gridDim.x >> 1;
@@ -897,7 +932,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], __ldg(&twm[t + T * j]));
             }
         }
-        p2_fft<MH, E, -1>(v, buf, a.p2_tw);
+        p2_fft<MH, E, -1>(v, buf, tws);
         __threadfence_block();
         {
             const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
@@ -907,7 +942,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                 v[j] = cmul(v[j], SYN ? cconj(hv) : hv);
             }
         }
-        p2_fft<MH, E, +1>(v, buf, a.p2_tw);
+        p2_fft<MH, E, +1>(v, buf, tws);
         if (h == 1) {
             const double2* __restrict__ twm = a.tabs + desc_at(a, ri).tw_off;
 #pragma unroll
@@ -995,6 +1030,8 @@ __global__ void __launch_bounds__(512, 1) p2c_h_kernel(const RingDesc* __restric
         if (i > M - N) return cconj(chirp[M - i]);
         return make_double2(0.0, 0.0);
     };
+    double2* tws = smem + p2pad(MH) + 16;
+    p2_twsm_build<MH, E>(tws, tw_half);
     double2 v[E];
 #pragma unroll
     for (int j = 0; j < E; ++j) {
@@ -1002,7 +1039,8 @@ __global__ void __launch_bounds__(512, 1) p2c_h_kernel(const RingDesc* __restric
         const double2 lo = hval(b), hi = hval(b + MH);
         v[j] = h == 0 ? cadd(lo, hi) : cmul(csub(lo, hi), twm[b]);
     }
-    p2_fft<MH, E, -1>(v, smem, tw_half);
+    __syncthreads();
+    p2_fft<MH, E, -1>(v, smem, tws);
 #pragma unroll
     for (int j = 0; j < E; ++j) tabs[d.h_off + 2 * (t + T * j) + h] = v[j];
 }
@@ -1282,9 +1320,10 @@ void blue_c(const RingDesc* descs, int n, double2* tabs, cudaStream_t s) {
 #ifndef P2B_MB_2048
 #define P2B_MB_2048 4
 #endif
-template <int M>
+template <int M, int E>
 size_t p2_smem(int mmax) {
-    return (size_t)(M + (M >> 4) + 16) * sizeof(double2) + (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
+    return (size_t)(M + (M >> 4) + 16 + P2Plan<M, E>::TW) * sizeof(double2) +
+           (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
 }
 // persistent grid: every resident CTA slot of the device (at most one per ring)
 template <class K>
@@ -1300,22 +1339,22 @@ template <int M, int E, int MINB, bool BLUE>
 void p2_synth(const RingStageArgs& a, cudaStream_t s) {
     static bool once = (cudaFuncSetAttribute(ring_p2_synth_kernel<M, E, MINB, BLUE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)p2_smem<M>(kMaxPhaseM)),
+                                             (int)p2_smem<M, E>(kMaxPhaseM)),
                         true);
     (void)once;
     auto k = ring_p2_synth_kernel<M, E, MINB, BLUE>;
-    const size_t sm = p2_smem<M>(a.mmax);
+    const size_t sm = p2_smem<M, E>(a.mmax);
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
 }
 template <int M, int E, int MINB, bool BLUE>
 void p2_anal(const RingStageArgs& a, cudaStream_t s) {
     static bool once = (cudaFuncSetAttribute(ring_p2_anal_kernel<M, E, MINB, BLUE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)p2_smem<M>(kMaxPhaseM)),
+                                             (int)p2_smem<M, E>(kMaxPhaseM)),
                         true);
     (void)once;
     auto k = ring_p2_anal_kernel<M, E, MINB, BLUE>;
-    const size_t sm = p2_smem<M>(a.mmax);
+    const size_t sm = p2_smem<M, E>(a.mmax);
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
 }
 // class -> (M, E, resident CTAs per SM, Bluestein)
@@ -1347,7 +1386,7 @@ void p2_dispatch(int cls, const RingStageArgs& a, cudaStream_t s) {
 
 namespace {
 size_t p2c_smem(int mmax) {
-    return (size_t)(FFT_P2C_B / 2 + FFT_P2C_B / 32 + 16) * sizeof(double2) +
+    return (size_t)(FFT_P2C_B / 2 + FFT_P2C_B / 32 + 16 + P2Plan<FFT_P2C_B / 2, 16>::TW) * sizeof(double2) +
            (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
 }
 template <bool SYN>

@@ -33,8 +33,10 @@ METRICS = [
 
 def short(name):
     name = name.replace("shtk::", "")
-    name = name.split("(")[0]
-    return name.replace("void ", "").split("<")[0]
+    name = name.split("(")[0].replace("void ", "")
+    if name.startswith("ring_p2"):  # size classes share a kernel name: keep <M, E, MINB, BLUE>
+        return name.replace(" ", "")
+    return name.split("<")[0]
 
 
 def raw_rows(rep):
