@@ -54,10 +54,12 @@ typedef enum {
 /* Per-call timing, CUDA events on the context stream (ms), plus side channels that the
  * reference keeps in TransformOptions::step_counter / Profiler (perfmodel.hpp:63-84). */
 typedef struct {
-    double legendre_ms;     /* Legendre stage kernel time */
-    double fft_ms;          /* fold + ring FFT + unfold kernel time */
-    double h2d_ms;          /* host->device copies (host-buffer entry points only) */
-    double d2h_ms;          /* device->host copies (host-buffer entry points only) */
+    double legendre_ms;     /* Legendre stage kernel time (host-buffer paths: sum over the
+                               pipelined launches, which overlap each other and the copies) */
+    double fft_ms;          /* fold + ring FFT + unfold kernel time (same convention) */
+    double h2d_ms;          /* host->device copy span (host-buffer entry points only) */
+    double d2h_ms;          /* device->host copies from the first copy's start to the end of
+                               the call (host-buffer entry points only) */
     double total_ms;        /* whole call on the stream */
     uint64_t nominal_steps; /* reference step count: sum over streams of lmax-m+1 */
     uint64_t executed_steps;/* (l, m, stream) steps the kernels actually ran */

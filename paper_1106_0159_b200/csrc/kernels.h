@@ -96,15 +96,20 @@ __host__ __device__ inline int leg_tile_start(int is) { return is >= 2 ? (is & ~
 // phases: bit0 = zero pass (dead tiles / orders without alive tiles), bit1 = the persistent
 // kernel over p's item list (callers may pass a view restricted to one chunk of items).
 // bit2 (map2alm) = keep the per-order completion counters of an earlier launch (the order's
-// work items are split over several launches; only the first one resets them).
-constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3, LEG_PHASE_KEEP_DONE = 4;
+// work items are split over several launches; only the first one resets them).  bit3 = the
+// caller has zeroed the queue counter (and m_done): concurrent launches on different streams
+// each get their own queue word.
+constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3, LEG_PHASE_KEEP_DONE = 4,
+              LEG_PHASE_NO_RESET = 8;
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
                         const int64_t* row_off, int* counters, cudaStream_t s,
                         int phases = LEG_PHASE_ALL);
 // a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.  scratch: m2a_scratch_elems.
+// counters[0] is the work queue; the per-order completion counters are m_done (n_m ints,
+// default counters + 1).
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s, int phases = LEG_PHASE_ALL);
+                        cudaStream_t s, int phases = LEG_PHASE_ALL, int* m_done = nullptr);
 int leg_persistent_blocks(int device);
 
 // ---------------------------------------------------------------------------------------

@@ -494,7 +494,7 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
     int blocks = leg_persistent_blocks(dev);
     const int need = (p.n_a2m_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
-    cudaMemsetAsync(counters, 0, sizeof(int), s);
+    if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
     leg_alm2map_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, alm, delta, row_off, counters);
 }
 
@@ -578,15 +578,15 @@ template <int R>
 __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, double2* __restrict__ alm,
-                       int accumulate, int* __restrict__ counters, double2* __restrict__ scratch) {
+                       int accumulate, int* __restrict__ queue, int* __restrict__ m_done,
+                       double2* __restrict__ scratch) {
     static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
     __shared__ M2AWarpSmem<R> sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     M2AWarpSmem<R>& sm = sm_all[warp];
-    int* m_done = counters + 1;
 
     for (;;) {
-        const int it = warp_next_item(counters);
+        const int it = warp_next_item(queue);
         if (it >= p.n_m2a_items) return;
         const LegItem item = p.m2a_items[it];
         const int mi = item.mi;
@@ -742,7 +742,7 @@ __global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm)
 
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s, int phases) {
+                        cudaStream_t s, int phases, int* m_done) {
     if (p.n_m == 0) return;
     if (!accumulate && (phases & LEG_PHASE_ZERO)) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
     if (!(phases & LEG_PHASE_MAIN) || p.n_m2a_items == 0) return;
@@ -754,9 +754,13 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
     int blocks = sms * (per > 0 ? per : 1);
     const int need = (p.n_m2a_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
-    cudaMemsetAsync(counters, 0, sizeof(int) * ((phases & LEG_PHASE_KEEP_DONE) ? 1 : 1 + p.n_m), s);
+    if (!m_done) m_done = counters + 1;
+    if (!(phases & LEG_PHASE_NO_RESET)) {
+        cudaMemsetAsync(counters, 0, sizeof(int), s);
+        if (!(phases & LEG_PHASE_KEEP_DONE)) cudaMemsetAsync(m_done, 0, sizeof(int) * p.n_m, s);
+    }
     leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, alm, accumulate,
-                                                                counters, scratch);
+                                                                counters, m_done, scratch);
 }
 
 }  // namespace shtk

@@ -12,11 +12,13 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
 #include <numeric>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "../../include/shtc.h"
@@ -106,24 +108,37 @@ struct LegPlan {
         tile_cnt, a2m_items, m2a_items, m2a_per_m, m2a_slot, m2a_scratch, counters, ck_q, ck_act,
         a2m_items_band, m2a_items_band, m2a_per_m_band, m2a_slot_band;
     uint64_t prefix_steps = 0, checked_steps = 0, fast_steps = 0;
-    // Pipelined host-buffer paths (see shtc_alm2map): latitude-band chunks of tiles, numbered
-    // from the equator.  alm2map launches: band tc's items (band 0 also split by order chunk
-    // mc so it can start while a_lm is still arriving); map2alm: band tc's items, after which
-    // the orders whose last item was in band tc are final (runs of order indices).
+    // Pipelined host-buffer paths (see shtc_alm2map): latitude bands of tiles, numbered from
+    // the equator.  alm2map launches: band tc's items (band 0 also split by order chunk mc so
+    // it can start while a_lm is still arriving); map2alm launches: band tc's items (the last
+    // band also split by order chunk so the a_lm copies start before it ends); after map2alm
+    // launch j the orders whose last item was in launch j are final (runs of order indices).
     struct PipeLaunch {
         int tc, mc, begin, end;
     };
     std::vector<int> chunk_mi;  // order chunk k = order indices [chunk_mi[k], chunk_mi[k+1])
     std::vector<PipeLaunch> a2m_launch;  // ranges of the band-ordered item lists
+    std::vector<PipeLaunch> m2a_launch;
     LegPlanView band_view{};             // view with the band-ordered item lists
-    std::vector<int> m2a_off;   // band tc = m2a items [m2a_off[tc], m2a_off[tc+1])
-    std::vector<std::vector<std::pair<int, int>>> m2a_done;  // per band: final order-index runs
+    std::vector<std::vector<std::pair<int, int>>> m2a_done;  // per m2a launch: final order runs
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
     double build_ms = 0.0;
 };
 
-constexpr int kPipeChunks = 4;  // chunks of the pipelined host-buffer entry points
+// pipelined host-buffer entry points: latitude bands (ring stage + Legendre units, pixel
+// copies) and order chunks (a_lm copies)
+constexpr int kMaxPipeBands = 16;
+// SHTC_PIPE_BANDS overrides the band count (experiments)
+int pipe_bands() {
+    static const int b = std::getenv("SHTC_PIPE_BANDS")
+                             ? std::min(kMaxPipeBands, std::max(1, std::atoi(std::getenv("SHTC_PIPE_BANDS"))))
+                             : 8;
+    return b;
+}
+#define kPipeBands pipe_bands()
+constexpr int kOrderChunks = 4;
+constexpr int kPipeEvents = 128;
 
 struct FftPlan {
     bool built = false;
@@ -180,13 +195,14 @@ struct shtc_ctx {
     // scratch
     DevBuf delta, alm_buf, map_buf, stats;
     cudaEvent_t ev[8] = {};
-    // pipelined host-buffer paths
-    cudaStream_t h2d = nullptr, d2h = nullptr;
-    cudaEvent_t pev[3][kPipeChunks] = {};  // ordering events of the copy streams
+    // pipelined host-buffer paths: copy streams, two Legendre streams (consecutive launches
+    // alternate so one launch's tail overlaps the next) and a high-priority ring-stage stream
+    cudaStream_t h2d = nullptr, d2h = nullptr, lst[2] = {}, fst = nullptr;
+    cudaEvent_t pev[kPipeEvents] = {};  // ordering events
+    cudaEvent_t tev[kPipeEvents] = {};  // timing events
     // ring stage: the small-ring classes run on side streams beside the large ones
     cudaStream_t fft_aux[2] = {};
     cudaEvent_t fft_fork = nullptr, fft_join[2] = {};
-    cudaEvent_t tev[3][kPipeChunks] = {};  // timing events of the pipelined segments
 };
 
 namespace {
@@ -279,8 +295,8 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     std::vector<int> band(nt);
     int64_t acc = 0;
     for (int t = 0; t < nt; ++t) {
-        const int polar = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
-        band[t] = kPipeChunks - 1 - polar;
+        const int polar = (int)std::min<int64_t>(kPipeBands - 1, acc * kPipeBands / std::max<int64_t>(total, 1));
+        band[t] = kPipeBands - 1 - polar;
         acc += pix[t];
     }
     return band;
@@ -296,6 +312,12 @@ std::vector<int> ring_bands(const shtc_ctx* c, std::vector<Stream> st) {
         if (st[i].south >= 0) rb[st[i].south] = tb[i / LEG_TILE];
     }
     return rb;
+}
+
+// tiles per map2alm item of the pipelined (band) item set; SHTC_M2A_BAND_GROUP overrides
+int m2a_band_group() {
+    static const int g = std::getenv("SHTC_M2A_BAND_GROUP") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_BAND_GROUP"))) : 1;
+    return g;
 }
 
 void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vector<int>& ms,
@@ -411,19 +433,26 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         std::reverse(alive.begin(), alive.end());
         tl.insert(tl.end(), alive.begin(), alive.end());
         tcnt[i] = (int)alive.size();
-        // map2alm items: up to LEG_M2A_GROUP consecutive alive tiles (both sets share the
-        // grouping, so the summation order and the results are identical)
-        per_m[i] = 0;
-        for (size_t a = 0; a < alive.size(); a += LEG_M2A_GROUP)
-            m2a.push_back(LegItem{i, toffs[i] + (int)a, (int)std::min<size_t>(LEG_M2A_GROUP, alive.size() - a),
-                                  per_m[i]++});
+        // map2alm items: up to G consecutive alive tiles.  Device-resident set: G =
+        // LEG_M2A_GROUP (fewer partial slots; one launch, so long items only delay its start).
+        // Band set: G = m2a_band_group tiles of one pipeline band, so no item outlasts the
+        // band's launch.  The two sets sum in different groupings (both deterministic).
+        auto group = [&](int G, bool by_band, std::vector<LegItem>& out, int& cnt) {
+            cnt = 0;
+            for (size_t a = 0; a < alive.size();) {
+                size_t e = a + 1;
+                while (e < alive.size() && e - a < (size_t)G && (!by_band || tband[alive[e]] == tband[alive[a]])) ++e;
+                out.push_back(LegItem{i, toffs[i] + (int)a, (int)(e - a), cnt++});
+                a = e;
+            }
+        };
+        group(LEG_M2A_GROUP, false, m2a, per_m[i]);
+        group(m2a_band_group(), true, m2a_b, per_m_b[i]);
         slot[i] = slots;
         slots += (int64_t)per_m[i] * (n + 1);
+        slot_b[i] = slots_b;
+        slots_b += (int64_t)per_m_b[i] * (n + 1);
     }
-    m2a_b = m2a;
-    per_m_b = per_m;
-    slot_b = slot;
-    slots_b = slots;
     // cost = degree steps actually run (from the tile's resume point)
     auto tile_cost = [&](int mi, int t) {
         return (int64_t)(lmax - ms[mi] + 1 - leg_tile_start(info[(size_t)mi * v.n_tiles + t].x));
@@ -441,12 +470,12 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         int64_t total = 0, acc = 0;
         for (int i = 0; i < n_m; ++i) total += lmax - ms[i] + 1;
         for (int i = 0; i < n_m; ++i) {
-            const int k = (int)std::min<int64_t>(kPipeChunks - 1, acc * kPipeChunks / std::max<int64_t>(total, 1));
+            const int k = (int)std::min<int64_t>(kOrderChunks - 1, acc * kOrderChunks / std::max<int64_t>(total, 1));
             while ((int)P.chunk_mi.size() <= k) P.chunk_mi.push_back(i);
             chunk_of[i] = k;
             acc += lmax - ms[i] + 1;
         }
-        while ((int)P.chunk_mi.size() <= kPipeChunks) P.chunk_mi.push_back(n_m);
+        while ((int)P.chunk_mi.size() <= kOrderChunks) P.chunk_mi.push_back(n_m);
     }
     std::stable_sort(a2m.begin(), a2m.end(),
                      [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
@@ -469,24 +498,29 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         P.a2m_launch.push_back({a2m_key(a2m_b[k]).first, a2m_key(a2m_b[k]).second, (int)k, (int)e});
         k = e;
     }
-    // map2alm band set: an item runs with the last band of its tiles (bands ascend along the
-    // tile list, so every tile's Delta rows are ready), then cost; an order is final after
-    // the band of its last item
-    auto m2a_band = [&](const LegItem& it) { return tband[tl[it.a + it.b - 1]]; };
+    // map2alm band set: an item runs with the band of its tiles (groups do not cross bands),
+    // the last band also split by order chunk, then cost; an order is final after the launch
+    // of its last item
+    auto m2a_key = [&](const LegItem& it) {
+        const int tc = tband[tl[it.a + it.b - 1]];
+        return std::make_pair(tc, tc == kPipeBands - 1 ? chunk_of[it.mi] : 0);
+    };
     std::stable_sort(m2a_b.begin(), m2a_b.end(), [&](const LegItem& a, const LegItem& b) {
-        if (m2a_band(a) != m2a_band(b)) return m2a_band(a) < m2a_band(b);
+        if (m2a_key(a) != m2a_key(b)) return m2a_key(a) < m2a_key(b);
         return m2a_cost(a) > m2a_cost(b);
     });
-    P.m2a_off.assign(kPipeChunks + 1, 0);
-    std::vector<int> last_band(n_m, 0);  // orders without items are final from the start
-    for (const auto& it : m2a_b) {
-        P.m2a_off[m2a_band(it) + 1]++;
-        last_band[it.mi] = std::max(last_band[it.mi], m2a_band(it));
+    P.m2a_launch.clear();
+    std::vector<int> last_launch(n_m, 0);  // orders without items are final from the start
+    for (size_t k = 0; k < m2a_b.size();) {
+        size_t e = k;
+        while (e < m2a_b.size() && m2a_key(m2a_b[e]) == m2a_key(m2a_b[k])) ++e;
+        for (size_t q = k; q < e; ++q) last_launch[m2a_b[q].mi] = (int)P.m2a_launch.size();
+        P.m2a_launch.push_back({m2a_key(m2a_b[k]).first, m2a_key(m2a_b[k]).second, (int)k, (int)e});
+        k = e;
     }
-    for (int k = 0; k < kPipeChunks; ++k) P.m2a_off[k + 1] += P.m2a_off[k];
-    P.m2a_done.assign(kPipeChunks, {});
+    P.m2a_done.assign(std::max<size_t>(1, P.m2a_launch.size()), {});
     for (int i = 0; i < n_m; ++i) {
-        auto& runs = P.m2a_done[last_band[i]];
+        auto& runs = P.m2a_done[last_launch[i]];
         if (!runs.empty() && runs.back().second == i) runs.back().second = i + 1;
         else runs.push_back({i, i + 1});
     }
@@ -503,7 +537,9 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.m2a_per_m_band.upload(per_m_b, s);
     P.m2a_slot_band.upload(slot_b, s);
     P.m2a_scratch.ensure((size_t)std::max<int64_t>(std::max(slots, slots_b), 1) * sizeof(double2));
-    P.counters.ensure((size_t)(1 + n_m) * sizeof(int));
+    // [0]: queue of single launches, [1, 1 + n_m): per-order completion, then one queue word
+    // per pipelined launch
+    P.counters.ensure((size_t)(1 + n_m + P.a2m_launch.size() + P.m2a_launch.size()) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
     v.tile_list_cnt = P.tile_cnt.as<int>();
@@ -655,7 +691,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         auto band = [&](const RingDesc& d) {
             return ring_band.empty() ? 0 : std::max(0, ring_band[rings[d.ring_pos]]);
         };
-        F.band_pix.assign(kPipeChunks, {});
+        F.band_pix.assign(kPipeBands, {});
         for (size_t pos = 0; pos < rings.size(); ++pos) {
             const int r = rings[pos];
             const int k = ring_band.empty() ? 0 : std::max(0, ring_band[r]);
@@ -668,9 +704,9 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
             std::stable_sort(per_class[cls].begin(), per_class[cls].end(),
                              [&](const RingDesc& a, const RingDesc& b) { return band(a) < band(b); });
             F.descs[cls].upload(per_class[cls], s);
-            F.range_start[cls].assign(kPipeChunks + 1, 0);
+            F.range_start[cls].assign(kPipeBands + 1, 0);
             for (const RingDesc& d : per_class[cls]) F.range_start[cls][band(d) + 1]++;
-            for (int k = 0; k < kPipeChunks; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
+            for (int k = 0; k < kPipeBands; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
         }
     }
     F.counters.ensure(FFT_N_CLASSES * sizeof(int));  // no allocation on the transform path
@@ -722,14 +758,13 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // the small-ring classes (latency bound: few CTAs, aliasing folds over many wraps) run on two
 // side streams at the same time, joined back before the stage ends.
 template <class Launch>
-void ring_stage(shtc_ctx* c, FftPlan& F, int range, Launch launch) {
+void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launch) {
     if (!c->fft_fork) {
         for (auto& st : c->fft_aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->fft_fork, cudaEventDisableTiming));
         for (auto& e : c->fft_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
     if (!F.counters.p) F.counters.ensure(FFT_N_CLASSES * sizeof(int));
-    cudaStream_t s = c->stream;
     CK(cudaMemsetAsync(F.counters.p, 0, FFT_N_CLASSES * sizeof(int), s));
     CK(cudaEventRecord(c->fft_fork, s));
     bool used[2] = {false, false};
@@ -765,8 +800,8 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, Launch launch) {
 }
 
 void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
-                    const int64_t* mb, const int64_t* mst, int range = -1) {
-    ring_stage(c, F, range, [&](int k, RingStageArgs& a, cudaStream_t st) {
+                    const int64_t* mb, const int64_t* mst, int range = -1, cudaStream_t s = nullptr) {
+    ring_stage(c, F, range, s ? s : c->stream, [&](int k, RingStageArgs& a, cudaStream_t st) {
         a.m_base = mb;
         a.m_stride = mst;
         a.delta_in = delta;
@@ -776,8 +811,9 @@ void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
 }
 
 void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
-                   const int64_t* mst, int range = -1, double2* const* col_ptr = nullptr) {
-    ring_stage(c, F, range, [&](int k, RingStageArgs& a, cudaStream_t st) {
+                   const int64_t* mst, int range = -1, double2* const* col_ptr = nullptr,
+                   cudaStream_t s = nullptr) {
+    ring_stage(c, F, range, s ? s : c->stream, [&](int k, RingStageArgs& a, cudaStream_t st) {
         a.m_base = mb;
         a.m_stride = mst;
         a.col_ptr = col_ptr;
@@ -892,12 +928,13 @@ void shtc_destroy(shtc_ctx* ctx) {
     cudaStreamSynchronize(ctx->stream);
     for (auto& e : ctx->ev)
         if (e) cudaEventDestroy(e);
-    for (auto& row : ctx->pev)
-        for (auto& e : row)
-            if (e) cudaEventDestroy(e);
-    for (auto& row : ctx->tev)
-        for (auto& e : row)
-            if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->pev)
+        if (e) cudaEventDestroy(e);
+    for (auto& e : ctx->tev)
+        if (e) cudaEventDestroy(e);
+    for (auto& st : ctx->lst)
+        if (st) cudaStreamDestroy(st);
+    if (ctx->fst) cudaStreamDestroy(ctx->fst);
     for (auto& st : ctx->fft_aux)
         if (st) cudaStreamDestroy(st);
     if (ctx->fft_fork) cudaEventDestroy(ctx->fft_fork);
@@ -1018,24 +1055,61 @@ shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_d
 }
 
 // Host-buffer entry points, pipelined over latitude bands (contiguous tile ranges of ~equal
-// pixel counts, see tile_bands) on three streams:
-//   alm2map: H2D of a_lm by order chunk || Legendre of band 0 by order chunk; then per band:
-//            Legendre (all orders, the band's rings) -> ring synthesis of the band's rings ->
-//            D2H of the band's pixels || the next band's Legendre
-//   map2alm: per band: H2D of the band's pixels || ring analysis + Legendre of the previous
-//            band; the orders whose last work item was in the band are final -> D2H of their
-//            a_lm || the next band
+// pixel counts, see tile_bands).  Streams: h2d / d2h copies, two Legendre streams that
+// consecutive launches alternate between (one launch's tail overlaps the next launch), and a
+// high-priority ring-stage stream whose blocks take the SMs the Legendre launches free.
+//   alm2map: H2D of a_lm by order chunk || Legendre of band 0 by order chunk, then the other
+//            bands' Legendre launches; ring synthesis of band k after band k's launches ->
+//            D2H of the band's pixels
+//   map2alm: H2D of band k's pixels -> ring analysis of band k -> band k's Legendre launches
+//            (the last band split by order chunk); after launch j (and j-1, the only launch
+//            that can still run beside it) the orders whose last item was in launch j are
+//            final -> D2H of their a_lm
 // Same kernels and arithmetic as the device-resident path (results are bit-identical).
 namespace {
 void ensure_pipe(shtc_ctx* c) {
     if (c->h2d) return;
+    int least = 0, greatest = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     CK(cudaStreamCreateWithFlags(&c->h2d, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
-    for (auto& row : c->pev)
-        for (auto& e : row) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& row : c->tev)
-        for (auto& e : row) CK(cudaEventCreate(&e));
+    for (auto& st : c->lst) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithPriority(&c->fst, cudaStreamNonBlocking, greatest));
+    for (auto& e : c->pev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : c->tev) CK(cudaEventCreate(&e));
 }
+
+// events of one pipelined call, handed out in order
+struct PipeEvents {
+    shtc_ctx* c;
+    int np = 0, nt = 0;
+    cudaEvent_t order(cudaStream_t st) {
+        if (np >= kPipeEvents) fail(SHTC_ECUDA, "pipeline event pool exhausted");
+        cudaEvent_t e = c->pev[np++];
+        CK(cudaEventRecord(e, st));
+        return e;
+    }
+    // (start, end) timing pair around enqueue(), recorded on st; returns the pair's index
+    int timed(cudaStream_t st, const std::function<void()>& enqueue) {
+        if (nt + 2 > kPipeEvents) fail(SHTC_ECUDA, "pipeline event pool exhausted");
+        const int i = nt;
+        CK(cudaEventRecord(c->tev[nt++], st));
+        enqueue();
+        CK(cudaEventRecord(c->tev[nt++], st));
+        return i;
+    }
+    float span(int i) const { return elapsed(c->tev[i], c->tev[i + 1]); }
+    // SHTC_PIPE_TRACE=1: every timed segment as (start, end) ms after the call's start event
+    void trace(const char* what, const std::vector<std::pair<const char*, int>>& segs) const {
+        static const bool on = std::getenv("SHTC_PIPE_TRACE") != nullptr;
+        if (!on) return;
+        std::fprintf(stderr, "[pipe %s]", what);
+        for (const auto& sg : segs)
+            std::fprintf(stderr, " %s %.3f-%.3f", sg.first, elapsed(c->ev[3], c->tev[sg.second]),
+                         elapsed(c->ev[3], c->tev[sg.second + 1]));
+        std::fprintf(stderr, " end %.3f\n", elapsed(c->ev[3], c->ev[6]));
+    }
+};
 
 // band-ordered items [begin, end) of one pipelined launch
 LegPlanView items_view(const LegPlan& P, int begin, int end, bool a2m) {
@@ -1059,12 +1133,22 @@ std::pair<size_t, size_t> alm_span(const shtc_ctx* c, int mi0, int mi1) {
     return {off(mi0), off(mi1)};
 }
 
-void band_timing(shtc_ctx* c, float& first, float& second) {
-    first = second = 0.f;
-    for (int k = 0; k < kPipeChunks; ++k) {
-        first += elapsed(c->tev[0][k], c->tev[1][k]);
-        second += elapsed(c->tev[1][k], c->tev[2][k]);
+// fork the pipeline streams off the caller's stream
+void pipe_fork(shtc_ctx* c) {
+    CK(cudaEventRecord(c->ev[3], c->stream));
+    for (cudaStream_t st : {c->h2d, c->d2h, c->lst[0], c->lst[1], c->fst})
+        CK(cudaStreamWaitEvent(st, c->ev[3], 0));
+}
+
+// join: every stream's work precedes the last D2H; the caller's stream continues after it
+void pipe_join(shtc_ctx* c) {
+    for (cudaStream_t st : {c->h2d, c->lst[0], c->lst[1], c->fst}) {
+        CK(cudaEventRecord(c->ev[5], st));
+        CK(cudaStreamWaitEvent(c->d2h, c->ev[5], 0));
     }
+    CK(cudaEventRecord(c->ev[6], c->d2h));
+    CK(cudaStreamWaitEvent(c->stream, c->ev[6], 0));
+    CK(cudaEventSynchronize(c->ev[6]));
 }
 }  // namespace
 
@@ -1081,53 +1165,81 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         ctx->alm_buf.ensure(na);
         ctx->map_buf.ensure(nb);
         ctx->delta.ensure((size_t)ctx->n_rings * (ctx->mmax + 1) * sizeof(double2));
-        cudaStream_t s = ctx->stream;
         LegPlan& P = ctx->leg;
         FftPlan& F = ctx->fft_id;
         double2* ab = ctx->alm_buf.as<double2>();
         double* mb = ctx->map_buf.as<double>();
-        CK(cudaEventRecord(ctx->ev[3], s));
-        CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
-        for (int k = 0; k < kPipeChunks; ++k) {
-            auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
-            if (e > b)
-                CK(cudaMemcpyAsync(ab + b, reinterpret_cast<const double2*>(alm) + b, (e - b) * sizeof(double2),
-                                   cudaMemcpyHostToDevice, ctx->h2d));
-            CK(cudaEventRecord(ctx->pev[0][k], ctx->h2d));
-        }
+        double2* dl = ctx->delta.as<double2>();
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
-        CK(cudaEventRecord(ctx->ev[0], s));
-        launch_leg_alm2map(P.view, ab, ctx->delta.as<double2>(), ro, P.counters.as<int>(), s, LEG_PHASE_ZERO);
-        size_t li = 0;
-        for (int tc = 0; tc < kPipeChunks; ++tc) {
-            CK(cudaEventRecord(ctx->tev[0][tc], s));
-            if (tc == 1) CK(cudaStreamWaitEvent(s, ctx->pev[0][kPipeChunks - 1], 0));
-            for (; li < P.a2m_launch.size() && P.a2m_launch[li].tc == tc; ++li) {
-                const auto& L = P.a2m_launch[li];
-                if (tc == 0) CK(cudaStreamWaitEvent(s, ctx->pev[0][L.mc], 0));
-                launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, ctx->delta.as<double2>(), ro,
-                                   P.counters.as<int>(), s, LEG_PHASE_MAIN);
-                CK(cudaGetLastError());
+        const int n_m = (int)ctx->ms.size();
+        int* queues = P.counters.as<int>() + 1 + n_m;  // one word per launch
+        PipeEvents E{ctx};
+        if (!P.a2m_launch.empty())
+            CK(cudaMemsetAsync(queues, 0, P.a2m_launch.size() * sizeof(int), ctx->stream));
+        pipe_fork(ctx);
+        // a_lm by order chunk
+        cudaEvent_t h_chunk[kOrderChunks];
+        const int th = E.timed(ctx->h2d, [&] {
+            for (int k = 0; k < kOrderChunks; ++k) {
+                auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
+                if (e > b)
+                    CK(cudaMemcpyAsync(ab + b, reinterpret_cast<const double2*>(alm) + b,
+                                       (e - b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->h2d));
+                h_chunk[k] = E.order(ctx->h2d);
             }
-            if (tc == 0) CK(cudaStreamWaitEvent(s, ctx->pev[0][kPipeChunks - 1], 0));
-            CK(cudaEventRecord(ctx->tev[1][tc], s));
-            run_ring_synth(ctx, F, ctx->delta.as<double2>(), mb, nullptr, nullptr, tc);
-            CK(cudaEventRecord(ctx->tev[2][tc], s));
-            CK(cudaEventRecord(ctx->pev[1][tc], s));
-            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][tc], 0));
-            for (const auto& iv : F.band_pix[tc])
-                CK(cudaMemcpyAsync(map + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
-                                   cudaMemcpyDeviceToHost, ctx->d2h));
+        });
+        // dead tiles' Delta rows (disjoint from every launch's rows) ahead of the ring stage
+        launch_leg_alm2map(P.view, ab, dl, ro, P.counters.as<int>(), ctx->fst, LEG_PHASE_ZERO);
+        CK(cudaGetLastError());
+        // SHTC_PIPE_MODE (experiments): 0 = Legendre launches run ahead freely on two streams;
+        // 1 = a band's launches wait for the ring synthesis two bands back (the Legendre stage
+        // runs at most one band ahead, so the ring stage gets whole SMs at launch tails);
+        // 2 = everything on one stream, band by band
+        static const int mode = std::getenv("SHTC_PIPE_MODE") ? std::atoi(std::getenv("SHTC_PIPE_MODE")) : 2;
+        std::vector<int> t_leg, t_fft;
+        std::vector<std::pair<const char*, int>> segs;
+        std::vector<cudaEvent_t> synth_done(kPipeBands, nullptr);
+        int t_d2h_first = -1;
+        size_t j = 0;
+        for (int tc = 0; tc < kPipeBands; ++tc) {
+            std::vector<cudaEvent_t> band_done;
+            for (; j < P.a2m_launch.size() && P.a2m_launch[j].tc == tc; ++j) {
+                const auto& L = P.a2m_launch[j];
+                cudaStream_t st = mode == 2 ? ctx->fst : ctx->lst[j & 1];
+                CK(cudaStreamWaitEvent(st, h_chunk[L.tc == 0 ? L.mc : kOrderChunks - 1], 0));
+                if (mode == 1 && tc >= 2 && synth_done[tc - 2]) CK(cudaStreamWaitEvent(st, synth_done[tc - 2], 0));
+                t_leg.push_back(E.timed(st, [&] {
+                    launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, dl, ro, queues + j, st,
+                                       LEG_PHASE_MAIN | LEG_PHASE_NO_RESET);
+                    CK(cudaGetLastError());
+                }));
+                if (st != ctx->fst) band_done.push_back(E.order(st));
+            }
+            if (F.band_pix[tc].empty() && band_done.empty()) continue;
+            for (cudaEvent_t e : band_done) CK(cudaStreamWaitEvent(ctx->fst, e, 0));
+            t_fft.push_back(E.timed(ctx->fst, [&] { run_ring_synth(ctx, F, dl, mb, nullptr, nullptr, tc, ctx->fst); }));
+            synth_done[tc] = E.order(ctx->fst);
+            CK(cudaStreamWaitEvent(ctx->d2h, synth_done[tc], 0));
+            const int ti = E.timed(ctx->d2h, [&] {
+                for (const auto& iv : F.band_pix[tc])
+                    CK(cudaMemcpyAsync(map + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
+                                       cudaMemcpyDeviceToHost, ctx->d2h));
+            });
+            if (t_d2h_first < 0) t_d2h_first = ti;
+            segs.push_back({"D", ti});
         }
-        CK(cudaEventRecord(ctx->ev[2], s));
-        CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
-        CK(cudaEventSynchronize(ctx->ev[6]));
-        CK(cudaEventSynchronize(ctx->ev[2]));  // the two streams end independently
+        pipe_join(ctx);
+        {
+            for (int i : t_leg) segs.push_back({"L", i});
+            for (int i : t_fft) segs.push_back({"F", i});
+            E.trace("alm2map", segs);
+        }
         if (t) {
-            float leg, fft;
-            band_timing(ctx, leg, fft);
-            fill_timing(t, leg, fft, elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
-                        elapsed(ctx->ev[3], ctx->ev[6]), P);
+            float leg = 0.f, fft = 0.f;
+            for (int i : t_leg) leg += E.span(i);
+            for (int i : t_fft) fft += E.span(i);
+            const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
+            fill_timing(t, leg, fft, E.span(th), d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }
@@ -1145,53 +1257,92 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         ctx->alm_buf.ensure(na);
         ctx->map_buf.ensure(nb);
         ctx->delta.ensure((size_t)ctx->n_rings * (ctx->mmax + 1) * sizeof(double2));
-        cudaStream_t s = ctx->stream;
         LegPlan& P = ctx->leg;
         FftPlan& F = ctx->fft_id;
         double2* ab = ctx->alm_buf.as<double2>();
         double* mb = ctx->map_buf.as<double>();
-        CK(cudaEventRecord(ctx->ev[3], s));
-        CK(cudaStreamWaitEvent(ctx->h2d, ctx->ev[3], 0));
-        for (int tc = 0; tc < kPipeChunks; ++tc) {
-            for (const auto& iv : F.band_pix[tc])
-                CK(cudaMemcpyAsync(mb + iv.first, map + iv.first, (iv.second - iv.first) * sizeof(double),
-                                   cudaMemcpyHostToDevice, ctx->h2d));
-            CK(cudaEventRecord(ctx->pev[0][tc], ctx->h2d));
-        }
+        double2* dl = ctx->delta.as<double2>();
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
-        CK(cudaEventRecord(ctx->ev[0], s));
-        launch_leg_map2alm(P.view, ctx->delta.as<double2>(), ro, ab, 0, P.counters.as<int>(),
-                           P.m2a_scratch.as<double2>(), s, LEG_PHASE_ZERO);
-        // the order-completion counters run across the band launches: reset them once here
-        CK(cudaMemsetAsync(P.counters.p, 0, (1 + ctx->ms.size()) * sizeof(int), s));
-        for (int tc = 0; tc < kPipeChunks; ++tc) {
-            CK(cudaStreamWaitEvent(s, ctx->pev[0][tc], 0));
-            CK(cudaEventRecord(ctx->tev[0][tc], s));
-            run_ring_anal(ctx, F, mb, ctx->delta.as<double2>(), nullptr, nullptr, tc);
-            CK(cudaEventRecord(ctx->tev[1][tc], s));
-            launch_leg_map2alm(items_view(P, P.m2a_off[tc], P.m2a_off[tc + 1], false), ctx->delta.as<double2>(),
-                               ro, ab, 0, P.counters.as<int>(), P.m2a_scratch.as<double2>(), s,
-                               LEG_PHASE_MAIN | LEG_PHASE_KEEP_DONE);
-            CK(cudaGetLastError());
-            CK(cudaEventRecord(ctx->tev[2][tc], s));
-            CK(cudaEventRecord(ctx->pev[1][tc], s));
-            CK(cudaStreamWaitEvent(ctx->d2h, ctx->pev[1][tc], 0));
-            for (const auto& run : P.m2a_done[tc]) {
-                auto [b, e] = alm_span(ctx, run.first, run.second);
-                if (e > b)
-                    CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ab + b, (e - b) * sizeof(double2),
-                                       cudaMemcpyDeviceToHost, ctx->d2h));
+        const int n_m = (int)ctx->ms.size();
+        int* m_done = P.counters.as<int>() + 1;
+        int* queues = m_done + n_m + P.a2m_launch.size();  // one word per launch
+        PipeEvents E{ctx};
+        // per-order completion counters run across the launches: zeroed once, with the queues
+        CK(cudaMemsetAsync(m_done, 0, (n_m + P.a2m_launch.size() + P.m2a_launch.size()) * sizeof(int),
+                           ctx->stream));
+        pipe_fork(ctx);
+        std::vector<cudaEvent_t> h_band(kPipeBands);
+        const int th = E.timed(ctx->h2d, [&] {
+            for (int tc = 0; tc < kPipeBands; ++tc) {
+                for (const auto& iv : F.band_pix[tc])
+                    CK(cudaMemcpyAsync(mb + iv.first, map + iv.first, (iv.second - iv.first) * sizeof(double),
+                                       cudaMemcpyHostToDevice, ctx->h2d));
+                h_band[tc] = E.order(ctx->h2d);
+            }
+        });
+        // SHTC_M2A_MODE (experiments): 0 (default) = Legendre launches alternate over two
+        // streams (one launch's tail overlaps the next) beside the high-priority ring analysis;
+        // 2 = analysis and launches band by band on one stream (measured slower: 14.0 against
+        // 13.4 ms at C4)
+        static const int mode = std::getenv("SHTC_M2A_MODE") ? std::atoi(std::getenv("SHTC_M2A_MODE")) : 0;
+        const bool serial = mode == 2;
+        // orders without alive tiles are zero: ahead of launch 0 (their copy follows it)
+        launch_leg_map2alm(P.view, dl, ro, ab, 0, P.counters.as<int>(), P.m2a_scratch.as<double2>(),
+                           serial ? ctx->fst : ctx->lst[0], LEG_PHASE_ZERO);
+        CK(cudaGetLastError());
+        std::vector<int> t_fft, t_leg;
+        std::vector<std::pair<const char*, int>> segs;
+        int t_d2h_first = -1;
+        cudaEvent_t prev = nullptr;
+        auto copy_final = [&](int j) {
+            const int ti = E.timed(ctx->d2h, [&] {
+                for (const auto& run : P.m2a_done[j]) {
+                    auto [b, e] = alm_span(ctx, run.first, run.second);
+                    if (e > b)
+                        CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ab + b, (e - b) * sizeof(double2),
+                                           cudaMemcpyDeviceToHost, ctx->d2h));
+                }
+            });
+            if (t_d2h_first < 0) t_d2h_first = ti;
+            segs.push_back({"D", ti});
+        };
+        if (P.m2a_launch.empty()) {
+            CK(cudaStreamWaitEvent(ctx->d2h, E.order(serial ? ctx->fst : ctx->lst[0]), 0));
+            copy_final(0);
+        }
+        size_t j = 0;
+        for (int tc = 0; tc < kPipeBands; ++tc) {
+            CK(cudaStreamWaitEvent(ctx->fst, h_band[tc], 0));
+            t_fft.push_back(E.timed(ctx->fst, [&] { run_ring_anal(ctx, F, mb, dl, nullptr, nullptr, tc, nullptr, ctx->fst); }));
+            cudaEvent_t anal_done = serial ? nullptr : E.order(ctx->fst);
+            for (; j < P.m2a_launch.size() && P.m2a_launch[j].tc == tc; ++j) {
+                const auto& L = P.m2a_launch[j];
+                cudaStream_t st = serial ? ctx->fst : ctx->lst[j & 1];
+                if (anal_done) CK(cudaStreamWaitEvent(st, anal_done, 0));
+                t_leg.push_back(E.timed(st, [&] {
+                    launch_leg_map2alm(items_view(P, L.begin, L.end, false), dl, ro, ab, 0, queues + j,
+                                       P.m2a_scratch.as<double2>(), st, LEG_PHASE_MAIN | LEG_PHASE_NO_RESET, m_done);
+                    CK(cudaGetLastError());
+                }));
+                cudaEvent_t done = E.order(st);
+                CK(cudaStreamWaitEvent(ctx->d2h, done, 0));
+                if (prev && !serial) CK(cudaStreamWaitEvent(ctx->d2h, prev, 0));
+                prev = done;
+                copy_final((int)j);
             }
         }
-        CK(cudaEventRecord(ctx->ev[2], s));
-        CK(cudaEventRecord(ctx->ev[6], ctx->d2h));
-        CK(cudaEventSynchronize(ctx->ev[6]));
-        CK(cudaEventSynchronize(ctx->ev[2]));  // the two streams end independently
+        pipe_join(ctx);
+        {
+            for (int i : t_leg) segs.push_back({"L", i});
+            for (int i : t_fft) segs.push_back({"F", i});
+            E.trace("map2alm", segs);
+        }
         if (t) {
-            float fft, leg;
-            band_timing(ctx, fft, leg);
-            fill_timing(t, leg, fft, elapsed(ctx->ev[3], ctx->ev[0]), elapsed(ctx->ev[2], ctx->ev[6]),
-                        elapsed(ctx->ev[3], ctx->ev[6]), P);
+            float leg = 0.f, fft = 0.f;
+            for (int i : t_leg) leg += E.span(i);
+            for (int i : t_fft) fft += E.span(i);
+            const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
+            fill_timing(t, leg, fft, E.span(th), d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }
