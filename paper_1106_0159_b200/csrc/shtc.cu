@@ -1133,6 +1133,18 @@ std::pair<size_t, size_t> alm_span(const shtc_ctx* c, int mi0, int mi1) {
     return {off(mi0), off(mi1)};
 }
 
+// device address of page-locked, mapped host memory (cudaHostAlloc, cudaHostRegister,
+// pinned torch tensors); nullptr for pageable memory
+double2* mapped_host_ptr(void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return nullptr;
+    }
+    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
+    return static_cast<double2*>(a.devicePointer);
+}
+
 // fork the pipeline streams off the caller's stream
 void pipe_fork(shtc_ctx* c) {
     CK(cudaEventRecord(c->ev[3], c->stream));
@@ -1259,12 +1271,16 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         ctx->delta.ensure((size_t)ctx->n_rings * (ctx->mmax + 1) * sizeof(double2));
         LegPlan& P = ctx->leg;
         FftPlan& F = ctx->fft_id;
-        double2* ab = ctx->alm_buf.as<double2>();
         double* mb = ctx->map_buf.as<double>();
         double2* dl = ctx->delta.as<double2>();
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
         const int n_m = (int)ctx->ms.size();
         int* m_done = P.counters.as<int>() + 1;
+        // a page-locked output buffer is written in place by each order's final reduction
+        // (mapped host memory over PCIe, as the order completes): no copy stage, no tail
+        double2* ab = mapped_host_ptr(alm);
+        const bool direct = ab != nullptr && !std::getenv("SHTC_NO_DIRECT");
+        if (!direct) ab = ctx->alm_buf.as<double2>();
         int* queues = m_done + n_m + P.a2m_launch.size();  // one word per launch
         PipeEvents E{ctx};
         // per-order completion counters run across the launches: zeroed once, with the queues
@@ -1295,6 +1311,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         int t_d2h_first = -1;
         cudaEvent_t prev = nullptr;
         auto copy_final = [&](int j) {
+            if (direct) return;
             const int ti = E.timed(ctx->d2h, [&] {
                 for (const auto& run : P.m2a_done[j]) {
                     auto [b, e] = alm_span(ctx, run.first, run.second);

@@ -168,3 +168,8 @@ def test_host_pipeline_matches_device_path(gpu_ctx, nside, lmax):
         if first is None:
             first = got_alm
         assert np.array_equal(got_alm, first)
+    # page-locked output: each order's final reduction writes the host buffer directly
+    pinned = torch.empty(2 * alm.size, dtype=torch.float64).pin_memory()
+    out = pinned.numpy().view(np.complex128)
+    gpu_ctx.map2alm(got_map, out=out)
+    assert np.array_equal(out, first)
