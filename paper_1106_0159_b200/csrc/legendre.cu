@@ -563,14 +563,64 @@ __device__ __forceinline__ double2 m2a_step_act(M2ALane<R>& L, double A, int i, 
     return part;
 }
 
-constexpr int M2A_G = 16;  // degrees per cross-lane reduction group
+// Cross-lane reduction of the per-lane partials (16 values per 8 degrees: degree x re/im).
+// Default: a shared-memory transpose over 16 degrees (each lane writes its row, lane j sums
+// column j).  LEG_M2A_SHFL=1: a register butterfly, reduce-scatter over the 32 lanes with
+// __shfl_xor (31 values exchanged per lane per 16 degrees, half the bytes of the transpose);
+// measured slower at C4 (11.2 against 8.85 ms): 64-bit shuffles cost more issue than the
+// shared-memory traffic they replace.
+#ifndef LEG_M2A_SHFL
+#define LEG_M2A_SHFL 0
+#endif
+#if LEG_M2A_SHFL
+constexpr int M2A_G = 8;  // degrees per cross-lane reduction group
+#else
+constexpr int M2A_G = 16;
+#endif
 
 template <int R>
 struct M2AWarpSmem {
     double A[LEG_CL];
+#if !LEG_M2A_SHFL
     double red[32][2 * M2A_G + 2];  // lane rows of (degree, re/im) partials, 16-byte aligned
-    double2 ck[R][32];              // activation checkpoints of the current tile
+#endif
+    double2 ck[R][32];  // activation checkpoints of the current tile
 };
+
+#if LEG_M2A_SHFL
+// Butterfly reduce-scatter: value c = 2u + comp (v[u].x / v[u].y) summed over the warp ends on
+// lanes 2c and 2c + 1 (both hold the same sum: the last stage adds a + b on one lane and b + a
+// on the other).  Fixed lane pairing and order, so the result is deterministic.
+__device__ __forceinline__ double m2a_reduce8(const double2 (&v)[8], int lane) {
+    double h[8];
+    const bool b4 = lane & 16;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        const double lo = (i & 1) ? v[i >> 1].y : v[i >> 1].x;               // c = i
+        const double hi = (i & 1) ? v[(i + 8) >> 1].y : v[(i + 8) >> 1].x;   // c = i + 8
+        const double recv = __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
+        h[i] = (b4 ? hi : lo) + recv;
+    }
+    const bool b3 = lane & 8;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const double recv = __shfl_xor_sync(0xffffffffu, b3 ? h[i] : h[i + 4], 8);
+        h[i] = (b3 ? h[i + 4] : h[i]) + recv;
+    }
+    const bool b2 = lane & 4;
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+        const double recv = __shfl_xor_sync(0xffffffffu, b2 ? h[i] : h[i + 2], 4);
+        h[i] = (b2 ? h[i + 2] : h[i]) + recv;
+    }
+    const bool b1 = lane & 2;
+    {
+        const double recv = __shfl_xor_sync(0xffffffffu, b1 ? h[0] : h[1], 2);
+        h[0] = (b1 ? h[1] : h[0]) + recv;
+    }
+    return h[0] + __shfl_xor_sync(0xffffffffu, h[0], 1);  // c = (lane >> 1) & 15
+}
+#endif
 
 }  // namespace
 
@@ -620,7 +670,11 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                 return i <= n ? gA[i] : 0.0;
             };
             // this lane's (degree, component) of the group in the scratch slot
+#if LEG_M2A_SHFL
+            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + (lane >> 1);
+#else
             double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
+#endif
             double nxt = fetch(0);
             for (int c = 0; c < nchunks; ++c) {
                 __syncwarp();
@@ -632,6 +686,55 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                 for (int g = 0; g < cnt; g += M2A_G) {
                     const int gc = min(M2A_G, cnt - g);
                     const int ig = i0 + g;  // even degree offset
+#if LEG_M2A_SHFL
+                    const int iw = ig + (lane >> 2);
+                    double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
+                    rmw_ptr += 2 * M2A_G;
+                    double2 row[M2A_G];  // this lane's partial (sum over its R streams) per degree
+                    if (ig > ie && gc == M2A_G) {
+                        // after the last activation: straight-line steps, coefficients in pairs
+#pragma unroll
+                        for (int u = 0; u < M2A_G; u += 2) {
+                            const double2 a = *reinterpret_cast<const double2*>(&sm.A[g + u]);
+                            row[u] = m2a_step<R, false>(L, a.x);
+                            row[u + 1] = m2a_step<R, true>(L, a.y);
+                        }
+                    } else {
+                        // activation window (warp-uniform event test per step), seed, partial group
+#pragma unroll
+                        for (int u = 0; u < M2A_G; u += 2) {
+                            const int i = ig + u;
+                            double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+                            if (u < gc) {
+                                if (i == 0) {
+                                    // seed term (degree offset 0): no recurrence step
+#pragma unroll
+                                    for (int r = 0; r < R; ++r) {
+                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
+                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
+                                    }
+                                } else if (i == ev) {
+                                    v1 = m2a_step_act<R, false>(L, sm.A[g + u], i, sm.ck, lane);
+                                    ev = next_activation<R>(L.act, i);
+                                } else {
+                                    v1 = m2a_step<R, false>(L, sm.A[g + u]);
+                                }
+                                if (u + 1 < gc) {
+                                    if (i + 1 == ev) {
+                                        v2 = m2a_step_act<R, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
+                                        ev = next_activation<R>(L.act, i + 1);
+                                    } else {
+                                        v2 = m2a_step<R, true>(L, sm.A[g + u + 1]);
+                                    }
+                                }
+                            }
+                            row[u] = v1;
+                            row[u + 1] = v2;
+                        }
+                    }
+                    const double v = m2a_reduce8(row, lane);
+                    const bool writer = !(lane & 1);
+#else
                     const int iw = ig + (lane >> 1);
                     double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
                     rmw_ptr += 2 * M2A_G;
@@ -690,9 +793,11 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                     }
                     const double v = (s0 + s1) + (s2 + s3);
                     __syncwarp();
+                    const bool writer = true;
+#endif
                     // first tile stores; later tiles add in place (fire-and-forget reduction,
                     // a single lane owns each word so the order is the tile order)
-                    if (iw <= n) {
+                    if (writer && iw <= n) {
                         if (tt == 0) *wp = v;
                         else asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
                     }

@@ -314,6 +314,13 @@ std::vector<int> ring_bands(const shtc_ctx* c, std::vector<Stream> st) {
     return rb;
 }
 
+// alm2map pipeline: bands whose Legendre launches run by order chunk while a_lm arrives
+// (SHTC_A2M_HEAD overrides)
+int a2m_head_bands() {
+    static const int h = std::getenv("SHTC_A2M_HEAD") ? std::max(1, std::atoi(std::getenv("SHTC_A2M_HEAD"))) : 2;
+    return std::min(h, kPipeBands);
+}
+
 // tiles per map2alm item of the pipelined (band) item set; SHTC_M2A_BAND_GROUP overrides
 int m2a_band_group() {
     static const int g = std::getenv("SHTC_M2A_BAND_GROUP") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_BAND_GROUP"))) : 1;
@@ -482,9 +489,12 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     std::stable_sort(m2a.begin(), m2a.end(),
                      [&](const LegItem& a, const LegItem& b) { return m2a_cost(a) > m2a_cost(b); });
     // alm2map band set: band, then (band 0 only) order chunk, then cost
+    // the head bands (0 .. a2m_head_bands()-1) run together, split by order chunk, while a_lm
+    // arrives (launch band tag 0)
     auto a2m_key = [&](const LegItem& it) {
         const int tc = tband[it.a];
-        return std::make_pair(tc, tc == 0 ? chunk_of[it.mi] : 0);
+        const bool head = tc < a2m_head_bands();
+        return std::make_pair(head ? 0 : tc, head ? chunk_of[it.mi] : 0);
     };
     std::vector<LegItem> a2m_b = a2m;
     std::stable_sort(a2m_b.begin(), a2m_b.end(), [&](const LegItem& a, const LegItem& b) {
@@ -1203,23 +1213,28 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         // dead tiles' Delta rows (disjoint from every launch's rows) ahead of the ring stage
         launch_leg_alm2map(P.view, ab, dl, ro, P.counters.as<int>(), ctx->fst, LEG_PHASE_ZERO);
         CK(cudaGetLastError());
-        // SHTC_PIPE_MODE (experiments): 0 = Legendre launches run ahead freely on two streams;
-        // 1 = a band's launches wait for the ring synthesis two bands back (the Legendre stage
-        // runs at most one band ahead, so the ring stage gets whole SMs at launch tails);
-        // 2 = everything on one stream, band by band
+        // SHTC_PIPE_MODE (experiments): 2 (default) = everything on one stream, band by band (the
+        // ring synthesis needs whole SMs, which a running persistent Legendre launch never
+        // frees); 0 = Legendre launches run ahead on two streams (measured slower)
         static const int mode = std::getenv("SHTC_PIPE_MODE") ? std::atoi(std::getenv("SHTC_PIPE_MODE")) : 2;
         std::vector<int> t_leg, t_fft;
         std::vector<std::pair<const char*, int>> segs;
-        std::vector<cudaEvent_t> synth_done(kPipeBands, nullptr);
         int t_d2h_first = -1;
-        size_t j = 0;
-        for (int tc = 0; tc < kPipeBands; ++tc) {
+        // band order: the head bands at the equator first (their launches run by order chunk
+        // while a_lm arrives), then from the pole back toward the equator, so the last band
+        // before the final copy has the cheap belt-ring synthesis (SHTC_A2M_ORDER=0: ascending)
+        static const bool polar_early = !std::getenv("SHTC_A2M_ORDER") || std::atoi(std::getenv("SHTC_A2M_ORDER"));
+        const int nh = a2m_head_bands();
+        std::vector<int> band_order(kPipeBands);
+        for (int k = 0; k < kPipeBands; ++k) band_order[k] = (!polar_early || k < nh) ? k : kPipeBands - 1 - (k - nh);
+        std::vector<std::vector<size_t>> band_launches(kPipeBands);
+        for (size_t q = 0; q < P.a2m_launch.size(); ++q) band_launches[P.a2m_launch[q].tc].push_back(q);
+        for (int tc : band_order) {
             std::vector<cudaEvent_t> band_done;
-            for (; j < P.a2m_launch.size() && P.a2m_launch[j].tc == tc; ++j) {
+            for (size_t j : band_launches[tc]) {
                 const auto& L = P.a2m_launch[j];
                 cudaStream_t st = mode == 2 ? ctx->fst : ctx->lst[j & 1];
                 CK(cudaStreamWaitEvent(st, h_chunk[L.tc == 0 ? L.mc : kOrderChunks - 1], 0));
-                if (mode == 1 && tc >= 2 && synth_done[tc - 2]) CK(cudaStreamWaitEvent(st, synth_done[tc - 2], 0));
                 t_leg.push_back(E.timed(st, [&] {
                     launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, dl, ro, queues + j, st,
                                        LEG_PHASE_MAIN | LEG_PHASE_NO_RESET);
@@ -1230,8 +1245,7 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
             if (F.band_pix[tc].empty() && band_done.empty()) continue;
             for (cudaEvent_t e : band_done) CK(cudaStreamWaitEvent(ctx->fst, e, 0));
             t_fft.push_back(E.timed(ctx->fst, [&] { run_ring_synth(ctx, F, dl, mb, nullptr, nullptr, tc, ctx->fst); }));
-            synth_done[tc] = E.order(ctx->fst);
-            CK(cudaStreamWaitEvent(ctx->d2h, synth_done[tc], 0));
+            CK(cudaStreamWaitEvent(ctx->d2h, E.order(ctx->fst), 0));
             const int ti = E.timed(ctx->d2h, [&] {
                 for (const auto& iv : F.band_pix[tc])
                     CK(cudaMemcpyAsync(map + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
