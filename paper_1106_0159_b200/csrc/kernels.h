@@ -75,6 +75,9 @@ struct LegPlanView {
     const int* m2a_items_per_m;     // [n_m]
     const int64_t* m2a_slot_base;   // [n_m] double2 offset of the order's first partial slot
     int64_t m2a_scratch_elems;
+    // map2alm: 0 = the last item of an order to finish sums the order's partial slots;
+    // 1 = the slots are left for leg_m2a_finalize (launched once the order's items are done)
+    int defer_final;
     // fused exchange (alm2map): ring r's output row is row_ptr[r] (an address in the ring
     // owner's receive buffer, peer memory) instead of delta + row_off[r]; nullptr: local
     double2* const* row_ptr;
@@ -111,6 +114,10 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
                         double2* alm, int accumulate, int* counters, double2* scratch,
                         cudaStream_t s, int phases = LEG_PHASE_ALL, int* m_done = nullptr);
 int leg_persistent_blocks(int device);
+// a_lm of the listed order indices from their partial slots (p's item set): slots summed in
+// slot order, scaled by c_l, stored (or added when accumulate) -- one thread per coefficient
+void launch_leg_m2a_finalize(const LegPlanView& p, const int* mis, int n_mis, const double2* scratch,
+                             double2* alm, int accumulate, cudaStream_t s);
 
 // ---------------------------------------------------------------------------------------
 // Ring Fourier stage

@@ -805,6 +805,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
             }
         }
 
+        if (p.defer_final) continue;
         // last item of this order to finish reduces the order's partial slots (fixed order)
         __threadfence();
         int last = 0;
@@ -834,6 +835,40 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
             }
         }
     }
+}
+
+__global__ void leg_m2a_finalize_kernel(LegPlanView p, const int* __restrict__ mis,
+                                        const double2* __restrict__ scratch, double2* __restrict__ alm,
+                                        int accumulate) {
+    const int mi = mis[blockIdx.y];
+    const int m = p.ms[mi];
+    const int n = p.lmax - m;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i > n) return;
+    const int G = p.m2a_items_per_m[mi];
+    if (G == 0) return;  // no alive tile: the zero pass wrote it
+    const double2* base = scratch + p.m2a_slot_base[mi] + i;
+    double2 v = make_double2(0.0, 0.0);
+    int g = 0;
+    for (; g + 4 <= G; g += 4) {  // same slot order and association as the in-kernel reduction
+        const double2 a0 = __ldcg(base + (int64_t)g * (n + 1));
+        const double2 a1 = __ldcg(base + (int64_t)(g + 1) * (n + 1));
+        const double2 a2 = __ldcg(base + (int64_t)(g + 2) * (n + 1));
+        const double2 a3 = __ldcg(base + (int64_t)(g + 3) * (n + 1));
+        v = cadd(cadd(cadd(cadd(v, a0), a1), a2), a3);
+    }
+    for (; g < G; ++g) v = cadd(v, __ldcg(base + (int64_t)g * (n + 1)));
+    const double c = p.tab.C[p.tab.tab_off[mi] + i];
+    v = make_double2(v.x * c, v.y * c);
+    double2* out = alm + alm_offset(m, p.lmax) + i;
+    *out = accumulate ? cadd(*out, v) : v;
+}
+
+void launch_leg_m2a_finalize(const LegPlanView& p, const int* mis, int n_mis, const double2* scratch,
+                             double2* alm, int accumulate, cudaStream_t s) {
+    if (n_mis <= 0) return;
+    dim3 grid((p.lmax + 1 + 127) / 128, n_mis);
+    leg_m2a_finalize_kernel<<<grid, 128, 0, s>>>(p, mis, scratch, alm, accumulate);
 }
 
 // orders without any alive tile: every term is dropped, a_lm = 0 (or unchanged when +=)

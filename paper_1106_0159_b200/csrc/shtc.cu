@@ -121,6 +121,8 @@ struct LegPlan {
     std::vector<PipeLaunch> m2a_launch;
     LegPlanView band_view{};             // view with the band-ordered item lists
     std::vector<std::vector<std::pair<int, int>>> m2a_done;  // per m2a launch: final order runs
+    DevBuf m2a_final_list;           // order indices final after each m2a launch, concatenated
+    std::vector<int> m2a_final_off;  // launch j: [m2a_final_off[j], m2a_final_off[j+1])
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
     double build_ms = 0.0;
@@ -321,6 +323,31 @@ int a2m_head_bands() {
     return std::min(h, kPipeBands);
 }
 
+// map2alm pipeline: the band after whose ring analysis each band's Legendre items launch
+// (default: every band on its own; SHTC_M2A_GROUPS="1,1,2,2,2" = band counts per launch --
+// merged launches measured slower at C4).
+std::vector<int> m2a_launch_bands() {
+    std::vector<int> sizes;
+    if (const char* e = std::getenv("SHTC_M2A_GROUPS")) {
+        for (const char* q = e; *q;) {
+            sizes.push_back(std::max(1, std::atoi(q)));
+            while (*q && *q != ',') ++q;
+            if (*q) ++q;
+        }
+    } else {
+        sizes.assign(kPipeBands, 1);
+    }
+    std::vector<int> tag(kPipeBands, kPipeBands - 1);
+    int first = 0;
+    for (int sz : sizes) {
+        const int last = std::min(kPipeBands - 1, first + sz - 1);
+        for (int b = first; b <= last; ++b) tag[b] = last;
+        first = last + 1;
+        if (first >= kPipeBands) break;
+    }
+    return tag;
+}
+
 // tiles per map2alm item of the pipelined (band) item set; SHTC_M2A_BAND_GROUP overrides
 int m2a_band_group() {
     static const int g = std::getenv("SHTC_M2A_BAND_GROUP") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_BAND_GROUP"))) : 1;
@@ -484,6 +511,19 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         }
         while ((int)P.chunk_mi.size() <= kOrderChunks) P.chunk_mi.push_back(n_m);
     }
+    // map2alm: the last band's launches by finer order chunks, so the a_lm copy of each
+    // chunk overlaps the next chunk's launch (SHTC_M2A_CHUNKS overrides)
+    static const int m2a_chunks =
+        std::getenv("SHTC_M2A_CHUNKS") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_CHUNKS"))) : 8;
+    std::vector<int> m2a_chunk_of(n_m, 0);
+    {
+        int64_t total = 0, acc = 0;
+        for (int i = 0; i < n_m; ++i) total += lmax - ms[i] + 1;
+        for (int i = 0; i < n_m; ++i) {
+            m2a_chunk_of[i] = (int)std::min<int64_t>(m2a_chunks - 1, acc * m2a_chunks / std::max<int64_t>(total, 1));
+            acc += lmax - ms[i] + 1;
+        }
+    }
     std::stable_sort(a2m.begin(), a2m.end(),
                      [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
     std::stable_sort(m2a.begin(), m2a.end(),
@@ -511,9 +551,10 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     // map2alm band set: an item runs with the band of its tiles (groups do not cross bands),
     // the last band also split by order chunk, then cost; an order is final after the launch
     // of its last item
+    const std::vector<int> m2a_tag = m2a_launch_bands();
     auto m2a_key = [&](const LegItem& it) {
-        const int tc = tband[tl[it.a + it.b - 1]];
-        return std::make_pair(tc, tc == kPipeBands - 1 ? chunk_of[it.mi] : 0);
+        const int tag = m2a_tag[tband[tl[it.a + it.b - 1]]];
+        return std::make_pair(tag, tag == kPipeBands - 1 ? m2a_chunk_of[it.mi] : 0);
     };
     std::stable_sort(m2a_b.begin(), m2a_b.end(), [&](const LegItem& a, const LegItem& b) {
         if (m2a_key(a) != m2a_key(b)) return m2a_key(a) < m2a_key(b);
@@ -529,11 +570,22 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         k = e;
     }
     P.m2a_done.assign(std::max<size_t>(1, P.m2a_launch.size()), {});
+    std::vector<std::vector<int>> final_of(P.m2a_done.size());
     for (int i = 0; i < n_m; ++i) {
         auto& runs = P.m2a_done[last_launch[i]];
         if (!runs.empty() && runs.back().second == i) runs.back().second = i + 1;
         else runs.push_back({i, i + 1});
+        final_of[last_launch[i]].push_back(i);
     }
+    // order indices final after each launch, for the deferred reduction (leg_m2a_finalize)
+    std::vector<int> fl;
+    P.m2a_final_off.assign(1, 0);
+    for (const auto& f : final_of) {
+        fl.insert(fl.end(), f.begin(), f.end());
+        P.m2a_final_off.push_back((int)fl.size());
+    }
+    if (fl.empty()) fl.push_back(0);
+    P.m2a_final_list.upload(fl, s);
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
     P.tile_off.upload(toffs, s);
@@ -566,6 +618,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.band_view.n_m2a_items = (int)m2a_b.size();
     P.band_view.m2a_items_per_m = P.m2a_per_m_band.as<int>();
     P.band_view.m2a_slot_base = P.m2a_slot_band.as<int64_t>();
+    P.band_view.defer_final = 1;
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float ms_el = 0.f;
@@ -1143,18 +1196,6 @@ std::pair<size_t, size_t> alm_span(const shtc_ctx* c, int mi0, int mi1) {
     return {off(mi0), off(mi1)};
 }
 
-// device address of page-locked, mapped host memory (cudaHostAlloc, cudaHostRegister,
-// pinned torch tensors); nullptr for pageable memory
-double2* mapped_host_ptr(void* p) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return nullptr;
-    }
-    if (a.type != cudaMemoryTypeHost || !a.devicePointer) return nullptr;
-    return static_cast<double2*>(a.devicePointer);
-}
-
 // fork the pipeline streams off the caller's stream
 void pipe_fork(shtc_ctx* c) {
     CK(cudaEventRecord(c->ev[3], c->stream));
@@ -1290,11 +1331,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
         const int n_m = (int)ctx->ms.size();
         int* m_done = P.counters.as<int>() + 1;
-        // a page-locked output buffer is written in place by each order's final reduction
-        // (mapped host memory over PCIe, as the order completes): no copy stage, no tail
-        double2* ab = mapped_host_ptr(alm);
-        const bool direct = ab != nullptr && !std::getenv("SHTC_NO_DIRECT");
-        if (!direct) ab = ctx->alm_buf.as<double2>();
+        double2* ab = ctx->alm_buf.as<double2>();
         int* queues = m_done + n_m + P.a2m_launch.size();  // one word per launch
         PipeEvents E{ctx};
         // per-order completion counters run across the launches: zeroed once, with the queues
@@ -1325,7 +1362,6 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         int t_d2h_first = -1;
         cudaEvent_t prev = nullptr;
         auto copy_final = [&](int j) {
-            if (direct) return;
             const int ti = E.timed(ctx->d2h, [&] {
                 for (const auto& run : P.m2a_done[j]) {
                     auto [b, e] = alm_span(ctx, run.first, run.second);
@@ -1355,10 +1391,15 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
                                        P.m2a_scratch.as<double2>(), st, LEG_PHASE_MAIN | LEG_PHASE_NO_RESET, m_done);
                     CK(cudaGetLastError());
                 }));
-                cudaEvent_t done = E.order(st);
-                CK(cudaStreamWaitEvent(ctx->d2h, done, 0));
-                if (prev && !serial) CK(cudaStreamWaitEvent(ctx->d2h, prev, 0));
-                prev = done;
+                // the launch's final orders: their items ran in this launch and earlier ones
+                // (launch j - 1 may still run beside it on the other stream)
+                if (prev && !serial) CK(cudaStreamWaitEvent(st, prev, 0));
+                prev = E.order(st);
+                launch_leg_m2a_finalize(P.band_view, P.m2a_final_list.as<int>() + P.m2a_final_off[j],
+                                        P.m2a_final_off[j + 1] - P.m2a_final_off[j], P.m2a_scratch.as<double2>(),
+                                        ab, 0, st);
+                CK(cudaGetLastError());
+                CK(cudaStreamWaitEvent(ctx->d2h, E.order(st), 0));
                 copy_final((int)j);
             }
         }
