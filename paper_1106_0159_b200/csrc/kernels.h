@@ -44,7 +44,10 @@ constexpr int LEG_CL = 32;        // degree steps staged per chunk (one entry pe
 #ifndef LEG_M2A_MINB
 #define LEG_M2A_MINB 4
 #endif
-constexpr int LEG_M2A_GROUP = 4;  // tiles per map2alm work item (partials reduce G-fold)
+#ifndef LEG_M2A_GROUP_DEF
+#define LEG_M2A_GROUP_DEF 4
+#endif
+constexpr int LEG_M2A_GROUP = LEG_M2A_GROUP_DEF;  // tiles per map2alm work item (partials reduce G-fold)
 
 // One warp-sized unit of work of the persistent kernels.
 //   alm2map: (mi, tile id, -, -); map2alm: (mi, first index into tile_list, tile count, item
@@ -98,21 +101,20 @@ __host__ __device__ inline int leg_tile_start(int is) { return is >= 2 ? (is & ~
 // counters: >= 1 + n_m ints of device scratch (zeroed by the launcher).
 // phases: bit0 = zero pass (dead tiles / orders without alive tiles), bit1 = the persistent
 // kernel over p's item list (callers may pass a view restricted to one chunk of items).
-// bit2 (map2alm) = keep the per-order completion counters of an earlier launch (the order's
-// work items are split over several launches; only the first one resets them).  bit3 = the
-// caller has zeroed the queue counter (and m_done): concurrent launches on different streams
-// each get their own queue word.
-constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3, LEG_PHASE_KEEP_DONE = 4,
-              LEG_PHASE_NO_RESET = 8;
+// bit3 = the
+// caller has zeroed the queue counter: concurrent launches on different streams each get
+// their own queue word.
+constexpr int LEG_PHASE_ZERO = 1, LEG_PHASE_MAIN = 2, LEG_PHASE_ALL = 3, LEG_PHASE_NO_RESET = 8;
 void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta,
                         const int64_t* row_off, int* counters, cudaStream_t s,
                         int phases = LEG_PHASE_ALL);
 // a_lm (= or +=) sum over streams; accumulate != 0 adds into alm.  scratch: m2a_scratch_elems.
-// counters[0] is the work queue; the per-order completion counters are m_done (n_m ints,
-// default counters + 1).
+// counters[0] is the work queue.  Unless p.defer_final, a finalize kernel sums every order's
+// slots after the main kernel (pipelined band launches call launch_leg_m2a_finalize
+// themselves once an order's last launch is done).
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s, int phases = LEG_PHASE_ALL, int* m_done = nullptr);
+                        cudaStream_t s, int phases = LEG_PHASE_ALL);
 int leg_persistent_blocks(int device);
 // a_lm of the listed order indices from their partial slots (p's item set): slots summed in
 // slot order, scaled by c_l, stored (or added when accumulate) -- one thread per coefficient

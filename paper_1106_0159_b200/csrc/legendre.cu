@@ -26,9 +26,9 @@
 //     coefficients (and c_l-scaled a_lm) in its own shared-memory slice LEG_CL degrees at a
 //     time, so no block-wide barrier couples warps that sit in different phases.
 //   * map2alm reduces over the 32 x R streams of a warp through a shared-memory transpose every
-//     16 degrees, accumulates up to LEG_M2A_GROUP tiles per work item into a scratch slot, and
-//     the last item of an order to finish sums the order's slots in a fixed order (no atomics
-//     on data, bitwise reproducible).
+//     16 degrees and accumulates up to LEG_M2A_GROUP tiles per work item into a scratch slot;
+//     a finalize kernel then sums each order's slots in a fixed order (one thread per
+//     coefficient; no atomics on data, bitwise reproducible).
 
 #include <climits>
 
@@ -627,8 +627,7 @@ __device__ __forceinline__ double m2a_reduce8(const double2 (&v)[8], int lane) {
 template <int R>
 __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
-                       const int64_t* __restrict__ row_off, double2* __restrict__ alm,
-                       int accumulate, int* __restrict__ queue, int* __restrict__ m_done,
+                       const int64_t* __restrict__ row_off, int* __restrict__ queue,
                        double2* __restrict__ scratch) {
     static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
     __shared__ M2AWarpSmem<R> sm_all[LEG_WARPS];
@@ -804,43 +803,15 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                 }
             }
         }
-
-        if (p.defer_final) continue;
-        // last item of this order to finish reduces the order's partial slots (fixed order)
-        __threadfence();
-        int last = 0;
-        if (lane == 0) last = (atomicAdd(m_done + mi, 1) == p.m2a_items_per_m[mi] - 1);
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-            __threadfence();
-            const double* __restrict__ gC = p.tab.C + toff;
-            const int G = p.m2a_items_per_m[mi];
-            const double2* base = scratch + p.m2a_slot_base[mi];
-            double2* out = alm + alm_offset(m, p.lmax);
-            for (int i = lane; i <= n; i += 32) {
-                // slots summed in order g = 0, 1, ...; loads issued in batches of 4
-                double2 v = make_double2(0.0, 0.0);
-                int g = 0;
-                for (; g + 4 <= G; g += 4) {
-                    const double2 a0 = __ldcg(base + (int64_t)g * (n + 1) + i);
-                    const double2 a1 = __ldcg(base + (int64_t)(g + 1) * (n + 1) + i);
-                    const double2 a2 = __ldcg(base + (int64_t)(g + 2) * (n + 1) + i);
-                    const double2 a3 = __ldcg(base + (int64_t)(g + 3) * (n + 1) + i);
-                    v = cadd(cadd(cadd(cadd(v, a0), a1), a2), a3);
-                }
-                for (; g < G; ++g) v = cadd(v, __ldcg(base + (int64_t)g * (n + 1) + i));
-                const double c = gC[i];
-                v = make_double2(v.x * c, v.y * c);
-                out[i] = accumulate ? cadd(out[i], v) : v;
-            }
-        }
     }
 }
 
+// a_lm of order mi, degree offset i: the order's partial slots summed in slot order (batches
+// of 4 loads), times c_l.  One thread per coefficient, after every item of the order is done.
 __global__ void leg_m2a_finalize_kernel(LegPlanView p, const int* __restrict__ mis,
                                         const double2* __restrict__ scratch, double2* __restrict__ alm,
                                         int accumulate) {
-    const int mi = mis[blockIdx.y];
+    const int mi = mis ? mis[blockIdx.y] : (int)blockIdx.y;
     const int m = p.ms[mi];
     const int n = p.lmax - m;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -850,7 +821,7 @@ __global__ void leg_m2a_finalize_kernel(LegPlanView p, const int* __restrict__ m
     const double2* base = scratch + p.m2a_slot_base[mi] + i;
     double2 v = make_double2(0.0, 0.0);
     int g = 0;
-    for (; g + 4 <= G; g += 4) {  // same slot order and association as the in-kernel reduction
+    for (; g + 4 <= G; g += 4) {
         const double2 a0 = __ldcg(base + (int64_t)g * (n + 1));
         const double2 a1 = __ldcg(base + (int64_t)(g + 1) * (n + 1));
         const double2 a2 = __ldcg(base + (int64_t)(g + 2) * (n + 1));
@@ -882,7 +853,7 @@ __global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm)
 
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
-                        cudaStream_t s, int phases, int* m_done) {
+                        cudaStream_t s, int phases) {
     if (p.n_m == 0) return;
     if (!accumulate && (phases & LEG_PHASE_ZERO)) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
     if (!(phases & LEG_PHASE_MAIN) || p.n_m2a_items == 0) return;
@@ -894,13 +865,11 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
     int blocks = sms * (per > 0 ? per : 1);
     const int need = (p.n_m2a_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
-    if (!m_done) m_done = counters + 1;
-    if (!(phases & LEG_PHASE_NO_RESET)) {
-        cudaMemsetAsync(counters, 0, sizeof(int), s);
-        if (!(phases & LEG_PHASE_KEEP_DONE)) cudaMemsetAsync(m_done, 0, sizeof(int) * p.n_m, s);
-    }
-    leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, alm, accumulate,
-                                                                counters, m_done, scratch);
+    if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
+    leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, counters, scratch);
+    // whole launches reduce every order's slots here; pipelined band launches (defer_final)
+    // leave them to the caller, which finalizes each order once its last launch is done
+    if (!p.defer_final) launch_leg_m2a_finalize(p, nullptr, p.n_m, scratch, alm, accumulate, s);
 }
 
 }  // namespace shtk

@@ -599,8 +599,8 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     P.m2a_per_m_band.upload(per_m_b, s);
     P.m2a_slot_band.upload(slot_b, s);
     P.m2a_scratch.ensure((size_t)std::max<int64_t>(std::max(slots, slots_b), 1) * sizeof(double2));
-    // [0]: queue of single launches, [1, 1 + n_m): per-order completion, then one queue word
-    // per pipelined launch
+    // [0]: queue of single launches, [1, 1 + n_m): spare, then one queue word per pipelined
+    // launch
     P.counters.ensure((size_t)(1 + n_m + P.a2m_launch.size() + P.m2a_launch.size()) * sizeof(int));
     v.tile_list = P.tile_list.as<int>();
     v.tile_list_off = P.tile_off.as<int>();
@@ -1330,13 +1330,11 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         double2* dl = ctx->delta.as<double2>();
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
         const int n_m = (int)ctx->ms.size();
-        int* m_done = P.counters.as<int>() + 1;
         double2* ab = ctx->alm_buf.as<double2>();
-        int* queues = m_done + n_m + P.a2m_launch.size();  // one word per launch
+        int* queues = P.counters.as<int>() + 1 + n_m + P.a2m_launch.size();  // one word per launch
         PipeEvents E{ctx};
-        // per-order completion counters run across the launches: zeroed once, with the queues
-        CK(cudaMemsetAsync(m_done, 0, (n_m + P.a2m_launch.size() + P.m2a_launch.size()) * sizeof(int),
-                           ctx->stream));
+        if (!P.m2a_launch.empty())
+            CK(cudaMemsetAsync(queues, 0, P.m2a_launch.size() * sizeof(int), ctx->stream));
         pipe_fork(ctx);
         std::vector<cudaEvent_t> h_band(kPipeBands);
         const int th = E.timed(ctx->h2d, [&] {
@@ -1388,7 +1386,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
                 if (anal_done) CK(cudaStreamWaitEvent(st, anal_done, 0));
                 t_leg.push_back(E.timed(st, [&] {
                     launch_leg_map2alm(items_view(P, L.begin, L.end, false), dl, ro, ab, 0, queues + j,
-                                       P.m2a_scratch.as<double2>(), st, LEG_PHASE_MAIN | LEG_PHASE_NO_RESET, m_done);
+                                       P.m2a_scratch.as<double2>(), st, LEG_PHASE_MAIN | LEG_PHASE_NO_RESET);
                     CK(cudaGetLastError());
                 }));
                 // the launch's final orders: their items ran in this launch and earlier ones
