@@ -280,7 +280,7 @@ void sort_streams(std::vector<Stream>& streams) {
 }
 
 // Pipeline band of every tile of the sorted streams: contiguous tile ranges of ~equal pixel
-// counts, band 0 at the equator.
+// counts (band 0 half), band 0 at the equator.
 std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     const int ns = (int)st.size();
     const int nt = (ns + LEG_TILE - 1) / LEG_TILE;
@@ -294,11 +294,19 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
         pix[i / LEG_TILE] += p;
         total += p;
     }
+    // band k covers the pixel fraction [cum[k], cum[k+1]) counted from the equator; the
+    // equatorial band 0 has half the weight of the others (it is map2alm's first H2D, so it
+    // sets the head latency) -- SHTC_BAND0_WEIGHT overrides
+    static const double w0 = std::getenv("SHTC_BAND0_WEIGHT") ? std::atof(std::getenv("SHTC_BAND0_WEIGHT")) : 0.5;
+    std::vector<double> cum(kPipeBands + 1, 0.0);
+    for (int k = 0; k < kPipeBands; ++k) cum[k + 1] = cum[k] + (k == 0 ? w0 : 1.0);
     std::vector<int> band(nt);
-    int64_t acc = 0;
+    int64_t acc = 0;  // pixels of the tiles polar of t
     for (int t = 0; t < nt; ++t) {
-        const int polar = (int)std::min<int64_t>(kPipeBands - 1, acc * kPipeBands / std::max<int64_t>(total, 1));
-        band[t] = kPipeBands - 1 - polar;
+        const double eq = (double)(total - acc - pix[t]) / (double)std::max<int64_t>(total, 1) * cum[kPipeBands];
+        int k = 0;
+        while (k + 1 < kPipeBands && eq >= cum[k + 1]) ++k;
+        band[t] = k;
         acc += pix[t];
     }
     return band;
