@@ -139,7 +139,12 @@ int pipe_bands() {
     return b;
 }
 #define kPipeBands pipe_bands()
-constexpr int kOrderChunks = 4;
+// a_lm order chunks of the alm2map head (SHTC_A2M_CHUNKS overrides)
+int order_chunks() {
+    static const int c = std::getenv("SHTC_A2M_CHUNKS") ? std::min(16, std::max(1, std::atoi(std::getenv("SHTC_A2M_CHUNKS")))) : 4;
+    return c;
+}
+#define kOrderChunks order_chunks()
 constexpr int kPipeEvents = 128;
 
 struct FftPlan {
@@ -1249,7 +1254,7 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
             CK(cudaMemsetAsync(queues, 0, P.a2m_launch.size() * sizeof(int), ctx->stream));
         pipe_fork(ctx);
         // a_lm by order chunk
-        cudaEvent_t h_chunk[kOrderChunks];
+        std::vector<cudaEvent_t> h_chunk(kOrderChunks);
         const int th = E.timed(ctx->h2d, [&] {
             for (int k = 0; k < kOrderChunks; ++k) {
                 auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
