@@ -29,9 +29,11 @@ def main():
     ap.add_argument("kernel")
     ap.add_argument("--top", type=int, default=30)
     ap.add_argument("--range", type=int, nargs=2)
+    ap.add_argument("--skip", type=int, default=0, help="launches of the matching kernels to skip")
     a = ap.parse_args()
     out = subprocess.run(["ncu", "-i", a.rep, "--page", "source", "--csv", "--print-source", "sass",
-                          "--kernel-name", "regex:" + a.kernel], capture_output=True, text=True).stdout
+                          "--kernel-name", "regex:" + a.kernel,
+                          "--launch-skip", str(a.skip), "--launch-count", "1"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h = rows[1]
     data = []
