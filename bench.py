@@ -301,11 +301,13 @@ def run_ours(args):
         if use_exchange:
             dist.barrier()
         ev0.record(stream)
+        n_launch0 = sht.kernel_launches()
         for _ in range(args.steps):
             t1, t2 = step()
             leg_s.append(t1["legendre_ms"]); fft_s.append(t1["fft_ms"])
             leg_a.append(t2["legendre_ms"]); fft_a.append(t2["fft_ms"])
         ev1.record(stream)
+        n_launches = sht.kernel_launches() - n_launch0  # the library's own kernels, timed region
         torch.cuda.synchronize(dev)
         if use_exchange:
             dist.barrier()
@@ -332,17 +334,20 @@ def run_ours(args):
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
+        n_launch_e0 = sht.kernel_launches()
         for _ in range(args.steps):
             ctx.alm2map(a_np, out=m_np)
             ctx.map2alm(m_np, out=b_np)
         e1.record(stream)
+        n_launch_e2e = sht.kernel_launches() - n_launch_e0
         torch.cuda.synchronize(dev)
         e2e_ms = e0.elapsed_time(e1) / args.steps
         bytes_alm = n_alm * 16
         bytes_map = grid.n_pix * 8
         e2e = {"value": 2 * falg_flops(lmax, mmax, grid.n_rings) / (e2e_ms * 1e-3) / 1e12,
                "unit": "TFLOP/s", "ms_per_step": e2e_ms,
-               "h2d_bytes_per_step": bytes_alm + bytes_map, "d2h_bytes_per_step": bytes_map + bytes_alm}
+               "h2d_bytes_per_step": bytes_alm + bytes_map, "d2h_bytes_per_step": bytes_map + bytes_alm,
+               "gpu_launches": n_launch_e2e}
 
     # ---- parity spot check of the timed output (the reference is checked in tests/) ----
     roundtrip = None
@@ -413,7 +418,7 @@ def run_ours(args):
                      if use_exchange else None),
         "roundtrip_rel_err": roundtrip,
         "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
-        "gpu_launches": args.steps * (2 + 2 + 2 * 4),
+        "gpu_launches": n_launches,
     }
     if ws == 1 and not args.no_cpu_baseline:
         try:

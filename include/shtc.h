@@ -69,6 +69,9 @@ typedef struct {
 shtc_status shtc_create(int device, shtc_ctx** out);
 void shtc_destroy(shtc_ctx* ctx);
 const char* shtc_last_error(const shtc_ctx* ctx); /* ctx may be NULL (last global error) */
+/* Kernel launches issued by the library so far (process-wide counter; a caller brackets a
+ * region with two reads to state how many of the library's kernels ran in it). */
+uint64_t shtc_kernel_launches(void);
 int shtc_device_count(void);
 /* Use an external CUDA stream (cudaStream_t passed as void*; NULL = the context's own). */
 shtc_status shtc_set_stream(shtc_ctx* ctx, void* cuda_stream);

@@ -6,6 +6,11 @@
 
 namespace shtk {
 
+// Every kernel launch of the library is counted (process-wide), so a caller can state how many
+// of the library's kernels ran inside a timed region (shtc_kernel_launches).
+void count_launch();
+unsigned long long launch_count();
+
 // ---------------------------------------------------------------------------------------
 // Legendre stage
 // ---------------------------------------------------------------------------------------

@@ -30,12 +30,19 @@
 //     a finalize kernel then sums each order's slots in a fixed order (one thread per
 //     coefficient; no atomics on data, bitwise reproducible).
 
+#include <atomic>
 #include <climits>
 
 #include "common.cuh"
 #include "kernels.h"
 
 namespace shtk {
+
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}  // namespace
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+unsigned long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 namespace {
 
@@ -117,6 +124,7 @@ __global__ void leg_tables_kernel(const int* __restrict__ ms, int n_m, int lmax,
 void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s) {
     const int th = 64;
     leg_tables_kernel<<<(n_m + th - 1) / th, th, 0, s>>>(ms_dev, n_m, lmax, tab);
+    count_launch();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -165,6 +173,7 @@ __global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out, double
 void launch_leg_scan(const LegPlanView& p, int* act_dev, double2* ck_dev, cudaStream_t s) {
     dim3 grid((p.st.n + 127) / 128, p.n_m);
     leg_scan_kernel<<<grid, 128, 0, s>>>(p, act_dev, ck_dev);
+    count_launch();
 }
 
 __global__ void leg_tile_summary_kernel(LegPlanView p, const int* __restrict__ act,
@@ -194,6 +203,7 @@ void launch_leg_tile_summary(const LegPlanView& p, const int* act_dev, int2* til
     const int tot = p.n_m * p.n_tiles;
     leg_tile_summary_kernel<<<(tot + 127) / 128, 128, 0, s>>>(p, act_dev, tile_info_dev,
                                                               useful_dev);
+    count_launch();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -487,6 +497,7 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
     if (phases & LEG_PHASE_ZERO) {
         dim3 zg((p.st.n + 127) / 128, p.n_m);
         leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off);
+        count_launch();
     }
     if (!(phases & LEG_PHASE_MAIN) || p.n_a2m_items == 0) return;
     int dev = 0;
@@ -496,6 +507,7 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
     if (need < blocks) blocks = need;
     if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
     leg_alm2map_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, alm, delta, row_off, counters);
+    count_launch();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -840,6 +852,7 @@ void launch_leg_m2a_finalize(const LegPlanView& p, const int* mis, int n_mis, co
     if (n_mis <= 0) return;
     dim3 grid((p.lmax + 1 + 127) / 128, n_mis);
     leg_m2a_finalize_kernel<<<grid, 128, 0, s>>>(p, mis, scratch, alm, accumulate);
+    count_launch();
 }
 
 // orders without any alive tile: every term is dropped, a_lm = 0 (or unchanged when +=)
@@ -855,7 +868,10 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
                         double2* alm, int accumulate, int* counters, double2* scratch,
                         cudaStream_t s, int phases) {
     if (p.n_m == 0) return;
-    if (!accumulate && (phases & LEG_PHASE_ZERO)) leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
+    if (!accumulate && (phases & LEG_PHASE_ZERO)) {
+        leg_zero_orders_kernel<<<p.n_m, 128, 0, s>>>(p, alm);
+        count_launch();
+    }
     if (!(phases & LEG_PHASE_MAIN) || p.n_m2a_items == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
@@ -867,6 +883,7 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
     if (need < blocks) blocks = need;
     if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
     leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, counters, scratch);
+    count_launch();
     // whole launches reduce every order's slots here; pipelined band launches (defer_final)
     // leave them to the caller, which finalizes each order once its last launch is done
     if (!p.defer_final) launch_leg_m2a_finalize(p, nullptr, p.n_m, scratch, alm, accumulate, s);

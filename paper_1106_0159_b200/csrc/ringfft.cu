@@ -1209,6 +1209,7 @@ void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cud
     for (int j0 = 0; j0 < n_jobs; j0 += 65535) {
         const int nj = n_jobs - j0 < 65535 ? n_jobs - j0 : 65535;
         fill_tables_kernel<<<dim3(16, nj), 256, 0, s>>>(jobs_dev + j0, tabs);
+        count_launch();
     }
 }
 
@@ -1265,6 +1266,7 @@ void synth_c(const RingStageArgs& a, cudaStream_t s) {
         b.rings = a.rings + r0;
         const int nr = a.n_rings - r0 < 65535 ? a.n_rings - r0 : 65535;
         ring_synth_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(a.mmax), s>>>(b);
+        count_launch();
     }
 }
 template <int C>
@@ -1276,6 +1278,7 @@ void anal_c(const RingStageArgs& a, cudaStream_t s) {
         b.rings = a.rings + r0;
         const int nr = a.n_rings - r0 < 65535 ? a.n_rings - r0 : 65535;
         ring_anal_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(a.mmax), s>>>(b);
+        count_launch();
     }
 }
 template <int C>
@@ -1285,6 +1288,7 @@ void blue_c(const RingDesc* descs, int n, double2* tabs, cudaStream_t s) {
     for (int r0 = 0; r0 < n; r0 += 65535) {
         const int nr = n - r0 < 65535 ? n - r0 : 65535;
         bluestein_h_kernel<kThr[C], kBmax[C]><<<nr, kThr[C], class_smem<C>(0), s>>>(descs + r0, tabs);
+        count_launch();
     }
 }
 // power-of-two engine: elements per thread (E, T = M/E threads) and resident CTAs per SM the
@@ -1345,6 +1349,7 @@ void p2_synth(const RingStageArgs& a, cudaStream_t s) {
     auto k = ring_p2_synth_kernel<M, E, MINB, BLUE>;
     const size_t sm = p2_smem<M, E>(a.mmax);
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
+    count_launch();
 }
 template <int M, int E, int MINB, bool BLUE>
 void p2_anal(const RingStageArgs& a, cudaStream_t s) {
@@ -1356,6 +1361,7 @@ void p2_anal(const RingStageArgs& a, cudaStream_t s) {
     auto k = ring_p2_anal_kernel<M, E, MINB, BLUE>;
     const size_t sm = p2_smem<M, E>(a.mmax);
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
+    count_launch();
 }
 // class -> (M, E, resident CTAs per SM, Bluestein)
 template <bool SYN, int M, int E, int MINB, bool BLUE>
@@ -1408,6 +1414,7 @@ void p2c_run(const RingStageArgs& a, cudaStream_t s) {
     }
     if (ncl > a.n_rings) ncl = a.n_rings;
     k<<<2 * ncl, 512, sm, s>>>(a);
+    count_launch();
 }
 }  // namespace
 
@@ -1425,6 +1432,7 @@ void launch_p2c_h(const RingDesc* descs_dev, int n, double2* tabs, const double2
     for (int r0 = 0; r0 < n; r0 += 32767) {
         const int nr = n - r0 < 32767 ? n - r0 : 32767;
         p2c_h_kernel<<<2 * nr, 512, p2c_smem(0), s>>>(descs_dev + r0, tabs, tw_half);
+        count_launch();
     }
 }
 int fft_class_for(int B) {
@@ -1513,10 +1521,12 @@ __global__ void peer_barrier_kernel(PeerFlags fl, int rank, int n, unsigned int 
 
 void launch_peer_barrier(const PeerFlags& flags, int rank, int n, unsigned int epoch, cudaStream_t s) {
     peer_barrier_kernel<<<1, 1, 0, s>>>(flags, rank, n, epoch);
+    count_launch();
 }
 
 void launch_dfma_peak(double* out, int blocks, int threads, int iters, cudaStream_t s) {
     dfma_peak_kernel<<<blocks, threads, 0, s>>>(out, iters);
+    count_launch();
 }
 
 }  // namespace shtk

@@ -970,6 +970,8 @@ const char* shtc_last_error(const shtc_ctx* ctx) {
     return ctx ? ctx->err.c_str() : g_last_error.c_str();
 }
 
+uint64_t shtc_kernel_launches(void) { return (uint64_t)shtk::launch_count(); }
+
 int shtc_device_count(void) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;

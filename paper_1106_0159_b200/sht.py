@@ -786,6 +786,11 @@ def reduce_partials(parts, n_rings: int) -> np.ndarray:
     return out
 
 
+def kernel_launches() -> int:
+    """Kernel launches the library has issued in this process (shtc_kernel_launches)."""
+    return int(lib().shtc_kernel_launches())
+
+
 def device_count() -> int:
     return int(lib().shtc_device_count())
 
