@@ -219,9 +219,9 @@ def run_ours(args):
     if not use_exchange:
         mp = torch.empty(grid.n_pix, dtype=torch.float64, device=dev)
 
-        def step():
-            t1 = ctx.alm2map_dev(alm.data_ptr(), mp.data_ptr(), timing=True)
-            t2 = ctx.map2alm_dev(mp.data_ptr(), alm_out.data_ptr(), timing=True)
+        def step(tm=False):
+            t1 = ctx.alm2map_dev(alm.data_ptr(), mp.data_ptr(), timing=tm)
+            t2 = ctx.map2alm_dev(mp.data_ptr(), alm_out.data_ptr(), timing=tm)
             return t1, t2
         ring_classes = None
     elif args.exchange == "peer":
@@ -242,20 +242,22 @@ def run_ours(args):
         _, sc, _, _, _, _ = sht.exchange_layout(layout, rank)
         exch_bytes = 16 * sum(c for j, c in enumerate(sc) if j != rank)
 
-        def step():
-            t1 = ctx.legendre_alm2map_peer(alm.data_ptr(), timing=True)
+        def step(tm=False):
+            t1 = ctx.legendre_alm2map_peer(alm.data_ptr(), timing=tm)
             xev[0].record(stream)
             px.barrier()
             xev[1].record(stream)
-            t3 = ctx.ring_synthesis_dev(px.recv, mp.data_ptr(), timing=True)
-            t4 = ctx.ring_analysis_peer(mp.data_ptr(), timing=True)
+            t3 = ctx.ring_synthesis_dev(px.recv, mp.data_ptr(), timing=tm)
+            t4 = ctx.ring_analysis_peer(mp.data_ptr(), timing=tm)
             xev[2].record(stream)
             px.barrier()
             xev[3].record(stream)
-            t2 = ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr(), timing=True)
-            t1["fft_ms"] = t3["fft_ms"]
-            t2["fft_ms"] = t4["fft_ms"]
-            exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
+            t2 = ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr(), timing=tm)
+            if tm:
+                t1["fft_ms"] = t3["fft_ms"]
+                t2["fft_ms"] = t4["fft_ms"]
+                torch.cuda.synchronize(dev)
+                exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
             return t1, t2
     else:
         import torch.distributed as dist
@@ -271,20 +273,22 @@ def run_ours(args):
         exch_ms = []
         exch_bytes = 16 * sum(c for j, c in enumerate(send_c) if j != rank)
 
-        def step():
-            t1 = ctx.legendre_alm2map_dev(alm.data_ptr(), send.data_ptr(), timing=True)
+        def step(tm=False):
+            t1 = ctx.legendre_alm2map_dev(alm.data_ptr(), send.data_ptr(), timing=tm)
             xev[0].record(stream)
             dist.all_to_all_single(recv, send, r_split, s_split)
             xev[1].record(stream)
-            t3 = ctx.ring_synthesis_dev(recv.data_ptr(), mp.data_ptr(), timing=True)
-            t4 = ctx.ring_analysis_dev(mp.data_ptr(), recv.data_ptr(), timing=True)
+            t3 = ctx.ring_synthesis_dev(recv.data_ptr(), mp.data_ptr(), timing=tm)
+            t4 = ctx.ring_analysis_dev(mp.data_ptr(), recv.data_ptr(), timing=tm)
             xev[2].record(stream)
             dist.all_to_all_single(send, recv, s_split, r_split)
             xev[3].record(stream)
-            t2 = ctx.legendre_map2alm_dev(send.data_ptr(), alm_out.data_ptr(), timing=True)
-            t1["fft_ms"] = t3["fft_ms"]
-            t2["fft_ms"] = t4["fft_ms"]
-            exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
+            t2 = ctx.legendre_map2alm_dev(send.data_ptr(), alm_out.data_ptr(), timing=tm)
+            if tm:
+                t1["fft_ms"] = t3["fft_ms"]
+                t2["fft_ms"] = t4["fft_ms"]
+                torch.cuda.synchronize(dev)
+                exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
             return t1, t2
 
     for _ in range(args.warmup):
@@ -302,10 +306,8 @@ def run_ours(args):
             dist.barrier()
         ev0.record(stream)
         n_launch0 = sht.kernel_launches()
-        for _ in range(args.steps):
-            t1, t2 = step()
-            leg_s.append(t1["legendre_ms"]); fft_s.append(t1["fft_ms"])
-            leg_a.append(t2["legendre_ms"]); fft_a.append(t2["fft_ms"])
+        for _ in range(args.steps):  # no host synchronisation inside the timed region
+            step()
         ev1.record(stream)
         n_launches = sht.kernel_launches() - n_launch0  # the library's own kernels, timed region
         torch.cuda.synchronize(dev)
@@ -317,6 +319,15 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
+
+    # ---- stage breakdown: separate (untimed) steps with per-stage CUDA events ----
+    for _ in range(max(1, min(args.steps, 5))):
+        t1, t2 = step(True)
+        leg_s.append(t1["legendre_ms"]); fft_s.append(t1["fft_ms"])
+        leg_a.append(t2["legendre_ms"]); fft_a.append(t2["fft_ms"])
+    torch.cuda.synchronize(dev)
+    if use_exchange:
+        dist.barrier()
 
     # ---- end to end through the host-buffer C ABI (pinned host memory) ----
     e2e = None
