@@ -162,6 +162,19 @@ def dist_ready():
         return False
 
 
+def config_tag(nside: int, lmax: int) -> str:
+    """BASELINE.json config label of a (nside, lmax) pair."""
+    tags = {(128, 256): " (C1)", (1024, 2048): " (C2/C3)", (2048, 4096): " (C4)", (4096, 8192): " (C5)"}
+    return tags.get((nside, lmax), "")
+
+
+def l2_note(n_alm: int, n_pix: int, n_rings: int, mmax: int) -> str:
+    mb = lambda b: f"{b / 1e6:.0f} MB"  # noqa: E731
+    sizes = (n_alm * 16, n_pix * 8, n_rings * (mmax + 1) * 16)
+    rel = "larger than" if min(sizes) > 126e6 else "not all larger than"
+    return f"inputs {rel} L2 (a_lm {mb(sizes[0])}, map {mb(sizes[1])}, Delta {mb(sizes[2])})"
+
+
 def run_ours(args):
     import torch
     from paper_1106_0159_b200 import sht
@@ -169,11 +182,20 @@ def run_ours(args):
     ws, rank, local = dist_env()
     if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION"):
         os.environ["NCCL_DEBUG"] = "WARN"  # rank 0 prints exactly one JSON line on stdout
+    # SHT_BENCH_SHARED_GPU=1 (testing the multi-rank path on one GPU): every rank on device 0,
+    # gloo for the control plane (NCCL refuses two ranks on one device); the Delta exchange
+    # is the peer-memory one, which needs no collective
+    shared = os.environ.get("SHT_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+        if args.exchange == "nccl":
+            raise SystemExit("SHT_BENCH_SHARED_GPU=1 needs --exchange peer or none")
+    backend = "gloo" if shared else "nccl"
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        dist.init_process_group(backend, **({} if shared else {"device_id": dev}))
     grid = sht.build_healpix_grid(args.nside)
     lmax = mmax = args.lmax
     ctx = sht.Context(local)
@@ -204,7 +226,7 @@ def run_ours(args):
                 os.environ.update(RANK="0", WORLD_SIZE="1", MASTER_ADDR="127.0.0.1",
                                   MASTER_PORT=str(so.getsockname()[1]))
                 so.close()
-            dist.init_process_group("nccl", device_id=dev)
+            dist.init_process_group(backend, **({} if shared else {"device_id": dev}))
     t0 = time.perf_counter()
     ctx.plan()
     plan_s = time.perf_counter() - t0
@@ -315,7 +337,7 @@ def run_ours(args):
             dist.barrier()
     ms_total = ev0.elapsed_time(ev1)
     if use_exchange:
-        t = torch.tensor([ms_total], dtype=torch.float64, device=dev)
+        t = torch.tensor([ms_total], dtype=torch.float64, device="cpu" if shared else dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
@@ -409,11 +431,11 @@ def run_ours(args):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: Gaussian a_lm (splitmix64 counter stream + Box-Muller, seed 12345); "
                 "map2alm input = the step's alm2map output",
-        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={lmax} (C4)",
+        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={lmax}{config_tag(args.nside, lmax)}",
                    "grid": "healpix-ring", "nside": args.nside, "lmax": lmax, "mmax": mmax,
                    "parallelism": f"m-distributed x{ws}" + {"none": "", "peer": " + fused peer-memory exchange",
                                                             "nccl": " + NCCL all-to-all"}[args.exchange],
-                   "l2": "inputs larger than L2 (a_lm 134 MB, map 403 MB, Delta 537 MB)"},
+                   "l2": l2_note(n_alm, grid.n_pix, grid.n_rings, mmax)},
         "ms_alm2map": ms_a2m, "ms_map2alm": ms_m2a,
         "stages_ms": {"alm2map": {"legendre": leg_s_ms, "fft": float(np.mean(fft_s))},
                       "map2alm": {"legendre": leg_a_ms, "fft": float(np.mean(fft_a))}},
@@ -462,7 +484,7 @@ def run_reference(args):
         "ms_per_step": float(np.median([s["ms_alm2map"] + s["ms_map2alm"] for s in steps])),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic: Gaussian a_lm (seed 12345)",
-        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={args.lmax} (C4)",
+        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={args.lmax}{config_tag(args.nside, args.lmax)}",
                    "sample": cb["sample"]},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -1,0 +1,40 @@
+"""The N > 1 bench path end to end (torchrun, one process per rank, m-distributed plan, fused
+peer-memory exchange, device-side barrier, max-over-ranks timing, one JSON line from rank 0),
+run on the one GPU this environment has: SHT_BENCH_SHARED_GPU=1 puts every rank on device 0
+and uses gloo for the control plane.  The per-rank results are checked bitwise against one
+worker in tests/test_gpu_peer_exchange.py; this test covers the driver's launch sequence."""
+import json
+import os
+import socket
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+
+def _free_port():
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_multirank_shared_gpu(n):
+    env = dict(os.environ, SHT_BENCH_SHARED_GPU="1")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(n),
+           "--steps", "3", "--warmup", "3", "--nside", "128", "--lmax", "256"]
+    r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout[-2000:]
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == n and d["steps"] == 3 and d["ms_per_step"] > 0
+    assert "peer-memory exchange" in d["config"]["parallelism"]
+    assert d["exchange"]["bytes_sent_per_rank_per_transform"] > 0
+    assert d["gpu_launches"] > 0
