@@ -121,6 +121,7 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
                         double2* alm, int accumulate, int* counters, double2* scratch,
                         cudaStream_t s, int phases = LEG_PHASE_ALL);
 int leg_persistent_blocks(int device);
+int leg_m2a_warps(int device);  // resident warps of the persistent map2alm kernel
 // a_lm of the listed order indices from their partial slots (p's item set): slots summed in
 // slot order, scaled by c_l, stored (or added when accumulate) -- one thread per coefficient
 void launch_leg_m2a_finalize(const LegPlanView& p, const int* mis, int n_mis, const double2* scratch,

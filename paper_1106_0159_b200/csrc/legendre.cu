@@ -864,6 +864,17 @@ __global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm)
     for (int i = threadIdx.x; i <= p.lmax - m; i += blockDim.x) out[i] = make_double2(0.0, 0.0);
 }
 
+int leg_m2a_warps(int device) {
+    static int cached[64] = {0};
+    if (device >= 0 && device < 64 && cached[device]) return cached[device];
+    int sms = 148, per = 1;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_map2alm_kernel<LEG_R>, LEG_WARPS * 32, 0);
+    const int v = sms * (per > 0 ? per : 1) * LEG_WARPS;
+    if (device >= 0 && device < 64) cached[device] = v;
+    return v;
+}
+
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
                         double2* alm, int accumulate, int* counters, double2* scratch,
                         cudaStream_t s, int phases) {

@@ -125,6 +125,7 @@ struct LegPlan {
     std::vector<int> m2a_final_off;  // launch j: [m2a_final_off[j], m2a_final_off[j+1])
     LegPlanView view{};
     uint64_t nominal = 0, executed = 0, useful = 0;
+    int m2a_group = LEG_M2A_GROUP;  // tiles per map2alm item of the device-resident set
     double build_ms = 0.0;
 };
 
@@ -457,6 +458,16 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     std::vector<int64_t> slot(n_m), slot_b(n_m);
     int64_t slots = 0, slots_b = 0;
     P.nominal = P.executed = P.prefix_steps = P.checked_steps = P.fast_steps = 0;
+    // tiles per map2alm item of the device-resident set: LEG_M2A_GROUP when the plan has
+    // many items per resident warp (whole transforms), fewer when it has few (one worker's
+    // orders of a multi-GPU partition), where the longest item would set the kernel time
+    int64_t alive_total = 0;
+    for (const int2& ti : info) alive_total += ti.x >= 0;
+    int dev_id = 0;
+    CK(cudaGetDevice(&dev_id));
+    const int g_dev = (int)std::max<int64_t>(
+        1, std::min<int64_t>(LEG_M2A_GROUP, alive_total / (8 * (int64_t)leg_m2a_warps(dev_id))));
+    P.m2a_group = g_dev;
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
         P.nominal += (uint64_t)(n + 1) * ns;
@@ -480,8 +491,8 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
         std::reverse(alive.begin(), alive.end());
         tl.insert(tl.end(), alive.begin(), alive.end());
         tcnt[i] = (int)alive.size();
-        // map2alm items: up to G consecutive alive tiles.  Device-resident set: G =
-        // LEG_M2A_GROUP (fewer partial slots; one launch, so long items only delay its start).
+        // map2alm items: up to G consecutive alive tiles.  Device-resident set: G = g_dev
+        // (fewer partial slots; one launch, so long items only delay its start).
         // Band set: G = m2a_band_group tiles of one pipeline band, so no item outlasts the
         // band's launch.  The two sets sum in different groupings (both deterministic).
         auto group = [&](int G, bool by_band, std::vector<LegItem>& out, int& cnt) {
@@ -493,7 +504,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
                 a = e;
             }
         };
-        group(LEG_M2A_GROUP, false, m2a, per_m[i]);
+        group(g_dev, false, m2a, per_m[i]);
         group(m2a_band_group(), true, m2a_b, per_m_b[i]);
         slot[i] = slots;
         slots += (int64_t)per_m[i] * (n + 1);

@@ -255,6 +255,72 @@ def assign_rings(grid: PixelGrid, n_workers: int):
     return sets
 
 
+def assign_rings_interleaved(grid: PixelGrid, n_workers: int):
+    """Ring sets of the multi-GPU runs: mirror pairs (north k, south R-1-k) dealt round-robin,
+    so every worker gets the same mix of polar-cap and belt rings.  The reference's
+    contiguous blocks (assign_rings) give the polar workers all the small, aliasing cap rings,
+    whose ring stage costs several times the belt rings' per pixel (measured at C4, 8 workers:
+    0.56 against 0.17 ms).  Results are partition-invariant, as in the reference."""
+    r_n = grid.n_rings
+    if n_workers < 1:
+        raise ValueError("assign_rings: n_workers must be >= 1")
+    if r_n < 1:
+        raise ValueError("assign_rings: empty grid")
+    if n_workers == 1:
+        return [list(range(r_n))]
+    if 2 * n_workers > r_n:
+        raise ValueError("assign_rings: n_workers > n_rings/2")
+    h = (r_n + 1) // 2
+    sets = [[] for _ in range(n_workers)]
+    for row in range(h):
+        s = sets[row % n_workers]
+        s.append(row)
+        if r_n - 1 - row != row:
+            s.append(r_n - 1 - row)
+    return [sorted(s) for s in sets]
+
+
+def assign_rings_balanced(grid: PixelGrid, n_workers: int):
+    """Ring sets of the multi-GPU runs: contiguous blocks of mirror pairs, as assign_rings, but
+    of equal ring-stage cost instead of equal ring count.  A ring shorter than the longest
+    (HEALPix polar caps: aliasing folds over many wraps, Bluestein sizes, small latency-bound
+    classes) weighs 3 + 3 (1 - n/n_max)^2 belt rings -- measured at C4 with 8 workers: 0.85 us
+    per ring of the polar-most caps, 0.43-0.58 us for the other caps, 0.14 us per belt ring.
+    Results are partition-invariant, as in the reference."""
+    r_n = grid.n_rings
+    if n_workers < 1:
+        raise ValueError("assign_rings: n_workers must be >= 1")
+    if r_n < 1:
+        raise ValueError("assign_rings: empty grid")
+    if n_workers == 1:
+        return [list(range(r_n))]
+    if 2 * n_workers > r_n:
+        raise ValueError("assign_rings: n_workers > n_rings/2")
+    h = (r_n + 1) // 2
+    nphi = np.asarray(grid.n_phi)
+    top = int(nphi.max())
+    frac = nphi[:h] / top
+    w = np.where(nphi[:h] < top, 3.0 + 3.0 * (1.0 - frac) ** 2, 1.0)
+    cum = np.concatenate([[0.0], np.cumsum(w)])
+    total = cum[-1]
+    sets, row = [], 0
+    for k in range(n_workers):
+        # rows [row, end): cumulative weight up to the k+1-th share, at least one row, and
+        # leave one row for each later worker
+        end = int(np.searchsorted(cum, total * (k + 1) / n_workers, side="left"))
+        end = max(row + 1, min(end, h - (n_workers - 1 - k)))
+        if k == n_workers - 1:
+            end = h
+        s = []
+        for r in range(row, end):
+            s.append(r)
+            if r_n - 1 - r != r:
+                s.append(r_n - 1 - r)
+        sets.append(sorted(s))
+        row = end
+    return sets
+
+
 def thread_partition(m_set, n_threads: int):
     if n_threads <= 0:
         raise ValueError("thread_partition: n_threads must be >= 1")
@@ -286,9 +352,13 @@ class WorkerLayout:
     ring_sets: list
 
     @staticmethod
-    def create(grid: PixelGrid, mmax: int, n_workers: int) -> "WorkerLayout":
+    def create(grid: PixelGrid, mmax: int, n_workers: int, rings: str = "blocks") -> "WorkerLayout":
+        """rings="blocks": the reference's assign_rings; "balanced": assign_rings_balanced (the
+        multi-GPU bench's choice); "interleaved": assign_rings_interleaved."""
         m_sets = [list(range(mmax + 1))] if n_workers == 1 else assign_m(mmax, n_workers)
-        return WorkerLayout(n_workers, mmax, grid.n_rings, m_sets, assign_rings(grid, n_workers))
+        ring_sets = {"blocks": assign_rings, "interleaved": assign_rings_interleaved,
+                     "balanced": assign_rings_balanced}[rings](grid, n_workers)
+        return WorkerLayout(n_workers, mmax, grid.n_rings, m_sets, ring_sets)
 
 
 def exchange_layout(layout: WorkerLayout, rank: int):

@@ -24,8 +24,11 @@ def alltoall(sends, send_counts, recv_counts, W):
     return out
 
 
-@pytest.mark.parametrize("nside,lmax,W", [(8, 16, 1), (8, 16, 2), (16, 40, 3), (64, 128, 4), (128, 256, 8), (256, 512, 1)])
-def test_stage_path_matches_single_worker(nside, lmax, W):
+@pytest.mark.parametrize("nside,lmax,W,rings", [(8, 16, 1, "blocks"), (8, 16, 2, "blocks"), (16, 40, 3, "blocks"),
+                                                 (64, 128, 4, "blocks"), (128, 256, 8, "blocks"),
+                                                 (256, 512, 1, "blocks"), (64, 128, 4, "balanced"),
+                                                 (128, 256, 8, "balanced"), (16, 40, 3, "interleaved")])
+def test_stage_path_matches_single_worker(nside, lmax, W, rings):
     dev = torch.device("cuda", 0)
     grid = sht.build_healpix_grid(nside)
     alm_h = sht.random_alm(lmax, lmax, 99)
@@ -36,7 +39,7 @@ def test_stage_path_matches_single_worker(nside, lmax, W):
     want_map = torch.from_numpy(single.alm2map(alm_h)).to(dev)
     want_alm = single.map2alm(want_map.cpu().numpy())
 
-    layout = sht.WorkerLayout.create(grid, lmax, W)
+    layout = sht.WorkerLayout.create(grid, lmax, W, rings=rings)
     ctxs, metas = [], []
     for w in range(W):
         c = sht.Context(0)

@@ -163,3 +163,20 @@ def test_distributed_synthesis_over_gloo_world_size_2():
     want = O.synthesis(O.random_alm(lmax, lmax, 11), lmax, lmax, grid)
     mp_ = np.concatenate([got[r] for r in range(grid.n_rings)])
     assert np.array_equal(mp_, want)
+
+
+@pytest.mark.parametrize("policy", ["balanced", "interleaved"])
+@pytest.mark.parametrize("nside,W", [(2, 2), (16, 3), (64, 8), (2048, 8)])
+def test_multi_gpu_ring_sets_cover_each_ring_once_mirror_closed(policy, nside, W):
+    g = sht.build_healpix_grid(nside)
+    fn = {"balanced": sht.assign_rings_balanced, "interleaved": sht.assign_rings_interleaved}[policy]
+    sets = fn(g, W)
+    assert len(sets) == W and all(sets)
+    assert sorted(sum(sets, [])) == list(range(g.n_rings))
+    for s in sets:  # mirror pairs stay together (the Legendre streams are mirror pairs)
+        assert set(s) == {g.n_rings - 1 - r for r in s}
+    if policy == "balanced":  # contiguous blocks of north rows, polar blocks shorter
+        norths = [sorted(r for r in s if r <= (g.n_rings - 1) // 2) for s in sets]
+        assert all(b == list(range(b[0], b[-1] + 1)) for b in norths)
+        if nside >= 64:
+            assert len(norths[0]) < len(norths[-1])

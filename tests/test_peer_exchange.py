@@ -76,9 +76,11 @@ def _replay(layout, send, recv, mem):
                 assert sv[row_off[r] + mi] == code(r, m), (i, r, m)
 
 
-@pytest.mark.parametrize("nside,lmax,W", [(2, 5, 1), (4, 12, 2), (4, 12, 3), (8, 16, 4), (4, 9, 5)])
-def test_peer_pointers_deliver_like_the_all_to_all(nside, lmax, W):
-    layout = sht.WorkerLayout.create(sht.build_healpix_grid(nside), lmax, W)
+@pytest.mark.parametrize("nside,lmax,W,rings", [(2, 5, 1, "blocks"), (4, 12, 2, "blocks"), (4, 12, 3, "blocks"),
+                                                 (8, 16, 4, "blocks"), (4, 9, 5, "blocks"), (8, 16, 4, "balanced"),
+                                                 (4, 12, 3, "interleaved")])
+def test_peer_pointers_deliver_like_the_all_to_all(nside, lmax, W, rings):
+    layout = sht.WorkerLayout.create(sht.build_healpix_grid(nside), lmax, W, rings=rings)
     send, recv, mem = _fake_bases(layout)
     _replay(layout, send, recv, mem)
     for buf in mem.values():  # every slot of every exchange buffer written exactly as planned
