@@ -147,6 +147,10 @@ int order_chunks() {
 }
 #define kOrderChunks order_chunks()
 constexpr int kPipeEvents = 128;
+// side streams of the ring stage: each small-ring class launch (latency bound, few CTAs busy)
+// gets its own, so their latencies overlap (a worker's share of polar rings is all small
+// classes)
+constexpr int kFftAux = 6;
 
 struct FftPlan {
     bool built = false;
@@ -209,8 +213,8 @@ struct shtc_ctx {
     cudaEvent_t pev[kPipeEvents] = {};  // ordering events
     cudaEvent_t tev[kPipeEvents] = {};  // timing events
     // ring stage: the small-ring classes run on side streams beside the large ones
-    cudaStream_t fft_aux[2] = {};
-    cudaEvent_t fft_fork = nullptr, fft_join[2] = {};
+    cudaStream_t fft_aux[kFftAux] = {};
+    cudaEvent_t fft_fork = nullptr, fft_join[kFftAux] = {};
 };
 
 namespace {
@@ -842,8 +846,8 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 
 // Ring stage launches of one plan (or of one pipeline band of it).  The large power-of-two
 // classes (buffers >= 2048, the belt and the big polar-cap rings) go on the caller's stream;
-// the small-ring classes (latency bound: few CTAs, aliasing folds over many wraps) run on two
-// side streams at the same time, joined back before the stage ends.
+// the small-ring classes (latency bound: few CTAs, aliasing folds over many wraps) run on
+// kFftAux side streams at the same time, joined back before the stage ends.
 template <class Launch>
 void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launch) {
     if (!c->fft_fork) {
@@ -854,7 +858,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
     if (!F.counters.p) F.counters.ensure(FFT_N_CLASSES * sizeof(int));
     CK(cudaMemsetAsync(F.counters.p, 0, FFT_N_CLASSES * sizeof(int), s));
     CK(cudaEventRecord(c->fft_fork, s));
-    bool used[2] = {false, false};
+    bool used[kFftAux] = {};
     int side = 0;
     for (int k = FFT_N_CLASSES - 1; k >= 0; --k) {
         const int b = range < 0 ? 0 : F.range_start[k][range];
@@ -863,7 +867,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         const bool big = k >= FFT_N_GENERIC && fft_class_bmax(k) >= 2048;
         cudaStream_t st = s;
         if (!big) {
-            const int i = side++ & 1;
+            const int i = side++ % kFftAux;
             if (!used[i]) CK(cudaStreamWaitEvent(c->fft_aux[i], c->fft_fork, 0));
             used[i] = true;
             st = c->fft_aux[i];
@@ -879,7 +883,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         launch(k, a, st);
         CK(cudaGetLastError());
     }
-    for (int i = 0; i < 2; ++i)
+    for (int i = 0; i < kFftAux; ++i)
         if (used[i]) {
             CK(cudaEventRecord(c->fft_join[i], c->fft_aux[i]));
             CK(cudaStreamWaitEvent(s, c->fft_join[i], 0));

@@ -16,6 +16,7 @@ std::invalid_argument maps to ValueError, std::domain_error to ArithmeticError.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import math
 from dataclasses import dataclass, field
 
@@ -280,12 +281,15 @@ def assign_rings_interleaved(grid: PixelGrid, n_workers: int):
     return [sorted(s) for s in sets]
 
 
+CAP_WEIGHT = float(os.environ.get("SHT_CAP_WEIGHT", "3.0"))
+
+
 def assign_rings_balanced(grid: PixelGrid, n_workers: int):
     """Ring sets of the multi-GPU runs: contiguous blocks of mirror pairs, as assign_rings, but
     of equal ring-stage cost instead of equal ring count.  A ring shorter than the longest
     (HEALPix polar caps: aliasing folds over many wraps, Bluestein sizes, small latency-bound
-    classes) weighs 3 + 3 (1 - n/n_max)^2 belt rings -- measured at C4 with 8 workers: 0.85 us
-    per ring of the polar-most caps, 0.43-0.58 us for the other caps, 0.14 us per belt ring.
+    classes) weighs CAP_WEIGHT = 3 belt rings -- measured at C4 with 8 workers: 0.34-0.59 us
+    per cap ring, 0.14-0.24 us per belt ring.
     Results are partition-invariant, as in the reference."""
     r_n = grid.n_rings
     if n_workers < 1:
@@ -299,8 +303,7 @@ def assign_rings_balanced(grid: PixelGrid, n_workers: int):
     h = (r_n + 1) // 2
     nphi = np.asarray(grid.n_phi)
     top = int(nphi.max())
-    frac = nphi[:h] / top
-    w = np.where(nphi[:h] < top, 3.0 + 3.0 * (1.0 - frac) ** 2, 1.0)
+    w = np.where(nphi[:h] < top, CAP_WEIGHT, 1.0)
     cum = np.concatenate([[0.0], np.cumsum(w)])
     total = cum[-1]
     sets, row = [], 0
