@@ -151,6 +151,15 @@ constexpr int kPipeEvents = 128;
 // gets its own, so their latencies overlap (a worker's share of polar rings is all small
 // classes)
 constexpr int kFftAux = 6;
+// SHTC_FFT_AUX overrides the count (1..kFftAux).  Tests that run several workers' contexts in
+// one process with device-side barriers use fewer, so that every context's streams keep their
+// own hardware queue (CUDA_DEVICE_MAX_CONNECTIONS <= 32): a spinning barrier kernel must never
+// share a queue with another worker's pending kernel
+int fft_aux_count() {
+    static const int n = std::getenv("SHTC_FFT_AUX") ? std::min(kFftAux, std::max(1, std::atoi(std::getenv("SHTC_FFT_AUX"))))
+                                                      : kFftAux;
+    return n;
+}
 
 struct FftPlan {
     bool built = false;
@@ -851,7 +860,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 template <class Launch>
 void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launch) {
     if (!c->fft_fork) {
-        for (auto& st : c->fft_aux) CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        for (int i = 0; i < fft_aux_count(); ++i) CK(cudaStreamCreateWithFlags(&c->fft_aux[i], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->fft_fork, cudaEventDisableTiming));
         for (auto& e : c->fft_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
@@ -867,7 +876,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         const bool big = k >= FFT_N_GENERIC && fft_class_bmax(k) >= 2048;
         cudaStream_t st = s;
         if (!big) {
-            const int i = side++ % kFftAux;
+            const int i = side++ % fft_aux_count();
             if (!used[i]) CK(cudaStreamWaitEvent(c->fft_aux[i], c->fft_fork, 0));
             used[i] = true;
             st = c->fft_aux[i];

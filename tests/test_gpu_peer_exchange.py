@@ -76,6 +76,7 @@ def _one_process(nside, lmax, W, q):
 def test_fused_exchange_one_process(nside, lmax, W):
     import torch.multiprocessing as mp
     os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"  # inherited by the spawned process
+    os.environ["SHTC_FFT_AUX"] = "2"  # W contexts x 3 ring-stage streams stay within 32 queues
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
@@ -85,6 +86,7 @@ def test_fused_exchange_one_process(nside, lmax, W):
         p.join(timeout=60)
     finally:
         os.environ.pop("CUDA_DEVICE_MAX_CONNECTIONS", None)
+        os.environ.pop("SHTC_FFT_AUX", None)
     assert status == "ok", res
     assert all(res), res
     assert p.exitcode == 0
