@@ -18,6 +18,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <thread>
 #include <functional>
 #include <vector>
 
@@ -44,6 +45,63 @@ void cuda_check(cudaError_t e, const char* what) {
              std::string(what) + ": " + cudaGetErrorString(e));
 }
 #define CK(x) cuda_check((x), #x)
+
+// Page-locked host staging buffer (cudaHostAlloc), grown on demand and kept by the context.
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    PinnedBuf() = default;
+    PinnedBuf(const PinnedBuf&) = delete;
+    PinnedBuf& operator=(const PinnedBuf&) = delete;
+    ~PinnedBuf() { release(); }
+    void release() {
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    void ensure(size_t b) {
+        if (b <= bytes && p) return;
+        release();
+        CK(cudaHostAlloc(&p, b ? b : 16, cudaHostAllocDefault));
+        bytes = b;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+// host memory the copy engines can read / write directly (cudaHostAlloc, cudaHostRegister,
+// pinned torch tensors); pageable memory (std::vector, numpy) goes through PinnedBuf staging
+bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// memcpy on all host cores (pageable <-> staging copies are bound by host memory bandwidth)
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    static const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    const size_t min_piece = size_t(4) << 20;
+    const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(hw, bytes / min_piece));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t piece = (bytes / nt + 63) & ~size_t(63);
+    std::vector<std::thread> th;
+    th.reserve(nt - 1);
+    for (unsigned i = 1; i < nt; ++i) {
+        const size_t b = std::min(bytes, piece * i), e = std::min(bytes, piece * (i + 1));
+        if (e > b)
+            th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b); });
+    }
+    std::memcpy(dst, src, std::min(bytes, piece));
+    for (auto& t : th) t.join();
+}
 
 struct DevBuf {
     void* p = nullptr;
@@ -215,6 +273,7 @@ struct shtc_ctx {
     std::vector<double> op_x;
     // scratch
     DevBuf delta, alm_buf, map_buf, stats;
+    PinnedBuf stage_alm, stage_map;  // staging of pageable host buffers (host-buffer entry points)
     cudaEvent_t ev[8] = {};
     // pipelined host-buffer paths: copy streams, two Legendre streams (consecutive launches
     // alternate so one launch's tail overlaps the next) and a high-priority ring-stage stream
@@ -1275,24 +1334,24 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         const int64_t* ro = ctx->id_row_off.as<int64_t>();
         const int n_m = (int)ctx->ms.size();
         int* queues = P.counters.as<int>() + 1 + n_m;  // one word per launch
+        // pageable host buffers (the C++ drop-in's std::vectors) go through page-locked
+        // staging: a_lm chunks are copied in on all host cores just before their H2D, band
+        // pixels are copied out as each band's D2H completes, both overlapping the GPU work
+        const bool in_pinned = host_pinned(alm), out_pinned = host_pinned(map);
+        const double2* alm_src = reinterpret_cast<const double2*>(alm);
+        if (!in_pinned) {
+            ctx->stage_alm.ensure(na);
+            alm_src = ctx->stage_alm.as<double2>();
+        }
+        double* map_dst = map;
+        if (!out_pinned) {
+            ctx->stage_map.ensure(nb);
+            map_dst = ctx->stage_map.as<double>();
+        }
         PipeEvents E{ctx};
         if (!P.a2m_launch.empty())
             CK(cudaMemsetAsync(queues, 0, P.a2m_launch.size() * sizeof(int), ctx->stream));
         pipe_fork(ctx);
-        // a_lm by order chunk
-        std::vector<cudaEvent_t> h_chunk(kOrderChunks);
-        const int th = E.timed(ctx->h2d, [&] {
-            for (int k = 0; k < kOrderChunks; ++k) {
-                auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
-                if (e > b)
-                    CK(cudaMemcpyAsync(ab + b, reinterpret_cast<const double2*>(alm) + b,
-                                       (e - b) * sizeof(double2), cudaMemcpyHostToDevice, ctx->h2d));
-                h_chunk[k] = E.order(ctx->h2d);
-            }
-        });
-        // dead tiles' Delta rows (disjoint from every launch's rows) ahead of the ring stage
-        launch_leg_alm2map(P.view, ab, dl, ro, P.counters.as<int>(), ctx->fst, LEG_PHASE_ZERO);
-        CK(cudaGetLastError());
         // SHTC_PIPE_MODE (experiments): 2 (default) = everything on one stream, band by band (the
         // ring synthesis needs whole SMs, which a running persistent Legendre launch never
         // frees); 0 = Legendre launches run ahead on two streams (measured slower)
@@ -1300,40 +1359,72 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         std::vector<int> t_leg, t_fft;
         std::vector<std::pair<const char*, int>> segs;
         int t_d2h_first = -1;
-        // band order: the head bands at the equator first (their launches run by order chunk
-        // while a_lm arrives), then from the pole back toward the equator, so the last band
-        // before the final copy has the cheap belt-ring synthesis (SHTC_A2M_ORDER=0: ascending)
+        std::vector<std::vector<size_t>> band_launches(kPipeBands);
+        for (size_t q = 0; q < P.a2m_launch.size(); ++q) band_launches[P.a2m_launch[q].tc].push_back(q);
+        std::vector<cudaEvent_t> band_done(kPipeBands);
+        auto leg_launch = [&](size_t j, cudaEvent_t ready) {
+            const auto& L = P.a2m_launch[j];
+            cudaStream_t st = mode == 2 ? ctx->fst : ctx->lst[j & 1];
+            CK(cudaStreamWaitEvent(st, ready, 0));
+            t_leg.push_back(E.timed(st, [&] {
+                launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, dl, ro, queues + j, st,
+                                   LEG_PHASE_MAIN | LEG_PHASE_NO_RESET);
+                CK(cudaGetLastError());
+            }));
+            if (st != ctx->fst) CK(cudaStreamWaitEvent(ctx->fst, E.order(st), 0));
+        };
+        // dead tiles' Delta rows (disjoint from every launch's rows) ahead of the ring stage
+        launch_leg_alm2map(P.view, ab, dl, ro, P.counters.as<int>(), ctx->fst, LEG_PHASE_ZERO);
+        CK(cudaGetLastError());
+        // a_lm by order chunk; the head bands' launches of chunk k follow its copy
+        std::vector<cudaEvent_t> h_chunk(kOrderChunks);
+        int th = -1, th_last = -1;
+        for (int k = 0; k < kOrderChunks; ++k) {
+            auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
+            if (!in_pinned && e > b)
+                par_memcpy(ctx->stage_alm.as<double2>() + b, reinterpret_cast<const double2*>(alm) + b,
+                           (e - b) * sizeof(double2));
+            const int ti = E.timed(ctx->h2d, [&] {
+                if (e > b)
+                    CK(cudaMemcpyAsync(ab + b, alm_src + b, (e - b) * sizeof(double2), cudaMemcpyHostToDevice,
+                                       ctx->h2d));
+            });
+            if (th < 0) th = ti;
+            th_last = ti;
+            h_chunk[k] = E.order(ctx->h2d);
+            for (size_t j : band_launches[0])
+                if (P.a2m_launch[j].mc == k) leg_launch(j, h_chunk[k]);
+        }
+        // band order: the head bands at the equator first (their launches ran by order chunk
+        // above), then from the pole back toward the equator, so the last band before the
+        // final copy has the cheap belt-ring synthesis (SHTC_A2M_ORDER=0: ascending)
         static const bool polar_early = !std::getenv("SHTC_A2M_ORDER") || std::atoi(std::getenv("SHTC_A2M_ORDER"));
         const int nh = a2m_head_bands();
         std::vector<int> band_order(kPipeBands);
         for (int k = 0; k < kPipeBands; ++k) band_order[k] = (!polar_early || k < nh) ? k : kPipeBands - 1 - (k - nh);
-        std::vector<std::vector<size_t>> band_launches(kPipeBands);
-        for (size_t q = 0; q < P.a2m_launch.size(); ++q) band_launches[P.a2m_launch[q].tc].push_back(q);
+        std::vector<int> copied;  // bands whose pixels go down, in order
         for (int tc : band_order) {
-            std::vector<cudaEvent_t> band_done;
-            for (size_t j : band_launches[tc]) {
-                const auto& L = P.a2m_launch[j];
-                cudaStream_t st = mode == 2 ? ctx->fst : ctx->lst[j & 1];
-                CK(cudaStreamWaitEvent(st, h_chunk[L.tc == 0 ? L.mc : kOrderChunks - 1], 0));
-                t_leg.push_back(E.timed(st, [&] {
-                    launch_leg_alm2map(items_view(P, L.begin, L.end, true), ab, dl, ro, queues + j, st,
-                                       LEG_PHASE_MAIN | LEG_PHASE_NO_RESET);
-                    CK(cudaGetLastError());
-                }));
-                if (st != ctx->fst) band_done.push_back(E.order(st));
-            }
-            if (F.band_pix[tc].empty() && band_done.empty()) continue;
-            for (cudaEvent_t e : band_done) CK(cudaStreamWaitEvent(ctx->fst, e, 0));
+            if (tc != 0)
+                for (size_t j : band_launches[tc]) leg_launch(j, h_chunk[kOrderChunks - 1]);
+            if (F.band_pix[tc].empty() && band_launches[tc].empty()) continue;
             t_fft.push_back(E.timed(ctx->fst, [&] { run_ring_synth(ctx, F, dl, mb, nullptr, nullptr, tc, ctx->fst); }));
             CK(cudaStreamWaitEvent(ctx->d2h, E.order(ctx->fst), 0));
             const int ti = E.timed(ctx->d2h, [&] {
                 for (const auto& iv : F.band_pix[tc])
-                    CK(cudaMemcpyAsync(map + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
+                    CK(cudaMemcpyAsync(map_dst + iv.first, mb + iv.first, (iv.second - iv.first) * sizeof(double),
                                        cudaMemcpyDeviceToHost, ctx->d2h));
             });
+            band_done[tc] = E.order(ctx->d2h);
+            copied.push_back(tc);
             if (t_d2h_first < 0) t_d2h_first = ti;
             segs.push_back({"D", ti});
         }
+        if (!out_pinned)
+            for (int tc : copied) {
+                CK(cudaEventSynchronize(band_done[tc]));
+                for (const auto& iv : F.band_pix[tc])
+                    par_memcpy(map + iv.first, map_dst + iv.first, (iv.second - iv.first) * sizeof(double));
+            }
         pipe_join(ctx);
         {
             for (int i : t_leg) segs.push_back({"L", i});
@@ -1345,7 +1436,8 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
             for (int i : t_leg) leg += E.span(i);
             for (int i : t_fft) fft += E.span(i);
             const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
-            fill_timing(t, leg, fft, E.span(th), d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
+            const float h2d = th < 0 ? 0.f : elapsed(ctx->tev[th], ctx->tev[th_last + 1]);
+            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }
@@ -1371,19 +1463,39 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         const int n_m = (int)ctx->ms.size();
         double2* ab = ctx->alm_buf.as<double2>();
         int* queues = P.counters.as<int>() + 1 + n_m + P.a2m_launch.size();  // one word per launch
+        // pageable host buffers go through page-locked staging (see shtc_alm2map): each band's
+        // pixels are copied in on all host cores just before its H2D, each launch's final
+        // orders are copied out as their D2H completes
+        const bool in_pinned = host_pinned(map), out_pinned = host_pinned(alm);
+        const double* map_src = map;
+        if (!in_pinned) {
+            ctx->stage_map.ensure(nb);
+            map_src = ctx->stage_map.as<double>();
+        }
+        double2* alm_dst = reinterpret_cast<double2*>(alm);
+        if (!out_pinned) {
+            ctx->stage_alm.ensure(na);
+            alm_dst = ctx->stage_alm.as<double2>();
+        }
         PipeEvents E{ctx};
         if (!P.m2a_launch.empty())
             CK(cudaMemsetAsync(queues, 0, P.m2a_launch.size() * sizeof(int), ctx->stream));
         pipe_fork(ctx);
-        std::vector<cudaEvent_t> h_band(kPipeBands);
-        const int th = E.timed(ctx->h2d, [&] {
-            for (int tc = 0; tc < kPipeBands; ++tc) {
+        int th = -1, th_last = -1;
+        auto band_h2d = [&](int tc) {
+            if (!in_pinned)
                 for (const auto& iv : F.band_pix[tc])
-                    CK(cudaMemcpyAsync(mb + iv.first, map + iv.first, (iv.second - iv.first) * sizeof(double),
+                    par_memcpy(ctx->stage_map.as<double>() + iv.first, map + iv.first,
+                               (iv.second - iv.first) * sizeof(double));
+            const int ti = E.timed(ctx->h2d, [&] {
+                for (const auto& iv : F.band_pix[tc])
+                    CK(cudaMemcpyAsync(mb + iv.first, map_src + iv.first, (iv.second - iv.first) * sizeof(double),
                                        cudaMemcpyHostToDevice, ctx->h2d));
-                h_band[tc] = E.order(ctx->h2d);
-            }
-        });
+            });
+            if (th < 0) th = ti;
+            th_last = ti;
+            return E.order(ctx->h2d);
+        };
         // SHTC_M2A_MODE (experiments): 0 (default) = Legendre launches alternate over two
         // streams (one launch's tail overlaps the next) beside the high-priority ring analysis;
         // 2 = analysis and launches band by band on one stream (measured slower: 14.0 against
@@ -1398,15 +1510,17 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         std::vector<std::pair<const char*, int>> segs;
         int t_d2h_first = -1;
         cudaEvent_t prev = nullptr;
+        std::vector<std::pair<int, cudaEvent_t>> d2h_done;  // (launch, its copies done)
         auto copy_final = [&](int j) {
             const int ti = E.timed(ctx->d2h, [&] {
                 for (const auto& run : P.m2a_done[j]) {
                     auto [b, e] = alm_span(ctx, run.first, run.second);
                     if (e > b)
-                        CK(cudaMemcpyAsync(reinterpret_cast<double2*>(alm) + b, ab + b, (e - b) * sizeof(double2),
-                                           cudaMemcpyDeviceToHost, ctx->d2h));
+                        CK(cudaMemcpyAsync(alm_dst + b, ab + b, (e - b) * sizeof(double2), cudaMemcpyDeviceToHost,
+                                           ctx->d2h));
                 }
             });
+            d2h_done.push_back({j, E.order(ctx->d2h)});
             if (t_d2h_first < 0) t_d2h_first = ti;
             segs.push_back({"D", ti});
         };
@@ -1416,7 +1530,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
         }
         size_t j = 0;
         for (int tc = 0; tc < kPipeBands; ++tc) {
-            CK(cudaStreamWaitEvent(ctx->fst, h_band[tc], 0));
+            CK(cudaStreamWaitEvent(ctx->fst, band_h2d(tc), 0));
             t_fft.push_back(E.timed(ctx->fst, [&] { run_ring_anal(ctx, F, mb, dl, nullptr, nullptr, tc, nullptr, ctx->fst); }));
             cudaEvent_t anal_done = serial ? nullptr : E.order(ctx->fst);
             for (; j < P.m2a_launch.size() && P.m2a_launch[j].tc == tc; ++j) {
@@ -1440,6 +1554,15 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
                 copy_final((int)j);
             }
         }
+        if (!out_pinned)
+            for (const auto& [jj, ev] : d2h_done) {
+                CK(cudaEventSynchronize(ev));
+                for (const auto& run : P.m2a_done[jj]) {
+                    auto [b, e] = alm_span(ctx, run.first, run.second);
+                    if (e > b)
+                        par_memcpy(reinterpret_cast<double2*>(alm) + b, alm_dst + b, (e - b) * sizeof(double2));
+                }
+            }
         pipe_join(ctx);
         {
             for (int i : t_leg) segs.push_back({"L", i});
@@ -1451,7 +1574,8 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
             for (int i : t_leg) leg += E.span(i);
             for (int i : t_fft) fft += E.span(i);
             const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
-            fill_timing(t, leg, fft, E.span(th), d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
+            const float h2d = th < 0 ? 0.f : elapsed(ctx->tev[th], ctx->tev[th_last + 1]);
+            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
         }
     });
 }

@@ -49,9 +49,16 @@ ctx = sht.Context(0)
 ctx.set_grid(g)
 ctx.set_band(lmax, lmax)
 ctx.plan()
-alm = torch.from_numpy(sht.gaussian_alm(lmax, lmax, 12345).view(np.float64)).pin_memory().numpy().view(np.complex128)
-mp = torch.empty(g.n_pix, dtype=torch.float64).pin_memory().numpy()
-back = torch.empty(2 * na, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
+if os.environ.get("E2E_PAGEABLE") == "1":  # plain numpy buffers, as the C++ drop-in's std::vectors
+    alm = sht.gaussian_alm(lmax, lmax, 12345)
+    mp = np.empty(g.n_pix)
+    back = np.empty(na, np.complex128)
+    mp.fill(0.0)
+    back.fill(0.0)
+else:
+    alm = torch.from_numpy(sht.gaussian_alm(lmax, lmax, 12345).view(np.float64)).pin_memory().numpy().view(np.complex128)
+    mp = torch.empty(g.n_pix, dtype=torch.float64).pin_memory().numpy()
+    back = torch.empty(2 * na, dtype=torch.float64).pin_memory().numpy().view(np.complex128)
 for it in range(int(os.environ.get("E2E_ITERS", 4))):
     t0 = time.perf_counter()
     _, t1 = ctx.alm2map(alm, out=mp, timing=True)
