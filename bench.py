@@ -240,14 +240,31 @@ def run_ours(args):
     exch_ms, exch_bytes = [], 0
 
     use_exchange = args.exchange != "none"
+    # Every step records CUDA events on the shared stream between its stages (no host
+    # synchronisation): [start, Legendre alm2map, (exchange), ring synthesis, ring analysis,
+    # (exchange), Legendre map2alm].  The stage times of the timed steps come from them.
+    mark = lambda evs, k: evs[k].record(stream) if evs is not None else None  # noqa: E731
     if not use_exchange:
         mp = torch.empty(grid.n_pix, dtype=torch.float64, device=dev)
+        # the whole-transform kernels through the stage entry points (identity layout: the
+        # same launches as shtc_alm2map_dev / shtc_map2alm_dev), Delta in its own buffer
+        delta = torch.empty(2 * grid.n_rings * (mmax + 1), dtype=torch.float64, device=dev)
+        n_marks = 5
 
-        def step(tm=False):
-            t1 = ctx.alm2map_dev(alm.data_ptr(), mp.data_ptr(), timing=tm)
-            t2 = ctx.map2alm_dev(mp.data_ptr(), alm_out.data_ptr(), timing=tm)
-            return t1, t2
-        ring_classes = None
+        def step(evs=None):
+            mark(evs, 0)
+            ctx.legendre_alm2map_dev(alm.data_ptr(), delta.data_ptr())
+            mark(evs, 1)
+            ctx.ring_synthesis_dev(delta.data_ptr(), mp.data_ptr())
+            mark(evs, 2)
+            ctx.ring_analysis_dev(mp.data_ptr(), delta.data_ptr())
+            mark(evs, 3)
+            ctx.legendre_map2alm_dev(delta.data_ptr(), alm_out.data_ptr())
+            mark(evs, 4)
+
+        def stages(evs):  # legendre a2m, fft synth, fft anal, legendre m2a, exchange
+            return (evs[0].elapsed_time(evs[1]), evs[1].elapsed_time(evs[2]), evs[2].elapsed_time(evs[3]),
+                    evs[3].elapsed_time(evs[4]), 0.0)
     elif args.exchange == "peer":
         # fused exchange: the Legendre (alm2map) and ring-analysis (map2alm) kernels store
         # Delta straight into the consumers' buffers over NVLink (CUDA IPC peer mappings),
@@ -261,28 +278,28 @@ def run_ours(args):
         px = sht.PeerExchange(ctx, layout, rank, all_gather=all_gather)
         send_c, recv_c = sht.exchange_sizes(layout, rank)
         mp = torch.zeros(grid.n_pix, dtype=torch.float64, device=dev)
-        xev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        exch_ms = []
         _, sc, _, _, _, _ = sht.exchange_layout(layout, rank)
         exch_bytes = 16 * sum(c for j, c in enumerate(sc) if j != rank)
+        n_marks = 7
 
-        def step(tm=False):
-            t1 = ctx.legendre_alm2map_peer(alm.data_ptr(), timing=tm)
-            xev[0].record(stream)
+        def step(evs=None):
+            mark(evs, 0)
+            ctx.legendre_alm2map_peer(alm.data_ptr())
+            mark(evs, 1)
             px.barrier()
-            xev[1].record(stream)
-            t3 = ctx.ring_synthesis_dev(px.recv, mp.data_ptr(), timing=tm)
-            t4 = ctx.ring_analysis_peer(mp.data_ptr(), timing=tm)
-            xev[2].record(stream)
+            mark(evs, 2)
+            ctx.ring_synthesis_dev(px.recv, mp.data_ptr())
+            mark(evs, 3)
+            ctx.ring_analysis_peer(mp.data_ptr())
+            mark(evs, 4)
             px.barrier()
-            xev[3].record(stream)
-            t2 = ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr(), timing=tm)
-            if tm:
-                t1["fft_ms"] = t3["fft_ms"]
-                t2["fft_ms"] = t4["fft_ms"]
-                torch.cuda.synchronize(dev)
-                exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
-            return t1, t2
+            mark(evs, 5)
+            ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr())
+            mark(evs, 6)
+
+        def stages(evs):
+            return (evs[0].elapsed_time(evs[1]), evs[2].elapsed_time(evs[3]), evs[3].elapsed_time(evs[4]),
+                    evs[5].elapsed_time(evs[6]), evs[1].elapsed_time(evs[2]) + evs[4].elapsed_time(evs[5]))
     else:
         import torch.distributed as dist
         row_off, send_c, recv_c, ring_list, m_base, m_stride = sht.exchange_layout(layout, rank)
@@ -292,28 +309,27 @@ def run_ours(args):
         mp = torch.zeros(grid.n_pix, dtype=torch.float64, device=dev)
         s_split = [2 * c for c in send_c]
         r_split = [2 * c for c in recv_c]
-
-        xev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        exch_ms = []
         exch_bytes = 16 * sum(c for j, c in enumerate(send_c) if j != rank)
+        n_marks = 7
 
-        def step(tm=False):
-            t1 = ctx.legendre_alm2map_dev(alm.data_ptr(), send.data_ptr(), timing=tm)
-            xev[0].record(stream)
+        def step(evs=None):
+            mark(evs, 0)
+            ctx.legendre_alm2map_dev(alm.data_ptr(), send.data_ptr())
+            mark(evs, 1)
             dist.all_to_all_single(recv, send, r_split, s_split)
-            xev[1].record(stream)
-            t3 = ctx.ring_synthesis_dev(recv.data_ptr(), mp.data_ptr(), timing=tm)
-            t4 = ctx.ring_analysis_dev(mp.data_ptr(), recv.data_ptr(), timing=tm)
-            xev[2].record(stream)
+            mark(evs, 2)
+            ctx.ring_synthesis_dev(recv.data_ptr(), mp.data_ptr())
+            mark(evs, 3)
+            ctx.ring_analysis_dev(mp.data_ptr(), recv.data_ptr())
+            mark(evs, 4)
             dist.all_to_all_single(send, recv, s_split, r_split)
-            xev[3].record(stream)
-            t2 = ctx.legendre_map2alm_dev(send.data_ptr(), alm_out.data_ptr(), timing=tm)
-            if tm:
-                t1["fft_ms"] = t3["fft_ms"]
-                t2["fft_ms"] = t4["fft_ms"]
-                torch.cuda.synchronize(dev)
-                exch_ms.append(xev[0].elapsed_time(xev[1]) + xev[2].elapsed_time(xev[3]))
-            return t1, t2
+            mark(evs, 5)
+            ctx.legendre_map2alm_dev(send.data_ptr(), alm_out.data_ptr())
+            mark(evs, 6)
+
+        def stages(evs):
+            return (evs[0].elapsed_time(evs[1]), evs[2].elapsed_time(evs[3]), evs[3].elapsed_time(evs[4]),
+                    evs[5].elapsed_time(evs[6]), evs[1].elapsed_time(evs[2]) + evs[4].elapsed_time(evs[5]))
 
     for _ in range(args.warmup):
         step()
@@ -323,15 +339,15 @@ def run_ours(args):
         dist.barrier()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
-    leg_a, leg_s, fft_a, fft_s = [], [], [], []
+    step_evs = [[torch.cuda.Event(enable_timing=True) for _ in range(n_marks)] for _ in range(args.steps)]
     with ClockSampler(local) as clk:
         torch.cuda.synchronize(dev)
         if use_exchange:
             dist.barrier()
         ev0.record(stream)
         n_launch0 = sht.kernel_launches()
-        for _ in range(args.steps):  # no host synchronisation inside the timed region
-            step()
+        for i in range(args.steps):  # no host synchronisation inside the timed region
+            step(step_evs[i])
         ev1.record(stream)
         n_launches = sht.kernel_launches() - n_launch0  # the library's own kernels, timed region
         torch.cuda.synchronize(dev)
@@ -344,14 +360,9 @@ def run_ours(args):
         ms_total = float(t.item())
     ms_step = ms_total / args.steps
 
-    # ---- stage breakdown: separate (untimed) steps with per-stage CUDA events ----
-    for _ in range(max(1, min(args.steps, 5))):
-        t1, t2 = step(True)
-        leg_s.append(t1["legendre_ms"]); fft_s.append(t1["fft_ms"])
-        leg_a.append(t2["legendre_ms"]); fft_a.append(t2["fft_ms"])
-    torch.cuda.synchronize(dev)
-    if use_exchange:
-        dist.barrier()
+    # ---- stage times of the timed steps (their events, read after the region) ----
+    st = np.array([stages(evs) for evs in step_evs])  # steps x (leg a2m, synth, anal, leg m2a, exch)
+    leg_s, fft_s, fft_a, leg_a, exch_ms = st[:, 0], st[:, 1], st[:, 2], st[:, 3], list(st[:, 4])
 
     # ---- end to end through the host-buffer C ABI (pinned host memory) ----
     e2e = None
