@@ -537,6 +537,26 @@ __device__ __forceinline__ const RingDesc& desc_at(const RingStageArgs& a, int r
 
 // Persistent CTAs pull rings from a queue and transform one ring at a time (the ring in
 // registers + one padded shared-memory exchange buffer).
+#ifdef P2_PROF
+// phase-timing instrumentation of the synthesis engine (tuning builds only, tools/p2prof.py):
+// thread 0's clock64() deltas per phase, summed per (class, phase); slot 15 counts rings
+__device__ unsigned long long g_p2prof[16][16];
+template <int M, bool BLUE>
+__device__ __forceinline__ int p2prof_slot() { return (BLUE ? 8 : 0) + p2_ilog2(M) - 8; }
+#define P2T(i)                                                                                    \
+    do {                                                                                          \
+        if (t == 0) {                                                                             \
+            const long long now = clock64();                                                      \
+            atomicAdd(&g_p2prof[p2prof_slot<M, BLUE>()][i], (unsigned long long)(now - p2t_));   \
+            p2t_ = now;                                                                           \
+        }                                                                                         \
+    } while (0)
+#define P2T_START long long p2t_ = clock64()
+#else
+#define P2T(i)
+#define P2T_START
+#endif
+
 template <int M, int E, int MINB, bool BLUE>
 __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArgs a) {
     constexpr int T = M / E;
@@ -558,6 +578,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
         // while this ring is transformed
         const int ri = s_ri;
         if (ri >= a.n_rings) break;
+        P2T_START;
         int nxt = 0;
         if (t == 0) nxt = atomicAdd(a.counter, 1);
         p2_prefetch_ring<M, T, true>(a, ri + gridDim.x);
@@ -571,6 +592,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
                 __syncthreads();
             }
+            P2T(0);
             // fold (ring_synthesis_into's bins, fourier.cpp:17-25): H_k for 0 <= k <= N, terms
             // in ascending m as the reference adds them.  k = N of a direct ring (N == M) is an
             // extra slot of thread 0 in the last batch.
@@ -637,7 +659,9 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                         if (kk[u] <= N) buf[p2pad(kk[u])] = h[u];
                 }
             }
+            P2T(1);
             __syncthreads();
+            P2T(2);
             // Z_k = (H_k + conj H_{N-k}) + i (H_k - conj H_{N-k}) e^{+2 pi i k/n}: the C2R of
             // length n as a complex inverse FFT of length N (chirped for Bluestein)
             const double2* __restrict__ hw = a.tabs + d.hw_off;
@@ -656,12 +680,16 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 if constexpr (BLUE) z = cmul(z, cconj(c));
                 v[j] = (k < N) ? z : make_double2(0.0, 0.0);
             }
+            P2T(3);
         }
         __syncthreads();  // H is read before the first pass overwrites buf
+        P2T(4);
         if constexpr (!BLUE) {
             p2_fft<M, E, +1>(v, buf, tws);
+            P2T(5);
         } else {
             p2_fft<M, E, -1>(v, buf, tws);
+            P2T(5);
             // fences keep ptxas from hoisting the table loads into the FFT passes
             __threadfence_block();
             {
@@ -669,7 +697,9 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], cconj(__ldg(&H[t + T * j])));
             }
+            P2T(6);
             p2_fft<M, E, +1>(v, buf, tws);
+            P2T(7);
             __threadfence_block();
             const RingDesc& d = desc_at(a, ri);
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
@@ -681,6 +711,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 const double2 c = __ldg(&chirp[k < N ? k : 0]);
                 v[j] = cscale(cmul(v[j], cconj(c)), inv);  // k >= N: not stored
             }
+            P2T(8);
         }
         {
             const RingDesc& d = desc_at(a, ri);
@@ -705,8 +736,13 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 }
             }
         }
+        P2T(9);
         if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
         __syncthreads();  // buf / phase table / s_ri reuse by the next ring
+        P2T(10);
+#ifdef P2_PROF
+        if (t == 0) atomicAdd(&g_p2prof[p2prof_slot<M, BLUE>()][15], 1ull);
+#endif
     }
 }
 
@@ -1204,6 +1240,18 @@ __global__ void fill_tables_kernel(const TableJob* __restrict__ jobs, double2* _
         tabs[jb.off + k] = make_double2(c, -s);
     }
 }
+
+#ifdef P2_PROF
+}  // namespace shtk
+extern "C" void shtc_p2prof(unsigned long long* out, int reset) {
+    cudaMemcpyFromSymbol(out, shtk::g_p2prof, sizeof(shtk::g_p2prof));
+    if (reset) {
+        static unsigned long long z[16][16] = {};
+        cudaMemcpyToSymbol(shtk::g_p2prof, z, sizeof(z));
+    }
+}
+namespace shtk {
+#endif
 
 void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cudaStream_t s) {
     for (int j0 = 0; j0 < n_jobs; j0 += 65535) {
