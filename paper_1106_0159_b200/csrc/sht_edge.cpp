@@ -136,7 +136,8 @@ CostParams CostParams::b200() {
     CostParams p;
     p.alpha = 2.0e-5;            // NCCL all-to-all launch + handshake on NVLink 5 / NVSwitch
     p.beta_inv_bw = 1.0 / 770e9; // measured peer copy, per direction per GPU (B200_PROFILING.md)
-    p.gamma = 1.65e-14;          // Legendre seconds per model flop at C4 (round 1, 1 GPU)
+    p.gamma = 1.42e-14;          // Legendre seconds per model flop at C4: (6.90 + 8.65) / 2 ms over
+                                 // 4 R_N lmax mmax = 549.7 G (round 1, 1 GPU, profiles/r01_bench.json)
     return p;
 }
 
