@@ -584,6 +584,10 @@ __device__ __forceinline__ double2 m2a_step_act(M2ALane<R>& L, double A, int i, 
 #ifndef LEG_M2A_SHFL
 #define LEG_M2A_SHFL 0
 #endif
+#ifndef LEG_M2A_APIPE
+#define LEG_M2A_APIPE 1  // FAST-group coefficient loads: 0 per pair, 1 one pair ahead (8.67 -> 8.57 ms
+                         // at C4), 2 all upfront (8.64 ms)
+#endif
 #if LEG_M2A_SHFL
 constexpr int M2A_G = 8;  // degrees per cross-lane reduction group
 #else
@@ -753,12 +757,34 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                     double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
                     if (ig > ie && gc == M2A_G) {
                         // after the last activation: straight-line steps, coefficients in pairs
+#if LEG_M2A_APIPE == 1
+                        // the next pair's coefficients are loaded before this pair's partials
+                        // are stored (the compiler cannot move the load across the stores)
+                        double2 a = *reinterpret_cast<const double2*>(&sm.A[g]);
+#pragma unroll
+                        for (int u = 0; u < M2A_G; u += 2) {
+                            const double2 an = *reinterpret_cast<const double2*>(&sm.A[g + (u + 2 < M2A_G ? u + 2 : u)]);
+                            row[u] = m2a_step<R, false>(L, a.x);
+                            row[u + 1] = m2a_step<R, true>(L, a.y);
+                            a = an;
+                        }
+#elif LEG_M2A_APIPE == 2
+                        double2 ag[M2A_G / 2];
+#pragma unroll
+                        for (int u = 0; u < M2A_G / 2; ++u) ag[u] = *reinterpret_cast<const double2*>(&sm.A[g + 2 * u]);
+#pragma unroll
+                        for (int u = 0; u < M2A_G; u += 2) {
+                            row[u] = m2a_step<R, false>(L, ag[u >> 1].x);
+                            row[u + 1] = m2a_step<R, true>(L, ag[u >> 1].y);
+                        }
+#else
 #pragma unroll
                         for (int u = 0; u < M2A_G; u += 2) {
                             const double2 a = *reinterpret_cast<const double2*>(&sm.A[g + u]);
                             row[u] = m2a_step<R, false>(L, a.x);
                             row[u + 1] = m2a_step<R, true>(L, a.y);
                         }
+#endif
                     } else {
                         // activation window (warp-uniform event test per step), seed, partial group
                         for (int u = 0; u < M2A_G; u += 2) {
