@@ -820,9 +820,10 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                     // lane j reduces column j (degree ig + j/2, component j&1) over the 32 lane
                     // rows in a fixed order and accumulates it into the warp's scratch slot
                     __syncwarp();
-                    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                    double s0 = sm.red[0][lane], s1 = sm.red[1][lane], s2 = sm.red[2][lane],
+                           s3 = sm.red[3][lane];
 #pragma unroll
-                    for (int rr = 0; rr < 32; rr += 4) {
+                    for (int rr = 4; rr < 32; rr += 4) {
                         s0 += sm.red[rr][lane];
                         s1 += sm.red[rr + 1][lane];
                         s2 += sm.red[rr + 2][lane];
