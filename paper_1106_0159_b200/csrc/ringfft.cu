@@ -596,7 +596,29 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             // fold (ring_synthesis_into's bins, fourier.cpp:17-25): H_k for 0 <= k <= N, terms
             // in ascending m as the reference adds them.  k = N of a direct ring (N == M) is an
             // extra slot of thread 0 in the last batch.
-            if (n > mmax) {
+            if (n - N + 1 > mmax) {
+                // no wraps and no conjugate terms below k = N (every n - k > mmax): H_k = v_k
+                // [k <= mmax], the row read once with all E loads in flight together (belt
+                // rings when lmax = 2 nside); H_N (whose conjugate term n - N may be <= mmax)
+                // by thread 0
+                double2 x[E];
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    x[j] = a.delta_in[delta_index(a, pos, (k < N && k <= mmax) ? k : 0)];
+                }
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) buf[p2pad(k)] = (k <= mmax) ? rot_value(x[j], k, rot, ph) : make_double2(0.0, 0.0);
+                }
+                if (t == 0) {
+                    double2 h = make_double2(0.0, 0.0);
+                    if (N <= mmax) h = folded_value(a, pos, N, rot, ph);
+                    if (n - N <= mmax) h = cadd(h, cconj(folded_value(a, pos, n - N, rot, ph)));
+                    buf[p2pad(N)] = h;
+                }
+            } else if (n > mmax) {
                 // no wraps: H_k = v_k [k <= mmax] + conj v_{n-k} [n-k <= mmax]; loads from
                 // clamped (always valid) positions and masked after, so the G elements' loads
                 // issue back to back
