@@ -682,17 +682,25 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 }
             }
             P2T(1);
-            __syncthreads();
-            P2T(2);
             // Z_k = (H_k + conj H_{N-k}) + i (H_k - conj H_{N-k}) e^{+2 pi i k/n}: the C2R of
-            // length n as a complex inverse FFT of length N (chirped for Bluestein)
+            // length n as a complex inverse FFT of length N (chirped for Bluestein).  The
+            // e^{2 pi i k/n} table loads are issued before the fold barrier, so their latency
+            // overlaps the wait.
             const double2* __restrict__ hw = a.tabs + d.hw_off;
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            double2 wv[E];
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                wv[j] = __ldg(&hw[k < N ? k : 0]);  // valid position, result masked below
+            }
+            __syncthreads();
+            P2T(2);
 #pragma unroll
             for (int j = 0; j < E; ++j) {
                 const int k = t + T * j;
                 const int kc = k < N ? k : 0;  // table loads from valid positions, result masked
-                const double2 w = __ldg(&hw[kc]);
+                const double2 w = wv[j];
                 double2 c = make_double2(1.0, 0.0);
                 if constexpr (BLUE) c = __ldg(&chirp[kc]);
                 const double2 Hp = buf[p2pad(kc)], Hq = buf[p2pad(N - kc)];
