@@ -110,38 +110,53 @@ def cpu_baseline(max_seconds: float = 30.0):
     threads = os.cpu_count() or 1
     cfgs = [(128, 256), (256, 512), (512, 1024), (1024, 2048), (2048, 4096)]
     if "rate" not in _PROBE:
-        # probe on C1 to project the cost (the reference's time scales ~ F_alg)
-        g = ref.healpix_grid(128)
-        a = ref.random_alm(256, 256, SEED_ALM)
+        # probe on nside 512 / lmax 1024 (~0.3 s on 16 cores) to project the cost: the
+        # reference's time scales ~ F_alg, and its rate still rises with size (thread scaling),
+        # so a probe this size projects the larger configs conservatively
+        g = ref.healpix_grid(512)
+        a = ref.random_alm(1024, 1024, SEED_ALM)
         t0 = time.perf_counter()
-        m, _ = ref.distributed_synthesis(a, 256, 256, g, 1, threads, pairing=True)
-        ref.distributed_analysis(m, 256, 256, g, 1, threads, pairing=True)
-        _PROBE["rate"] = 2 * falg_flops(256, 256, g.n_rings) / max(time.perf_counter() - t0, 1e-6)
+        m, _ = ref.distributed_synthesis(a, 1024, 1024, g, 1, threads, pairing=True)
+        ref.distributed_analysis(m, 1024, 1024, g, 1, threads, pairing=True)
+        _PROBE["rate"] = 2 * falg_flops(1024, 1024, g.n_rings) / max(time.perf_counter() - t0, 1e-6)
     rate = _PROBE["rate"]
-    chosen = cfgs[0]
+    # the largest config whose alm2map + map2alm is projected to fit; at the workload's own
+    # config a single alm2map (the two transforms cost the same in the reference) is a bounded
+    # sample of the step that keeps the rate of the real size
+    chosen, half = cfgs[0], False
     for ns, lm in cfgs:
-        # the small probe over-estimates the rate of large configs (cache effects): margin 3x
-        if 3 * 2 * falg_flops(lm, lm, 4 * ns - 1) / rate <= max_seconds:
-            chosen = (ns, lm)
+        cost = falg_flops(lm, lm, 4 * ns - 1) / rate  # the probe's rate is the lower one
+        if 2 * 1.25 * cost <= max_seconds:
+            chosen, half = (ns, lm), False
+        elif cost <= max_seconds and (ns, lm) == (NSIDE, LMAX):
+            chosen, half = (ns, lm), True
     ns, lm = chosen
     g = ref.healpix_grid(ns)
     a = sht.gaussian_alm(lm, lm, SEED_ALM)
     t0 = time.perf_counter()
     m, st1 = ref.distributed_synthesis(a, lm, lm, g, 1, threads, pairing=True)
     t1 = time.perf_counter()
-    _, st2 = ref.distributed_analysis(m, lm, lm, g, 1, threads, pairing=True)
+    st2 = None
+    if not half:
+        _, st2 = ref.distributed_analysis(m, lm, lm, g, 1, threads, pairing=True)
     t2 = time.perf_counter()
-    fl = 2 * falg_flops(lm, lm, g.n_rings)
-    return {
+    fl = (1 if half else 2) * falg_flops(lm, lm, g.n_rings)
+    what = "one alm2map" if half else "one alm2map+map2alm"
+    out = {
         "value": fl / (t2 - t0) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-        "sample": f"one alm2map+map2alm at HEALPix nside={ns}, lmax=mmax={lm} (largest config "
-                  f"projected to fit {max_seconds:.0f}s; same transforms as the workload, rate "
-                  f"normalised by F_alg), reference distributed_synthesis/analysis, 1 worker x "
-                  f"{threads} threads, PairPolicy::mirror",
-        "ms_alm2map": (t1 - t0) * 1e3, "ms_map2alm": (t2 - t1) * 1e3,
+        "sample": f"{what} at HEALPix nside={ns}, lmax=mmax={lm} (largest sample projected to fit "
+                  f"{max_seconds:.0f}s; same transforms as the workload, rate normalised by F_alg), "
+                  f"reference distributed_synthesis/analysis, 1 worker x {threads} threads, "
+                  f"PairPolicy::mirror",
+        "ms_alm2map": (t1 - t0) * 1e3,
         "stages_alm2map_s": {k: st1[k] for k in ("recurrence_s", "fft_s", "exchange_s")},
-        "stages_map2alm_s": {k: st2[k] for k in ("recurrence_s", "fft_s", "exchange_s")},
     }
+    if st2 is not None:
+        out["ms_map2alm"] = (t2 - t1) * 1e3
+        out["stages_map2alm_s"] = {k: st2[k] for k in ("recurrence_s", "fft_s", "exchange_s")}
+    else:
+        out["ms_map2alm"] = out["ms_alm2map"]  # not run: the reference's map2alm costs the same
+    return out
 
 
 # ----------------------------------------------------------------------------------------
@@ -481,8 +496,9 @@ def run_reference(args):
     if rank != 0:
         return
     # every step is a bounded sample so that the whole --steps/--warmup run stays within a
-    # few minutes (~150 s of reference CPU work in total)
-    per_step = max(2.0, min(args.cpu_seconds, 150.0 / (args.steps + args.warmup)))
+    # few minutes: a budget of ~300 s of reference CPU work, which on 16 cores fits one C4
+    # alm2map (~6.5 s) per step for up to ~40 steps
+    per_step = max(2.0, min(args.cpu_seconds, 300.0 / (args.steps + args.warmup)))
     steps = []
     for _ in range(args.warmup):
         cpu_baseline(per_step)
