@@ -383,23 +383,29 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
             double A, C;
             double2 v;
         };
-        auto fetch = [&](int c, Raw& rw) {
-            const int i = i_first + c * LEG_CL + lane;
-            if (i <= n) {
-                rw.C = gC[i];
-                rw.v = galm[i];
-                rw.A = gA[i];
-            } else {
-                rw.A = rw.C = 0.0;
-                rw.v = make_double2(0.0, 0.0);
+        constexpr int K = LEG_CL / 32;  // entries per lane per chunk
+        auto fetch = [&](int c, Raw (&rw)[K]) {
+#pragma unroll
+            for (int q = 0; q < K; ++q) {
+                const int i = i_first + c * LEG_CL + q * 32 + lane;
+                if (i <= n) {
+                    rw[q].C = gC[i];
+                    rw[q].v = galm[i];
+                    rw[q].A = gA[i];
+                } else {
+                    rw[q].A = rw[q].C = 0.0;
+                    rw[q].v = make_double2(0.0, 0.0);
+                }
             }
         };
         const int nchunks = (n - i_first + 1 + LEG_CL - 1) / LEG_CL;
-        Raw nxt;
+        Raw nxt[K];
         if (nchunks > 0) fetch(0, nxt);
         for (int c = 0; c < nchunks; ++c) {
             __syncwarp();
-            sm.put(lane, Coef{nxt.A, nxt.v.x * nxt.C, nxt.v.y * nxt.C});
+#pragma unroll
+            for (int q = 0; q < K; ++q)
+                sm.put(q * 32 + lane, Coef{nxt[q].A, nxt[q].v.x * nxt[q].C, nxt[q].v.y * nxt[q].C});
             __syncwarp();
             if (c + 1 < nchunks) fetch(c + 1, nxt);
             const int i0 = i_first + c * LEG_CL;  // odd: pairs are (odd, even) degree offsets
@@ -680,9 +686,13 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
             __syncwarp();
             int ev = next_activation<R>(L.act, ic - 1 + (ic == 0));
 
-            auto fetch = [&](int c) {
-                const int i = ic + c * LEG_CL + lane;
-                return i <= n ? gA[i] : 0.0;
+            constexpr int K = LEG_CL / 32;  // entries per lane per chunk
+            auto fetch = [&](int c, double (&v)[K]) {
+#pragma unroll
+                for (int q = 0; q < K; ++q) {
+                    const int i = ic + c * LEG_CL + q * 32 + lane;
+                    v[q] = i <= n ? gA[i] : 0.0;
+                }
             };
             // this lane's (degree, component) of the group in the scratch slot
 #if LEG_M2A_SHFL
@@ -690,12 +700,14 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
 #else
             double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
 #endif
-            double nxt = fetch(0);
+            double nxt[K];
+            fetch(0, nxt);
             for (int c = 0; c < nchunks; ++c) {
                 __syncwarp();
-                sm.A[lane] = nxt;
+#pragma unroll
+                for (int q = 0; q < K; ++q) sm.A[q * 32 + lane] = nxt[q];
                 __syncwarp();
-                if (c + 1 < nchunks) nxt = fetch(c + 1);
+                if (c + 1 < nchunks) fetch(c + 1, nxt);
                 const int i0 = ic + c * LEG_CL;
                 const int cnt = min(LEG_CL, n - i0 + 1);
                 for (int g = 0; g < cnt; g += M2A_G) {
