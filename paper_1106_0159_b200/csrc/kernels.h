@@ -57,6 +57,9 @@ static_assert(LEG_CL % 32 == 0, "whole entries per lane");
 #define LEG_M2A_GROUP_DEF 4
 #endif
 constexpr int LEG_M2A_GROUP = LEG_M2A_GROUP_DEF;  // tiles per map2alm work item (partials reduce G-fold)
+#ifndef LEG_M2A_ITEMS_PER_WARP
+#define LEG_M2A_ITEMS_PER_WARP 8  // fewer tiles per item when a plan has fewer items per resident warp
+#endif
 
 // One warp-sized unit of work of the persistent kernels.
 //   alm2map: (mi, tile id, -, -); map2alm: (mi, first index into tile_list, tile count, item

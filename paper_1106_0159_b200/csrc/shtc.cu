@@ -612,7 +612,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vect
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
     const int g_dev = (int)std::max<int64_t>(
-        1, std::min<int64_t>(LEG_M2A_GROUP, alive_total / (8 * (int64_t)leg_m2a_warps(dev_id))));
+        1, std::min<int64_t>(LEG_M2A_GROUP, alive_total / (LEG_M2A_ITEMS_PER_WARP * (int64_t)leg_m2a_warps(dev_id))));
     P.m2a_group = g_dev;
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
