@@ -47,6 +47,10 @@ unsigned long long launch_count() { return g_launches.load(std::memory_order_rel
 namespace {
 
 constexpr double INV_LN2 = 1.4426950408889634074;  // legendre.cpp:10
+
+#ifndef LEG_A2M_G
+#define LEG_A2M_G 8  // alm2map FAST group: steps whose coefficients are loaded up front
+#endif
 constexpr double SCALE_DOWN = 0x1p-512;
 
 __device__ __forceinline__ void seed_value(int m, double log_mu_m, double log2s2, int s2pos,
@@ -429,10 +433,10 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
                 }
             }
             // after the last activation: groups of 8 steps, coefficients loaded up front
-            for (; j + 8 <= cnt; j += 8) {
-                Coef cg[8];
+            for (; j + LEG_A2M_G <= cnt; j += LEG_A2M_G) {
+                Coef cg[LEG_A2M_G];
 #pragma unroll
-                for (int u = 0; u < 8; u += 2) {
+                for (int u = 0; u < LEG_A2M_G; u += 2) {
                     const double2 a = *reinterpret_cast<const double2*>(&sm.A[j + u]);
                     const double2 xr = *reinterpret_cast<const double2*>(&sm.ar[j + u]);
                     const double2 xi = *reinterpret_cast<const double2*>(&sm.ai[j + u]);
@@ -440,7 +444,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
                     cg[u + 1] = Coef{a.y, xr.y, xi.y};
                 }
 #pragma unroll
-                for (int u = 0; u < 8; u += 2) {
+                for (int u = 0; u < LEG_A2M_G; u += 2) {
                     a2m_step<R, true>(L, cg[u]);
                     a2m_step<R, false>(L, cg[u + 1]);
                 }
