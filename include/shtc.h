@@ -99,7 +99,11 @@ shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* che
                                   uint64_t* fast);
 
 /* ---- whole transforms ---------------------------------------------------------------- */
-/* alm: 2*AlmSet::count(lmax,mmax) doubles; map: n_pix doubles.  Host buffers. */
+/* alm: 2*AlmSet::count(lmax,mmax) doubles; map: n_pix doubles.  Host buffers: the copies are
+ * pipelined against the kernels over latitude bands.  Page-locked buffers (cudaHostAlloc,
+ * cudaHostRegister, pinned tensors) are copied directly; pageable ones (std::vector, numpy) go
+ * through page-locked staging buffers the context keeps, copied on all host cores.  Returns when
+ * the output is in place. */
 shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_timing* t);
 shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_timing* t);
 /* Same, device-resident buffers (no host copies). */
