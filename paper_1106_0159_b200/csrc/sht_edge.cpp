@@ -95,7 +95,7 @@ SkyMap read_map(const std::string& path) {
     std::ifstream is(path, std::ios::binary);
     if (!is) throw std::runtime_error("read_map: cannot open " + path);
     const Header h = header(is, "SHTMAP1", "read_map");
-    const std::string& scheme = field(h, "scheme", "read_map");
+    const std::string scheme = field(h, "scheme", "read_map");
     SkyMap map;
     if (scheme == "healpix-ring")
         map.grid = build_healpix_grid(static_cast<int>(ifield(h, "nside", "read_map")));

@@ -514,7 +514,7 @@ int m2a_band_group() {
     return g;
 }
 
-void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int mmax, const std::vector<int>& ms,
+void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set ms*/, const std::vector<int>& ms,
                     std::vector<Stream> streams, const std::vector<double>& log_mu) {
     cudaStream_t s = c->stream;
     cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
@@ -1454,7 +1454,8 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
         std::vector<cudaEvent_t> h_chunk(kOrderChunks);
         int th = -1, th_last = -1;
         for (int k = 0; k < kOrderChunks; ++k) {
-            auto [b, e] = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
+            const auto span = alm_span(ctx, P.chunk_mi[k], P.chunk_mi[k + 1]);
+            const size_t b = span.first, e = span.second;  // (a lambda below captures them)
             if (!in_pinned && e > b)
                 par_memcpy(ctx->stage_alm.as<double2>() + b, reinterpret_cast<const double2*>(alm) + b,
                            (e - b) * sizeof(double2));
