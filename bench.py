@@ -409,6 +409,65 @@ def run_ours(args):
                "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": bytes_alm + bytes_map, "d2h_bytes_per_step": bytes_map + bytes_alm,
                "gpu_launches": n_launch_e2e}
+    elif args.exchange == "peer":
+        # N ranks: every rank reads its orders' a_lm from a pinned host triangle, runs the fused
+        # m-distributed step, writes its rings' pixels to a pinned host map, reads them back as
+        # the map2alm input and writes its orders' a_lm back; copies on the shared stream
+        # (not pipelined against the kernels), max over ranks
+        alm_pin = torch.from_numpy(alm_h.view(np.float64)).pin_memory()
+        map_pin = torch.zeros(grid.n_pix, dtype=torch.float64).pin_memory()
+        alm_back = torch.zeros_like(alm_pin).pin_memory()
+        ivs = []  # this rank's rings as pixel intervals
+        offs, nphi = np.asarray(grid.pixel_offset), np.asarray(grid.n_phi)
+        for r in sorted(layout.ring_sets[rank]):
+            b, e = int(offs[r]), int(offs[r] + nphi[r])
+            if ivs and ivs[-1][1] == b:
+                ivs[-1][1] = e
+            else:
+                ivs.append([b, e])
+        alm_dev = torch.empty_like(alm)
+
+        def e2e_step():
+            ctx.copy_orders(alm_pin.data_ptr(), alm_dev.data_ptr(), True)
+            ctx.legendre_alm2map_peer(alm_dev.data_ptr())
+            px.barrier()
+            ctx.ring_synthesis_dev(px.recv, mp.data_ptr())
+            for b, e in ivs:
+                map_pin[b:e].copy_(mp[b:e], non_blocking=True)
+            for b, e in ivs:
+                mp[b:e].copy_(map_pin[b:e], non_blocking=True)
+            ctx.ring_analysis_peer(mp.data_ptr())
+            px.barrier()
+            ctx.legendre_map2alm_dev(px.send, alm_out.data_ptr())
+            ctx.copy_orders(alm_out.data_ptr(), alm_back.data_ptr(), False)
+        for _ in range(args.warmup):
+            e2e_step()
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        n_launch_e0 = sht.kernel_launches()
+        for _ in range(args.steps):
+            e2e_step()
+        e1.record(stream)
+        n_launch_e2e = sht.kernel_launches() - n_launch_e0
+        torch.cuda.synchronize(dev)
+        dist.barrier()
+        own_alm = sum(lmax - m + 1 for m in layout.m_sets[rank]) * 16
+        own_map = sum(e - b for b, e in ivs) * 8
+        t = torch.tensor([e0.elapsed_time(e1), float(own_alm + own_map)], dtype=torch.float64,
+                         device="cpu" if shared else dev)
+        tm = t.clone()
+        dist.all_reduce(tm, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_ms = float(tm[0].item()) / args.steps
+        moved = int(t[1].item())  # whole job, each direction
+        e2e = {"value": 2 * falg_flops(lmax, mmax, grid.n_rings) / (e2e_ms * 1e-3) / 1e12,
+               "unit": "TFLOP/s", "ms_per_step": e2e_ms, "h2d_bytes_per_step": moved,
+               "d2h_bytes_per_step": moved, "gpu_launches": n_launch_e2e,
+               "note": "per rank: its orders' a_lm and its rings' pixels over its own PCIe link, "
+                       "copies not pipelined against the kernels"}
 
     # ---- parity spot check of the timed output (the reference is checked in tests/) ----
     roundtrip = None

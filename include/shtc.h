@@ -159,6 +159,11 @@ shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_t
  * uint32 flag array (zeroed at allocation); epoch must increase by one per barrier. */
 shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint64_t* flags,
                               uint32_t epoch);
+/* Host <-> device copy of this context's orders (the set_band order set) between two full
+ * m-major a_lm triangles (2*AlmSet::count(lmax,mmax) doubles each): the a_lm share a worker
+ * of an m-distributed run reads (to_device != 0) or returns.  One async copy per order on the
+ * context stream; page-locked host memory for overlap. */
+shtc_status shtc_copy_orders(shtc_ctx* ctx, const double* src, double* dst, int to_device);
 
 /* ---- Legendre-stage operators (transforms.cpp:269-365), host buffers ------------------ */
 /* Delta^A_m(r) for the given latitudes and orders; delta: n_lat x n_m complex, ring-major.

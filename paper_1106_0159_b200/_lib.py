@@ -23,7 +23,7 @@ EXPORTED = [
     "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
     "shtc_measure_fp64_peak", "shtc_dev_alloc", "shtc_dev_free", "shtc_ipc_handle", "shtc_ipc_open",
     "shtc_ipc_close", "shtc_set_exchange_peers", "shtc_legendre_alm2map_peer", "shtc_ring_analysis_peer",
-    "shtc_peer_barrier", "shtc_kernel_launches",
+    "shtc_peer_barrier", "shtc_kernel_launches", "shtc_copy_orders",
 ]
 
 
@@ -59,6 +59,7 @@ def lib():
         L.shtc_device_count.restype = i32
         L.shtc_kernel_launches.restype = C.c_uint64
         L.shtc_kernel_launches.argtypes = []
+        L.shtc_copy_orders.argtypes = [vp, vp, vp, i32]
         L.shtc_set_stream.argtypes = [vp, vp]
         L.shtc_set_grid.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32]
         L.shtc_set_band.argtypes = [vp, i32, i32, i32, vp]

@@ -1908,6 +1908,25 @@ shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint
     });
 }
 
+shtc_status shtc_copy_orders(shtc_ctx* ctx, const double* src, double* dst, int to_device) {
+    if (!ctx || !src || !dst) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if (!ctx->band_set) fail(SHTC_EINVAL, "no band set");
+        const cudaMemcpyKind kind = to_device ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToHost;
+        const double2* s2 = reinterpret_cast<const double2*>(src);
+        double2* d2 = reinterpret_cast<double2*>(dst);
+        for (size_t i = 0; i < ctx->ms.size();) {
+            // runs of consecutive orders are contiguous in the triangle: one copy per run
+            size_t e = i + 1;
+            while (e < ctx->ms.size() && ctx->ms[e] == ctx->ms[e - 1] + 1) ++e;
+            const size_t b0 = (size_t)alm_offset(ctx->ms[i], ctx->lmax);
+            const size_t b1 = (size_t)alm_offset(ctx->ms[e - 1], ctx->lmax) + (ctx->lmax - ctx->ms[e - 1] + 1);
+            CK(cudaMemcpyAsync(d2 + b0, s2 + b0, (b1 - b0) * sizeof(double2), kind, ctx->stream));
+            i = e;
+        }
+    });
+}
+
 // ---- Legendre-stage operators ---------------------------------------------------------
 namespace {
 void op_plan(shtc_ctx* c, int lmax, int mmax, int n_lat, const double* x, int n_m, const int32_t* ms) {

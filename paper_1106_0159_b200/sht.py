@@ -581,6 +581,12 @@ class Context:
         self._check(lib().shtc_ring_analysis_peer(self._h, C.c_void_p(map_ptr), C.byref(t) if timing else None))
         return t.as_dict() if timing else None
 
+    def copy_orders(self, src_ptr: int, dst_ptr: int, to_device: bool):
+        """This context's orders between two full a_lm triangles (host <-> device, async on
+        the context stream)."""
+        self._check(lib().shtc_copy_orders(self._h, C.c_void_p(src_ptr), C.c_void_p(dst_ptr),
+                                           1 if to_device else 0))
+
     def peer_barrier(self, rank: int, n_workers: int, flag_ptrs, epoch: int):
         f = np.ascontiguousarray(flag_ptrs, np.uint64)
         self._check(lib().shtc_peer_barrier(self._h, rank, n_workers, _p(f), C.c_uint32(epoch & 0xFFFFFFFF)))

@@ -38,3 +38,6 @@ def test_bench_multirank_shared_gpu(n):
     assert "peer-memory exchange" in d["config"]["parallelism"]
     assert d["exchange"]["bytes_sent_per_rank_per_transform"] > 0
     assert d["gpu_launches"] > 0
+    # end to end through pinned host buffers at N ranks: the whole job's a_lm + map each way
+    assert d["e2e"]["ms_per_step"] > 0 and d["e2e"]["gpu_launches"] > 0
+    assert d["e2e"]["h2d_bytes_per_step"] == 16 * (257 * 258 // 2) + 8 * 12 * 128 * 128
