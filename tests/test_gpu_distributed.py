@@ -79,3 +79,34 @@ def test_stage_path_matches_single_worker(nside, lmax, W, rings):
     torch.cuda.synchronize()
     got = out.cpu().numpy().view(np.complex128)
     assert np.array_equal(got, want_alm)
+
+
+def test_copy_orders_moves_exactly_the_worker_orders():
+    """shtc_copy_orders: a worker's order segments between full host / device a_lm triangles
+    (the multi-rank e2e path); other orders untouched."""
+    dev = torch.device("cuda", 0)
+    lmax = 40
+    grid = sht.build_healpix_grid(16)
+    layout = sht.WorkerLayout.create(grid, lmax, 3)
+    ms = layout.m_sets[1]
+    c = sht.Context(0)
+    c.set_grid(grid)
+    c.set_band(lmax, lmax, ms)
+    alm_h = sht.random_alm(lmax, lmax, 5)
+    host = torch.from_numpy(alm_h.view(np.float64).copy()).pin_memory()
+    d = torch.full((host.numel(),), -7.0, dtype=torch.float64, device=dev)
+    torch.cuda.synchronize()
+    c.copy_orders(host.data_ptr(), d.data_ptr(), True)
+    torch.cuda.synchronize()
+    back = torch.full_like(host, 3.0).pin_memory()
+    c.copy_orders(d.data_ptr(), back.data_ptr(), False)
+    torch.cuda.synchronize()
+    got_d = d.cpu().numpy().view(np.complex128)
+    got_b = back.numpy().view(np.complex128)
+    mine = np.zeros(alm_h.size, bool)
+    for m in ms:
+        o = sht.alm_offset(m, lmax)
+        mine[o:o + lmax - m + 1] = True
+    assert np.array_equal(got_d[mine], alm_h[mine]) and np.all(got_d[~mine] == -7.0 - 7.0j)
+    assert np.array_equal(got_b[mine], alm_h[mine]) and np.all(got_b[~mine] == 3.0 + 3.0j)
+    c.close()
