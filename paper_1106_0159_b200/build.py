@@ -89,7 +89,7 @@ def build_dropin(force: bool = False) -> Path:
     return DROPIN_LIB
 
 
-def build_variant(name: str, defines: list[str]) -> Path:
+def build_variant(name: str, defines: list[str], flags: list[str] | None = None) -> Path:
     """Tuning experiments: libshtc.so rebuilt with extra -D flags into _build/var_<name>/
     (selected at run time with SHTC_VARIANT_LIB; never the shipped library)."""
     d = OBJ / f"var_{name}"
@@ -99,7 +99,7 @@ def build_variant(name: str, defines: list[str]) -> Path:
     for src in CU_SOURCES:
         o = d / (src + ".o")
         objs.append(o)
-        jobs.append([nvcc(), *NVCC_FLAGS, *[f"-D{x}" for x in defines], "-I", str(ROOT / "include"), "-c",
+        jobs.append([nvcc(), *NVCC_FLAGS, *(flags or []), *[f"-D{x}" for x in defines], "-I", str(ROOT / "include"), "-c",
                      str(CSRC / src), "-o", str(o)])
     with ThreadPoolExecutor(max_workers=len(jobs)) as ex:
         res = list(ex.map(_run, jobs))
