@@ -99,63 +99,45 @@ class ClockSampler:
 # ----------------------------------------------------------------------------------------
 # CPU baseline: the reference itself (oracle/_ref), bounded sample
 # ----------------------------------------------------------------------------------------
-_PROBE = {}
-
-
-def cpu_baseline(max_seconds: float = 30.0):
-    """Reference alm2map+map2alm (distributed_synthesis/analysis, 1 worker, all host threads,
-    mirror pairing = its fastest path) on the largest HEALPix config projected to fit."""
+def cpu_baseline(nside: int = NSIDE, lmax: int = LMAX, transforms=("alm2map", "map2alm")):
+    """The reference's own CPU implementation (oracle/_ref: the unmodified sources compiled
+    here) on the workload's own config: one alm2map and one map2alm of the bench's Gaussian
+    a_lm, through distributed_synthesis / distributed_analysis (distribution.cpp:300-490) with
+    1 worker x all host threads and PairPolicy::mirror, its fastest path.  No projection, no
+    smaller stand-in grid: the same transforms the GPU step runs."""
     from oracle import ref
     from paper_1106_0159_b200 import sht
     threads = os.cpu_count() or 1
-    cfgs = [(128, 256), (256, 512), (512, 1024), (1024, 2048), (2048, 4096)]
-    if "rate" not in _PROBE:
-        # probe on nside 512 / lmax 1024 (~0.3 s on 16 cores) to project the cost: the
-        # reference's time scales ~ F_alg, and its rate still rises with size (thread scaling),
-        # so a probe this size projects the larger configs conservatively
-        g = ref.healpix_grid(512)
-        a = ref.random_alm(1024, 1024, SEED_ALM)
+    g = ref.healpix_grid(nside)
+    a = sht.gaussian_alm(lmax, lmax, SEED_ALM)
+    out = {"unit": "TFLOP/s", "cores": threads, "kind": "reference"}
+    fl = 0.0
+    t_total = 0.0
+    m = None
+    if "alm2map" in transforms:
         t0 = time.perf_counter()
-        m, _ = ref.distributed_synthesis(a, 1024, 1024, g, 1, threads, pairing=True)
-        ref.distributed_analysis(m, 1024, 1024, g, 1, threads, pairing=True)
-        _PROBE["rate"] = 2 * falg_flops(1024, 1024, g.n_rings) / max(time.perf_counter() - t0, 1e-6)
-    rate = _PROBE["rate"]
-    # the largest config whose alm2map + map2alm is projected to fit; at the workload's own
-    # config a single alm2map (the two transforms cost the same in the reference) is a bounded
-    # sample of the step that keeps the rate of the real size
-    chosen, half = cfgs[0], False
-    for ns, lm in cfgs:
-        cost = falg_flops(lm, lm, 4 * ns - 1) / rate  # the probe's rate is the lower one
-        if 2 * 1.25 * cost <= max_seconds:
-            chosen, half = (ns, lm), False
-        elif cost <= max_seconds and (ns, lm) == (NSIDE, LMAX):
-            chosen, half = (ns, lm), True
-    ns, lm = chosen
-    g = ref.healpix_grid(ns)
-    a = sht.gaussian_alm(lm, lm, SEED_ALM)
-    t0 = time.perf_counter()
-    m, st1 = ref.distributed_synthesis(a, lm, lm, g, 1, threads, pairing=True)
-    t1 = time.perf_counter()
-    st2 = None
-    if not half:
-        _, st2 = ref.distributed_analysis(m, lm, lm, g, 1, threads, pairing=True)
-    t2 = time.perf_counter()
-    fl = (1 if half else 2) * falg_flops(lm, lm, g.n_rings)
-    what = "one alm2map" if half else "one alm2map+map2alm"
-    out = {
-        "value": fl / (t2 - t0) / 1e12, "unit": "TFLOP/s", "cores": threads, "kind": "reference",
-        "sample": f"{what} at HEALPix nside={ns}, lmax=mmax={lm} (largest sample projected to fit "
-                  f"{max_seconds:.0f}s; same transforms as the workload, rate normalised by F_alg), "
-                  f"reference distributed_synthesis/analysis, 1 worker x {threads} threads, "
-                  f"PairPolicy::mirror",
-        "ms_alm2map": (t1 - t0) * 1e3,
-        "stages_alm2map_s": {k: st1[k] for k in ("recurrence_s", "fft_s", "exchange_s")},
-    }
-    if st2 is not None:
-        out["ms_map2alm"] = (t2 - t1) * 1e3
+        m, st1 = ref.distributed_synthesis(a, lmax, lmax, g, 1, threads, pairing=True)
+        dt = time.perf_counter() - t0
+        out["ms_alm2map"] = dt * 1e3
+        out["stages_alm2map_s"] = {k: st1[k] for k in ("recurrence_s", "fft_s", "exchange_s")}
+        fl += falg_flops(lmax, lmax, g.n_rings)
+        t_total += dt
+    if "map2alm" in transforms:
+        if m is None:
+            m = sht.gaussian_map(int(g.n_pix), 2026)
+        t0 = time.perf_counter()
+        _, st2 = ref.distributed_analysis(m, lmax, lmax, g, 1, threads, pairing=True)
+        dt = time.perf_counter() - t0
+        out["ms_map2alm"] = dt * 1e3
         out["stages_map2alm_s"] = {k: st2[k] for k in ("recurrence_s", "fft_s", "exchange_s")}
-    else:
-        out["ms_map2alm"] = out["ms_alm2map"]  # not run: the reference's map2alm costs the same
+        fl += falg_flops(lmax, lmax, g.n_rings)
+        t_total += dt
+    out["value"] = fl / t_total / 1e12
+    out["ms_per_step"] = t_total * 1e3
+    names = " + ".join(transforms)
+    out["sample"] = (f"{names} at HEALPix nside={nside}, lmax=mmax={lmax} (the workload's own config, "
+                     f"Gaussian a_lm seed {SEED_ALM}; map2alm of that alm2map output), reference "
+                     f"distributed_synthesis/analysis, 1 worker x {threads} threads, PairPolicy::mirror")
     return out
 
 
@@ -408,7 +390,42 @@ def run_ours(args):
         e2e = {"value": 2 * falg_flops(lmax, mmax, grid.n_rings) / (e2e_ms * 1e-3) / 1e12,
                "unit": "TFLOP/s", "ms_per_step": e2e_ms,
                "h2d_bytes_per_step": bytes_alm + bytes_map, "d2h_bytes_per_step": bytes_map + bytes_alm,
-               "gpu_launches": n_launch_e2e}
+               "gpu_launches": n_launch_e2e, "host_memory": "page-locked (pinned torch tensors)"}
+        # the path a reference C++ user hits: pageable std::vector-like buffers (numpy), which
+        # the library stages through its own page-locked buffers (wall clock: the call returns
+        # when the output is in place)
+        a_pg = alm_h.copy()
+        m_pg = np.empty(grid.n_pix)
+        b_pg = np.empty_like(alm_h)
+        ctx.alm2map(a_pg, out=m_pg)
+        ctx.map2alm(m_pg, out=b_pg)
+        n_pg = min(args.steps, 5)
+        t0 = time.perf_counter()
+        for _ in range(n_pg):
+            ctx.alm2map(a_pg, out=m_pg)
+            ctx.map2alm(m_pg, out=b_pg)
+        pg_ms = (time.perf_counter() - t0) * 1e3 / n_pg
+        e2e["pageable"] = {"value": 2 * falg_flops(lmax, mmax, grid.n_rings) / (pg_ms * 1e-3) / 1e12,
+                           "unit": "TFLOP/s", "ms_per_step": pg_ms, "steps": n_pg,
+                           "host_memory": "pageable (numpy), staged by the library on all host cores"}
+        # first call on a fresh context: geometry + band + plan (recurrence tables, activation
+        # scan, FFT tables) + one alm2map + one map2alm from pinned host buffers (wall clock)
+        t0 = time.perf_counter()
+        cold = sht.Context(local)
+        cold.set_stream(stream.cuda_stream)
+        cold.set_grid(grid, mirror=True)
+        cold.set_band(lmax, mmax)
+        t1 = time.perf_counter()
+        cold.plan()
+        t2 = time.perf_counter()
+        cold.alm2map(a_np, out=m_np)
+        cold.map2alm(m_np, out=b_np)
+        t3 = time.perf_counter()
+        cold.close()
+        e2e["first_call"] = {"ms": (t3 - t0) * 1e3, "plan_ms": (t2 - t1) * 1e3,
+                             "transforms_ms": (t3 - t2) * 1e3, "setup_ms": (t1 - t0) * 1e3,
+                             "note": "fresh context: set_grid + set_band + plan + alm2map + map2alm, "
+                                     "pinned host buffers, wall clock"}
     elif args.exchange == "peer":
         # N ranks: every rank reads its orders' a_lm from a pinned host triangle, runs the fused
         # m-distributed step, writes its rings' pixels to a pinned host map, reads them back as
@@ -486,7 +503,12 @@ def run_ours(args):
     leg_a_ms, leg_s_ms = float(np.mean(leg_a)), float(np.mean(leg_s))
     fl_leg = falg_flops(lmax, mmax, grid.n_rings) / ws  # per rank, per launch
     dom_ms, dom_name = (leg_a_ms, "leg_map2alm_kernel") if leg_a_ms >= leg_s_ms else (leg_s_ms, "leg_alm2map_kernel")
-    achieved = fl_leg / (dom_ms * 1e-3) / 1e12
+    # headline basis: the (l, m, ring-pair) steps the kernel actually executes x 8 flops (dead
+    # and never-activating streams are skipped, so the F_alg basis would count work that never
+    # runs); F_alg = 8 x n_alm x ceil(R_N/2) is kept as the secondary figure
+    exec_fl = 8.0 * stats["executed"]  # this rank's plan, per launch
+    achieved = exec_fl / (dom_ms * 1e-3) / 1e12
+    falg_achieved = fl_leg / (dom_ms * 1e-3) / 1e12
     # DRAM bytes per launch and ncu-executed DP rate from the committed full capture
     traffic, ncu_rec = None, {}
     tf = ROOT / "profiles" / "ncu_kernels.json"
@@ -499,16 +521,21 @@ def run_ours(args):
     roofline = {
         "bound": "fp64", "kernel": dom_name, "achieved": achieved, "peak": peak_tf,
         "unit": "TFLOP/s", "frac": achieved / peak_tf, "traffic": traffic,
+        "basis": "executed: 8 flops x (l, m, ring-pair) steps the kernel runs (plan count, "
+                 "cross-checked against ncu's executed DP instructions)",
         "peak_source": "measured live: DFMA-loop probe (shtc_measure_fp64_peak); "
                        "MEASURED_PEAKS.json has no FP64 entry",
-        "flops_per_launch": fl_leg,
-        "flops_basis": "algorithmic 8 x n_alm x ceil(R_N/2) (reference mirror-path steps x 8)",
-        "useful_tflops": 8.0 * stats["useful"] / ws / (dom_ms * 1e-3) / 1e12,
-        "executed_tflops": 8.0 * stats["executed"] / (dom_ms * 1e-3) / 1e12,
+        "flops_per_launch": exec_fl,
+        "falg": {"achieved": falg_achieved, "frac": falg_achieved / peak_tf, "flops_per_launch": fl_leg,
+                 "basis": "algorithmic 8 x n_alm x ceil(R_N/2) (reference mirror-path steps x 8; "
+                          "counts the skipped dead-stream steps)"},
+        "useful_tflops": 8.0 * stats["useful"] / (dom_ms * 1e-3) / 1e12,
         "ncu": {"executed_dp_tflops": ncu_rec.get("executed_dp_tflops"),
                 "fp64_pipe_pct": ncu_rec.get("fp64_pipe_pct"), "source": ncu_rec.get("source")},
-        "alm2map_kernel": {"ms": leg_s_ms, "achieved": fl_leg / (leg_s_ms * 1e-3) / 1e12},
-        "map2alm_kernel": {"ms": leg_a_ms, "achieved": fl_leg / (leg_a_ms * 1e-3) / 1e12},
+        "alm2map_kernel": {"ms": leg_s_ms, "achieved": exec_fl / (leg_s_ms * 1e-3) / 1e12,
+                           "falg_achieved": fl_leg / (leg_s_ms * 1e-3) / 1e12},
+        "map2alm_kernel": {"ms": leg_a_ms, "achieved": exec_fl / (leg_a_ms * 1e-3) / 1e12,
+                           "falg_achieved": fl_leg / (leg_a_ms * 1e-3) / 1e12},
     }
     ms_a2m = float(np.mean(leg_s)) + float(np.mean(fft_s))
     ms_m2a = float(np.mean(leg_a)) + float(np.mean(fft_a))
@@ -542,7 +569,7 @@ def run_ours(args):
     }
     if ws == 1 and not args.no_cpu_baseline:
         try:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_seconds)
+            line["cpu_baseline"] = cpu_baseline(args.nside, lmax)
         except Exception as exc:  # the oracle must exist; report instead of hiding
             line["cpu_baseline"] = {"error": repr(exc)}
     print(json.dumps(line), flush=True)
@@ -551,33 +578,64 @@ def run_ours(args):
 
 
 def run_reference(args):
+    """The reference arm: the reference's CPU implementation (oracle/_ref) on all host threads,
+    every step = one alm2map + one map2alm at the workload's own config (C4 by default, ~13 s
+    on 16 cores).  Warm-up on a CPU only touches the caches and thread pool, so at most one
+    warm-up step runs (keeps `--steps 20 --warmup 5` at ~4.5 minutes)."""
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    # every step is a bounded sample so that the whole --steps/--warmup run stays within a
-    # few minutes: a budget of ~300 s of reference CPU work, which on 16 cores fits one C4
-    # alm2map (~6.5 s) per step for up to ~40 steps
-    per_step = max(2.0, min(args.cpu_seconds, 300.0 / (args.steps + args.warmup)))
-    steps = []
-    for _ in range(args.warmup):
-        cpu_baseline(per_step)
-    for _ in range(args.steps):
-        steps.append(cpu_baseline(per_step))
-    v = float(np.median([s["value"] for s in steps]))
+    for _ in range(min(args.warmup, 1)):
+        cpu_baseline(args.nside, args.lmax)
+    steps = [cpu_baseline(args.nside, args.lmax) for _ in range(args.steps)]
+    ms_step = float(np.median([s["ms_per_step"] for s in steps]))
+    v = 2 * falg_flops(args.lmax, args.lmax, 4 * args.nside - 1) / (ms_step * 1e-3) / 1e12
     cb = dict(steps[-1])
     cb["value"] = v
+    cb["ms_per_step"] = ms_step
+    cb["sample"] = cb["sample"] + f"; median of {args.steps} steps"
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": ws,
-        "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": float(np.median([s["ms_alm2map"] + s["ms_map2alm"] for s in steps])),
+        "steps": args.steps, "warmup": args.warmup, "warmup_run": min(args.warmup, 1),
+        "ms_per_step": ms_step,
+        "ms_alm2map": float(np.median([s["ms_alm2map"] for s in steps])),
+        "ms_map2alm": float(np.median([s["ms_map2alm"] for s in steps])),
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic: Gaussian a_lm (seed 12345)",
-        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={args.lmax}{config_tag(args.nside, args.lmax)}",
+        "data": "synthetic: Gaussian a_lm (splitmix64 counter stream + Box-Muller, seed 12345); "
+                "map2alm input = the step's alm2map output",
+        "config": {"workload": f"alm2map+map2alm HEALPix nside={args.nside} lmax=mmax={args.lmax}"
+                               f"{config_tag(args.nside, args.lmax)}",
+                   "grid": "healpix-ring", "nside": args.nside, "lmax": args.lmax, "mmax": args.lmax,
+                   "parallelism": f"reference CPU, 1 worker x {cb['cores']} threads",
                    "sample": cb["sample"]},
         "cpu_baseline": cb,
         "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def _free_port() -> int:
+    import socket
+    with socket.socket() as so:
+        so.bind(("127.0.0.1", 0))
+        return so.getsockname()[1]
+
+
+def ensure_world(args):
+    """`python bench.py --gpus N` runs N ranks: outside torchrun (no WORLD_SIZE) with N > 1 the
+    script re-executes itself under torch.distributed.run, one process per GPU; inside torchrun
+    the world size must equal N."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None:
+        if args.gpus > 1:
+            cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                   f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+                   "--master-port", str(_free_port()), str(Path(__file__).resolve()), *sys.argv[1:]]
+            sys.stdout.flush()
+            os.execv(sys.executable, cmd)
+        return
+    if int(ws) != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}")
 
 
 def main():
@@ -588,7 +646,6 @@ def main():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--nside", type=int, default=NSIDE)
     p.add_argument("--lmax", type=int, default=LMAX)
-    p.add_argument("--cpu-seconds", type=float, default=30.0)
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--exchange", choices=["auto", "none", "peer", "nccl"], default="auto",
                    help="Delta exchange of the m-distributed path: peer (fused stores over peer "
@@ -597,6 +654,9 @@ def main():
     args = p.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus < 1:
+        raise SystemExit("bench.py: --gpus must be >= 1")
+    ensure_world(args)
     if args.impl == "reference":
         run_reference(args)
     else:

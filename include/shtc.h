@@ -156,7 +156,11 @@ shtc_status shtc_set_exchange_peers(shtc_ctx* ctx, const uint64_t* row_ptr, cons
 shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, shtc_timing* t);
 shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_timing* t);
 /* Device-side barrier on the context stream: flags[w] = address of worker w's n_workers-word
- * uint32 flag array (zeroed at allocation); epoch must increase by one per barrier. */
+ * uint32 flag array (zeroed at allocation); epoch must increase by one per barrier.
+ * Ordering contract: a peer-store stage writes into buffers another worker's consumer stage of
+ * the PREVIOUS call of the same direction may still read.  alm2map and map2alm calls that
+ * alternate are ordered by the other direction's barrier; when a direction repeats, every
+ * worker passes one extra barrier before its peer stores (sht.PeerExchange does this). */
 shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint64_t* flags,
                               uint32_t epoch);
 /* Host <-> device copy of this context's orders (the set_band order set) between two full

@@ -864,7 +864,9 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         // buffers) the generic in-place mixed-radix kernels.  Bluestein's FFT(conj chirp) is
         // built by the generic class of the same length at plan time.
         const int gcls = fft_class_for(d.B);
-        const bool clus = half && d.B == FFT_P2C_B;  // 16384-point Bluestein: 2-CTA clusters
+        // 16384-point Bluestein buffers (N < 8192): 2-CTA clusters.  A direct 16384-point ring
+        // (n_phi = 32768, N a power of two) is not one of them: it has no class and fails below
+        const bool clus = half && !smooth && d.B == FFT_P2C_B;
         int cls = clus ? FFT_P2C_CLASS : (half ? fft_p2_class_for(d.B, !smooth) : -1);
         if (cls < 0) cls = gcls;
         if (cls < 0)
@@ -1223,6 +1225,7 @@ shtc_status shtc_set_grid(shtc_ctx* ctx, int n_rings, const double* cos_theta, c
         ctx->fft_custom.built = false;
         ctx->id_row_off.release();
         ctx->custom_layout = false;
+        ctx->peers_set = false;  // peer targets index the old ring / order layout
     });
 }
 
@@ -1247,6 +1250,7 @@ shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int3
         ctx->leg.built = false;
         ctx->id_row_off.release();
         ctx->custom_layout = false;
+        ctx->peers_set = false;
     });
 }
 
@@ -1662,6 +1666,7 @@ shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int 
     if (!ctx) return SHTC_EINVAL;
     return guarded(ctx, [&] {
         if (!ctx->grid_set || !ctx->band_set) fail(SHTC_EINVAL, "set grid and band first");
+        ctx->peers_set = false;  // the peer targets are rebuilt on top of the new layout
         if (!row_off) {
             ctx->custom_layout = false;
             return;
@@ -1860,7 +1865,8 @@ shtc_status shtc_set_exchange_peers(shtc_ctx* ctx, const uint64_t* row_ptr, cons
 shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, shtc_timing* t) {
     if (!ctx || !alm_dev) return SHTC_EINVAL;
     return guarded(ctx, [&] {
-        if (!ctx->peers_set) fail(SHTC_EINVAL, "exchange peers not set");
+        if (!ctx->peers_set || !ctx->custom_layout || !ctx->fft_custom.built)
+            fail(SHTC_EINVAL, "exchange peers not set");
         ensure_leg_plan(ctx);
         LegPlanView v = ctx->leg.view;
         v.row_ptr = ctx->peer_row_ptr.as<double2*>();
@@ -1880,7 +1886,8 @@ shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, sht
 shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_timing* t) {
     if (!ctx || !map_dev) return SHTC_EINVAL;
     return guarded(ctx, [&] {
-        if (!ctx->peers_set) fail(SHTC_EINVAL, "exchange peers not set");
+        if (!ctx->peers_set || !ctx->custom_layout || !ctx->fft_custom.built)
+            fail(SHTC_EINVAL, "exchange peers not set");
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         run_ring_anal(ctx, ctx->fft_custom, map_dev, nullptr, ctx->m_base_d.as<int64_t>(),
                       ctx->m_stride_d.as<int64_t>(), -1, ctx->peer_col_ptr.as<double2*>());

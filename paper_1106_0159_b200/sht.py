@@ -669,6 +669,7 @@ class PeerExchange:
         self.recv = dev_alloc(dev, 16 * max(recv_c, 1))
         self.flags = dev_alloc(dev, 4 * W)
         self.epoch = 0
+        self._last = None
         self._opened = []
         mine = (self.send, self.recv, self.flags)
         if peers is not None:                       # workers in one process: plain addresses
@@ -705,13 +706,23 @@ class PeerExchange:
         self.epoch += 1
         self.ctx.peer_barrier(self.rank, self.n, self._flag_ptrs, self.epoch)
 
+    # Write-after-read: alm2map's peer stores land in the other workers' `recv`, which their
+    # previous alm2map's ring synthesis may still be reading (map2alm: `send` and the Legendre
+    # stage).  Alternating directions are ordered by the other direction's barrier; a repeated
+    # direction passes one extra barrier before its peer stores.
     def alm2map(self, alm_ptr: int, map_ptr: int, timing=False):
+        if self._last == "alm2map":
+            self.barrier()
+        self._last = "alm2map"
         t1 = self.ctx.legendre_alm2map_peer(alm_ptr, timing)
         self.barrier()
         t2 = self.ctx.ring_synthesis_dev(self.recv, map_ptr, timing)
         return (t1, t2) if timing else None
 
     def map2alm(self, map_ptr: int, alm_ptr: int, timing=False):
+        if self._last == "map2alm":
+            self.barrier()
+        self._last = "map2alm"
         t1 = self.ctx.ring_analysis_peer(map_ptr, timing)
         self.barrier()
         t2 = self.ctx.legendre_map2alm_dev(self.send, alm_ptr, timing)

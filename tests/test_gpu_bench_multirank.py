@@ -5,7 +5,6 @@ and uses gloo for the control plane.  The per-rank results are checked bitwise a
 worker in tests/test_gpu_peer_exchange.py; this test covers the driver's launch sequence."""
 import json
 import os
-import socket
 import subprocess
 import sys
 from pathlib import Path
@@ -17,17 +16,13 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 
-def _free_port():
-    with socket.socket() as so:
-        so.bind(("127.0.0.1", 0))
-        return so.getsockname()[1]
-
-
 @pytest.mark.parametrize("n", [2, 3])
 def test_bench_multirank_shared_gpu(n):
-    env = dict(os.environ, SHT_BENCH_SHARED_GPU="1")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
-           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()), "bench.py", "--gpus", str(n),
+    # exactly the driver's form `python bench.py --gpus N` (no torchrun wrapper): bench.py
+    # re-executes itself under torch.distributed.run with N ranks
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    env["SHT_BENCH_SHARED_GPU"] = "1"
+    cmd = [sys.executable, "bench.py", "--gpus", str(n),
            "--steps", "3", "--warmup", "3", "--nside", "128", "--lmax", "256"]
     r = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, (r.stdout + r.stderr)[-4000:]
@@ -41,3 +36,4 @@ def test_bench_multirank_shared_gpu(n):
     # end to end through pinned host buffers at N ranks: the whole job's a_lm + map each way
     assert d["e2e"]["ms_per_step"] > 0 and d["e2e"]["gpu_launches"] > 0
     assert d["e2e"]["h2d_bytes_per_step"] == 16 * (257 * 258 // 2) + 8 * 12 * 128 * 128
+

@@ -62,3 +62,19 @@ def test_ring_classes_match_reference(gpu_ctx, lmax, phase):
     back_want, _ = ref.analysis(want, lmax, lmax, g, pairing=True)
     back = gpu_ctx.map2alm(want)
     assert rel_max(back, back_want) < 1e-12, rel_max(back, back_want)
+
+
+@pytest.mark.parametrize("nphi", [32768, 8193, 65540])
+def test_unsupported_ring_lengths_fail_loudly(gpu_ctx, nphi):
+    """Ring lengths beyond the size classes (direct N = 16384, i.e. n_phi = 32768 / HEALPix
+    nside >= 8192 belt rings; odd non-7-smooth n_phi > 4096, e.g. the Gauss-Legendre 2 lmax + 1
+    = 8193 at lmax 4096; Bluestein buffers above 16384) are refused with SHTC_EUNSUPPORTED at
+    plan time, never computed wrongly."""
+    from paper_1106_0159_b200._lib import SHTC_EUNSUPPORTED, ShtcError
+    g = mixed_grid([16, nphi], 0.0)
+    gpu_ctx.set_grid(sht.PixelGrid("x", 0, g.cos_theta, g.n_phi, g.phi_0, g.weight))
+    gpu_ctx.set_band(8, 8)
+    with pytest.raises(ShtcError) as ei:
+        gpu_ctx.alm2map(ref.random_alm(8, 8, 1))
+    assert ei.value.code == SHTC_EUNSUPPORTED
+    assert "ring length" in str(ei.value)
