@@ -86,6 +86,11 @@ shtc_status shtc_set_grid(shtc_ctx* ctx, int n_rings, const double* cos_theta,
 /* Band limits and the orders this context owns (NULL / n_m<=0 = all of 0..mmax).  The
  * owned set is the worker's M_i of assign_m (distribution.cpp:82-99) for multi-GPU runs. */
 shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int32_t* ms);
+/* Rescaling ladder of the recurrence (ScaleLadder, legendre.hpp:26-47): enabled != 0 is
+ * ScaleLadder::standard() (the default, the 2^+-512 window), 0 is ScaleLadder::unscaled()
+ * (thresholds never trip: a stream whose seed lies below the window never counts).  Applies to
+ * the plans built afterwards (whole transforms and the Legendre-stage operators). */
+shtc_status shtc_set_ladder(shtc_ctx* ctx, int enabled);
 /* Builds (and caches) the Legendre plan (recurrence tables, underflow activation scan)
  * and the ring-FFT plan; otherwise built lazily by the first transform. */
 shtc_status shtc_plan(shtc_ctx* ctx, double* plan_ms);
@@ -168,6 +173,55 @@ shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint
  * of an m-distributed run reads (to_device != 0) or returns.  One async copy per order on the
  * context stream; page-locked host memory for overlap. */
 shtc_status shtc_copy_orders(shtc_ctx* ctx, const double* src, double* dst, int to_device);
+
+/* ---- single-process multi-GPU group -------------------------------------------------- */
+/* distributed_synthesis / distributed_analysis (distribution.cpp:300-490; distribution.hpp:
+ * 70-77) as one process driving W device contexts, worker i on device_ids[i] (NULL: device
+ * i mod device count; workers may share a device).  Orders and rings are owned per worker
+ * (m_owner[m], ring_owner[r]: a partition, e.g. from assign_m / assign_rings,
+ * distribution.cpp:82-124); every worker must own at least one order and one ring.
+ * Exchange of the Delta panel between the stages (exchange_m_to_rings / rings_to_m,
+ * distribution.cpp:233-298):
+ *   SHTC_EXCHANGE_PEER  fused: the producing stage kernel stores each entry straight into the
+ *                       consumer's buffer (NVLink peer memory; plain stores on a shared device),
+ *                       consumers wait on the producers' completion events;
+ *   SHTC_EXCHANGE_NCCL  ncclCommInitAll + grouped ncclSend/ncclRecv on the packed buffers
+ *                       (libnccl dlopen'ed on first use; needs one distinct device per worker).
+ * Results equal the single-context transforms.  Calls are synchronous (return with the output
+ * in place). */
+typedef struct shtc_group shtc_group;
+enum { SHTC_EXCHANGE_PEER = 0, SHTC_EXCHANGE_NCCL = 1 };
+typedef struct {
+    double legendre_ms;      /* stage maxima over the workers (CUDA events per worker) */
+    double fft_ms;
+    double exchange_ms;      /* end of the producer stage -> start of the consumer stage */
+    double h2d_ms;
+    double d2h_ms;
+    double total_ms;         /* wall clock of the whole call */
+    uint64_t exchange_bytes; /* Delta bytes moved between distinct workers */
+    uint64_t nominal_steps;  /* reference step count summed over the workers */
+} shtc_group_timing;
+shtc_status shtc_group_create(int n_workers, const int32_t* device_ids, int exchange_mode,
+                              shtc_group** out);
+void shtc_group_destroy(shtc_group* g);
+const char* shtc_group_last_error(const shtc_group* g); /* g may be NULL */
+shtc_status shtc_group_device(const shtc_group* g, int worker, int* device);
+shtc_status shtc_group_set_grid(shtc_group* g, int n_rings, const double* cos_theta,
+                                const int32_t* n_phi, const double* phi_0, const double* weight,
+                                const int64_t* pixel_offset, int mirror);
+/* Band limits + ownership; builds every worker's plans and exchange buffers. */
+shtc_status shtc_group_set_layout(shtc_group* g, int lmax, int mmax, const int32_t* m_owner,
+                                  const int32_t* ring_owner);
+shtc_status shtc_group_plan_ms(const shtc_group* g, double* plan_ms);
+/* Host buffers (pageable or page-locked), the whole a_lm triangle / map. */
+shtc_status shtc_group_alm2map(shtc_group* g, const double* alm, double* map, shtc_group_timing* t);
+shtc_status shtc_group_map2alm(shtc_group* g, const double* map, double* alm, shtc_group_timing* t);
+/* Device buffers, one per worker on its device: a full a_lm triangle / full map each (a worker
+ * reads and writes only its own orders / rings). */
+shtc_status shtc_group_alm2map_dev(shtc_group* g, const uint64_t* alm_dev, const uint64_t* map_dev,
+                                   shtc_group_timing* t);
+shtc_status shtc_group_map2alm_dev(shtc_group* g, const uint64_t* map_dev, const uint64_t* alm_dev,
+                                   shtc_group_timing* t);
 
 /* ---- Legendre-stage operators (transforms.cpp:269-365), host buffers ------------------ */
 /* Delta^A_m(r) for the given latitudes and orders; delta: n_lat x n_m complex, ring-major.

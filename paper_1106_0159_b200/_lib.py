@@ -24,7 +24,12 @@ EXPORTED = [
     "shtc_measure_fp64_peak", "shtc_dev_alloc", "shtc_dev_free", "shtc_ipc_handle", "shtc_ipc_open",
     "shtc_ipc_close", "shtc_set_exchange_peers", "shtc_legendre_alm2map_peer", "shtc_ring_analysis_peer",
     "shtc_peer_barrier", "shtc_kernel_launches", "shtc_copy_orders",
+    "shtc_group_create", "shtc_group_destroy", "shtc_group_last_error", "shtc_group_device",
+    "shtc_group_set_grid", "shtc_group_set_layout", "shtc_group_plan_ms", "shtc_group_alm2map",
+    "shtc_group_map2alm", "shtc_group_alm2map_dev", "shtc_group_map2alm_dev", "shtc_set_ladder",
 ]
+
+SHTC_EXCHANGE_PEER, SHTC_EXCHANGE_NCCL = 0, 1
 
 
 class Timing(C.Structure):
@@ -32,6 +37,17 @@ class Timing(C.Structure):
         ("legendre_ms", C.c_double), ("fft_ms", C.c_double), ("h2d_ms", C.c_double),
         ("d2h_ms", C.c_double), ("total_ms", C.c_double), ("nominal_steps", C.c_uint64),
         ("executed_steps", C.c_uint64),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class GroupTiming(C.Structure):
+    _fields_ = [
+        ("legendre_ms", C.c_double), ("fft_ms", C.c_double), ("exchange_ms", C.c_double),
+        ("h2d_ms", C.c_double), ("d2h_ms", C.c_double), ("total_ms", C.c_double),
+        ("exchange_bytes", C.c_uint64), ("nominal_steps", C.c_uint64),
     ]
 
     def as_dict(self):
@@ -63,6 +79,7 @@ def lib():
         L.shtc_set_stream.argtypes = [vp, vp]
         L.shtc_set_grid.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32]
         L.shtc_set_band.argtypes = [vp, i32, i32, i32, vp]
+        L.shtc_set_ladder.argtypes = [vp, i32]
         L.shtc_plan.argtypes = [vp, C.POINTER(dbl)]
         L.shtc_plan_stats.argtypes = [vp, u64p, u64p, u64p]
         L.shtc_plan_phase_stats.argtypes = [vp, u64p, u64p, u64p]
@@ -84,6 +101,17 @@ def lib():
         L.shtc_legendre_alm2map_peer.argtypes = [vp, vp, C.POINTER(Timing)]
         L.shtc_ring_analysis_peer.argtypes = [vp, vp, C.POINTER(Timing)]
         L.shtc_peer_barrier.argtypes = [vp, i32, i32, vp, C.c_uint32]
+        L.shtc_group_create.argtypes = [i32, vp, i32, C.POINTER(vp)]
+        L.shtc_group_destroy.argtypes = [vp]
+        L.shtc_group_destroy.restype = None
+        L.shtc_group_last_error.argtypes = [vp]
+        L.shtc_group_last_error.restype = C.c_char_p
+        L.shtc_group_device.argtypes = [vp, i32, C.POINTER(i32)]
+        L.shtc_group_set_grid.argtypes = [vp, i32, vp, vp, vp, vp, vp, i32]
+        L.shtc_group_set_layout.argtypes = [vp, i32, i32, vp, vp]
+        L.shtc_group_plan_ms.argtypes = [vp, C.POINTER(dbl)]
+        for f in ("shtc_group_alm2map", "shtc_group_map2alm", "shtc_group_alm2map_dev", "shtc_group_map2alm_dev"):
+            getattr(L, f).argtypes = [vp, vp, vp, C.POINTER(GroupTiming)]
         _LIB = L
     return _LIB
 
@@ -94,10 +122,10 @@ class ShtcError(RuntimeError):
         self.code = code
 
 
-def check(rc: int, ctx=None):
+def check(rc: int, ctx=None, group=None):
     if rc == SHTC_OK:
         return
-    msg = lib().shtc_last_error(ctx).decode(errors="replace")
+    msg = (lib().shtc_group_last_error(group) if group is not None else lib().shtc_last_error(ctx)).decode(errors="replace")
     # error classes of the reference (std::invalid_argument / std::domain_error)
     if rc == SHTC_EINVAL:
         raise ValueError(msg)

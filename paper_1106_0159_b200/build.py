@@ -24,7 +24,7 @@ CLI_BIN = PKG / "sht_b200"
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "--expt-relaxed-constexpr", "-Xcompiler", "-fPIC",
               "-Xcompiler", "-O2", "-Xptxas", "-v"] + ARCH
-CU_SOURCES = ["legendre.cu", "ringfft.cu", "shtc.cu"]
+CU_SOURCES = ["legendre.cu", "ringfft.cu", "shtc.cu", "group.cu"]
 
 
 def nvcc() -> str:
@@ -64,7 +64,7 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         if verbose:
             print(ptxas_log.read_text())
     if force or jobs or not LIB.exists():
-        _run([nvcc(), "-shared", *ARCH, "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart"])
+        _run([nvcc(), "-shared", *ARCH, "-o", str(LIB) + ".tmp", *map(str, objs), "-lcudart", "-ldl"])
         os.replace(str(LIB) + ".tmp", LIB)
     build_dropin(force=force)
     return LIB
@@ -105,7 +105,7 @@ def build_variant(name: str, defines: list[str], flags: list[str] | None = None)
         res = list(ex.map(_run, jobs))
     (d / "ptxas.log").write_text("".join(r.stderr for r in res))
     lib = d / "libshtc.so"
-    _run([nvcc(), "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lcudart"])
+    _run([nvcc(), "-shared", *ARCH, "-o", str(lib), *map(str, objs), "-lcudart", "-ldl"])
     return lib
 
 

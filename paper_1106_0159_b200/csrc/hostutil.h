@@ -1,0 +1,121 @@
+// Host-side helpers shared by the context (shtc.cu) and the multi-GPU group (group.cu):
+// page-locked detection and the host copy pool that stages pageable buffers on all cores.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <condition_variable>
+#include <cstring>
+#include <functional>
+#include <mutex>
+#include <thread>
+#include <vector>
+
+namespace shtc_host {
+
+// host memory the copy engines can read / write directly (cudaHostAlloc, cudaHostRegister,
+// pinned torch tensors); pageable memory (std::vector, numpy) goes through PinnedBuf staging
+inline bool host_pinned(const void* p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeHost;
+}
+
+// Persistent host worker pool for the staging copies (process-wide; threads start on first use
+// and park on a condition variable between jobs).
+class CopyPool {
+public:
+    static CopyPool& get() {
+        static CopyPool pool;
+        return pool;
+    }
+    unsigned size() const { return (unsigned)workers_.size() + 1; }
+    // run fn(i) for i in [0, n) on the workers and the calling thread; returns when all are done
+    void run(unsigned n, const std::function<void(unsigned)>& fn) {
+        std::unique_lock<std::mutex> job_lock(job_mu_);  // one job at a time
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            fn_ = &fn;
+            n_ = n;
+            next_ = 1;  // index 0 runs on the caller
+            pending_ = n - 1;
+            ++gen_;
+        }
+        cv_.notify_all();
+        fn(0);
+        for (;;) {  // the caller takes pieces too
+            unsigned i;
+            {
+                std::lock_guard<std::mutex> lk(mu_);
+                if (next_ >= n_) break;
+                i = next_++;
+            }
+            fn(i);
+            std::lock_guard<std::mutex> lk(mu_);
+            if (--pending_ == 0) done_.notify_all();
+        }
+        std::unique_lock<std::mutex> lk(mu_);
+        done_.wait(lk, [&] { return pending_ == 0; });
+        fn_ = nullptr;
+    }
+    ~CopyPool() {
+        {
+            std::lock_guard<std::mutex> lk(mu_);
+            stop_ = true;
+            ++gen_;
+        }
+        cv_.notify_all();
+        for (auto& t : workers_) t.join();
+    }
+
+private:
+    CopyPool() {
+        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
+    }
+    void loop() {
+        unsigned seen = 0;
+        for (;;) {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return stop_ || (gen_ != seen && fn_ && next_ < n_); });
+            if (stop_) return;
+            seen = gen_;
+            while (fn_ && next_ < n_) {
+                const unsigned i = next_++;
+                const std::function<void(unsigned)>* fn = fn_;
+                lk.unlock();
+                (*fn)(i);
+                lk.lock();
+                if (--pending_ == 0) done_.notify_all();
+            }
+        }
+    }
+    std::vector<std::thread> workers_;
+    std::mutex mu_, job_mu_;
+    std::condition_variable cv_, done_;
+    const std::function<void(unsigned)>* fn_ = nullptr;
+    unsigned n_ = 0, next_ = 0, pending_ = 0, gen_ = 0;
+    bool stop_ = false;
+};
+
+// memcpy on all host cores (pageable <-> staging copies are bound by host memory bandwidth)
+inline void par_memcpy(void* dst, const void* src, size_t bytes) {
+    CopyPool& pool = CopyPool::get();
+    const size_t min_piece = size_t(2) << 20;
+    const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(pool.size(), bytes / min_piece));
+    if (nt <= 1) {
+        std::memcpy(dst, src, bytes);
+        return;
+    }
+    const size_t piece = (bytes / nt + 63) & ~size_t(63);
+    pool.run(nt, [&](unsigned i) {
+        const size_t b = std::min(bytes, piece * i), e = i + 1 == nt ? bytes : std::min(bytes, piece * (i + 1));
+        if (e > b) std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+    });
+}
+
+}  // namespace shtc_host

@@ -96,6 +96,10 @@ struct LegPlanView {
     // fused exchange (alm2map): ring r's output row is row_ptr[r] (an address in the ring
     // owner's receive buffer, peer memory) instead of delta + row_off[r]; nullptr: local
     double2* const* row_ptr;
+    // ScaleLadder::unscaled() (legendre.hpp:26-47, the reference's transparency check): no
+    // rescaling, so a stream counts from its seed if the seed is at scale k == 0 and never
+    // otherwise (plan-time only: it changes the activation scan)
+    int unscaled;
 };
 
 void launch_leg_tables(const int* ms_dev, int n_m, int lmax, LegTables tab, cudaStream_t s);

@@ -149,7 +149,8 @@ __global__ void leg_scan_kernel(LegPlanView p, int* __restrict__ act_out, double
     }
     int act = (valid && k == 0) ? 0 : INT_MAX;
     double2 ck = make_double2(0.0, act == 0 ? q1 : 0.0);  // state at activation (k == 0 scale)
-    bool done = !valid || k == 0;
+    // unscaled ladder: the scale never changes, so a seed below k == 0 never counts
+    bool done = !valid || k == 0 || p.unscaled;
     const double* __restrict__ A = p.tab.A + p.tab.tab_off[mi];
     const double* __restrict__ T = p.tab.T + p.tab.tab_off[mi];
     for (int i = 1; i <= n; ++i) {

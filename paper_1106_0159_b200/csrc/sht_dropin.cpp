@@ -15,6 +15,7 @@
 // handle); calls are serialised by a mutex.  SHT_DEVICE selects the CUDA device.
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -52,12 +53,76 @@ void ok(shtc_status st, const shtc_ctx* c) {
     if (st != SHTC_OK) raise(st, c);
 }
 
+struct GridKey {
+    std::vector<double> cos, phi0, w;
+    std::vector<int> nphi;
+    int mirror = -1;
+    bool operator==(const GridKey&) const = default;
+};
+
+GridKey grid_key(const PixelGrid& g, bool mirror) {
+    GridKey k;
+    for (const auto& r : g.rings) {
+        k.cos.push_back(r.cos_theta);
+        k.phi0.push_back(r.phi_0);
+        k.w.push_back(r.weight);
+        k.nphi.push_back(r.n_phi);
+    }
+    k.mirror = mirror ? 1 : 0;
+    return k;
+}
+
+std::vector<int64_t> pixel_offsets(const PixelGrid& g) {
+    std::vector<int64_t> off;
+    for (const auto& r : g.rings) off.push_back(r.pixel_offset);
+    return off;
+}
+
+// Devices of an n-worker group: SHT_DEVICES="0,1,..." (worker i on entry i mod its length), else
+// worker i on device i mod the device count (workers share a device on smaller boxes)
+std::vector<int32_t> worker_devices(int n) {
+    std::vector<int32_t> list;
+    if (const char* e = std::getenv("SHT_DEVICES")) {
+        for (const char* q = e; *q;) {
+            list.push_back(std::atoi(q));
+            while (*q && *q != ',') ++q;
+            if (*q) ++q;
+        }
+    }
+    if (list.empty()) {
+        const int nd = std::max(1, shtc_device_count());
+        for (int i = 0; i < nd; ++i) list.push_back(i);
+    }
+    std::vector<int32_t> d(n);
+    for (int i = 0; i < n; ++i) d[i] = list[i % list.size()];
+    return d;
+}
+
+[[noreturn]] void raise_group(shtc_status st, const shtc_group* g) {
+    const std::string msg = shtc_group_last_error(g);
+    switch (st) {
+        case SHTC_EINVAL: throw std::invalid_argument(msg);
+        case SHTC_EDOMAIN: throw std::domain_error(msg);
+        default: throw std::runtime_error("sht (B200): " + msg);
+    }
+}
+
+void gok(shtc_status st, const shtc_group* g) {
+    if (st != SHTC_OK) raise_group(st, g);
+}
+
 struct Engine {
     std::mutex mu;
     shtc_ctx* ctx = nullptr;
-    std::vector<double> g_cos, g_phi0, g_w;
-    std::vector<int> g_nphi;
+    GridKey grid;
     int lmax = -1, mmax = -1;
+    bool ladder = true;
+    // multi-worker layouts: one shtc_group (W device contexts) per worker count in use
+    shtc_group* grp = nullptr;
+    int grp_workers = 0;
+    GridKey grp_grid;
+    int grp_lmax = -1, grp_mmax = -1;
+    std::vector<std::vector<int>> grp_msets, grp_rsets;
 
     shtc_ctx* get() {
         if (!ctx) {
@@ -66,27 +131,16 @@ struct Engine {
         }
         return ctx;
     }
-    void bind(const PixelGrid& g, int lmax_, int mmax_) {
+    void bind(const PixelGrid& g, int lmax_, int mmax_, bool mirror) {
         shtc_ctx* c = get();
-        std::vector<double> cs(g.rings.size()), p0(g.rings.size()), w(g.rings.size());
-        std::vector<int> np(g.rings.size());
-        std::vector<int64_t> off(g.rings.size());
-        for (size_t i = 0; i < g.rings.size(); ++i) {
-            cs[i] = g.rings[i].cos_theta;
-            p0[i] = g.rings[i].phi_0;
-            w[i] = g.rings[i].weight;
-            np[i] = g.rings[i].n_phi;
-            off[i] = g.rings[i].pixel_offset;
-        }
-        if (cs != g_cos || p0 != g_phi0 || w != g_w || np != g_nphi) {
-            std::vector<int32_t> np32(np.begin(), np.end());
-            ok(shtc_set_grid(c, (int)cs.size(), cs.data(), np32.data(), p0.data(), w.data(),
-                             off.data(), 1),
+        GridKey k = grid_key(g, mirror);
+        if (!(k == grid)) {
+            std::vector<int32_t> np32(k.nphi.begin(), k.nphi.end());
+            const auto off = pixel_offsets(g);
+            ok(shtc_set_grid(c, (int)k.cos.size(), k.cos.data(), np32.data(), k.phi0.data(), k.w.data(), off.data(),
+                             mirror ? 1 : 0),
                c);
-            g_cos = cs;
-            g_phi0 = p0;
-            g_w = w;
-            g_nphi = np;
+            grid = std::move(k);
             lmax = mmax = -1;
         }
         if (lmax != lmax_ || mmax != mmax_) {
@@ -94,6 +148,58 @@ struct Engine {
             lmax = lmax_;
             mmax = mmax_;
         }
+    }
+    void set_ladder(const ScaleLadder& l) {
+        // the GPU plans know the reference's two ladders; any other window is refused
+        const bool standard = l.enabled && l.step == 0x1p512 && l.inv_step == 0x1p-512 && l.hi == 0x1p512 &&
+                              l.lo == 0x1p-512;
+        if (l.enabled && !standard)
+            throw std::invalid_argument("ScaleLadder: only ScaleLadder::standard() and ScaleLadder::unscaled() "
+                                        "are supported by the GPU plans");
+        shtc_ctx* c = get();
+        if (ladder != l.enabled) {
+            ok(shtc_set_ladder(c, l.enabled ? 1 : 0), c);
+            ladder = l.enabled;
+        }
+    }
+    shtc_group* group(const PixelGrid& g, const WorkerLayout& l, int lmax_, int mmax_, bool mirror) {
+        const int W = l.n_workers;
+        if (grp && grp_workers != W) {
+            shtc_group_destroy(grp);
+            grp = nullptr;
+        }
+        if (!grp) {
+            const char* ex = std::getenv("SHT_EXCHANGE");
+            const int mode = (ex && std::string(ex) == "nccl") ? SHTC_EXCHANGE_NCCL : SHTC_EXCHANGE_PEER;
+            const auto devs = worker_devices(W);
+            gok(shtc_group_create(W, devs.data(), mode, &grp), nullptr);
+            grp_workers = W;
+            grp_grid = GridKey{};
+            grp_msets.clear();
+        }
+        GridKey k = grid_key(g, mirror);
+        if (!(k == grp_grid)) {
+            std::vector<int32_t> np32(k.nphi.begin(), k.nphi.end());
+            const auto off = pixel_offsets(g);
+            gok(shtc_group_set_grid(grp, (int)k.cos.size(), k.cos.data(), np32.data(), k.phi0.data(), k.w.data(),
+                                    off.data(), mirror ? 1 : 0),
+                grp);
+            grp_grid = std::move(k);
+            grp_msets.clear();
+        }
+        if (grp_msets != l.m_sets || grp_rsets != l.ring_sets || grp_lmax != lmax_ || grp_mmax != mmax_) {
+            std::vector<int32_t> mo(mmax_ + 1), ro(g.n_rings());
+            for (int w = 0; w < W; ++w) {
+                for (int m : l.m_sets[w]) mo[m] = w;
+                for (int r : l.ring_sets[w]) ro[r] = w;
+            }
+            gok(shtc_group_set_layout(grp, lmax_, mmax_, mo.data(), ro.data()), grp);
+            grp_msets = l.m_sets;
+            grp_rsets = l.ring_sets;
+            grp_lmax = lmax_;
+            grp_mmax = mmax_;
+        }
+        return grp;
     }
 };
 
@@ -289,7 +395,7 @@ std::string to_string(GridScheme s) {
 // ---- Legendre-stage operators --------------------------------------------------------------
 namespace {
 DeltaPanel delta_panel(const AlmSet& alm, std::span<const double> x, std::span<const int> m_set,
-                       std::uint64_t* steps, const char* where) {
+                       const ScaleLadder& ladder, std::uint64_t* steps, const char* where) {
     auto ms = checked_m_set(m_set, alm.mmax, where);
     check_latitudes(x, where);
     DeltaPanel p;
@@ -300,6 +406,7 @@ DeltaPanel delta_panel(const AlmSet& alm, std::span<const double> x, std::span<c
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
     shtc_ctx* c = e.get();
+    e.set_ladder(ladder);
     std::vector<int32_t> ms32(ms.begin(), ms.end());
     ok(shtc_delta_a(c, reinterpret_cast<const double*>(alm.values.data()), alm.lmax, alm.mmax,
                     (int)x.size(), x.data(), (int)ms32.size(), ms32.data(),
@@ -309,7 +416,7 @@ DeltaPanel delta_panel(const AlmSet& alm, std::span<const double> x, std::span<c
 }
 
 AlmSet accumulate_core(const DeltaPanel& panel, std::span<const double> x, int lmax, int mmax,
-                       std::uint64_t* steps, const char* where) {
+                       const ScaleLadder& ladder, std::uint64_t* steps, const char* where) {
     if (lmax < mmax || mmax < 0) throw std::invalid_argument(std::string(where) + ": need lmax >= mmax >= 0");
     if (x.size() != panel.rings.size())
         throw std::invalid_argument(std::string(where) + ": latitude count != panel rings");
@@ -339,6 +446,7 @@ AlmSet accumulate_core(const DeltaPanel& panel, std::span<const double> x, int l
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
     shtc_ctx* c = e.get();
+    e.set_ladder(ladder);
     for (const auto& cols : groups) {
         std::vector<int32_t> ms32;
         std::vector<cdouble> sub(nr * cols.size());
@@ -356,33 +464,33 @@ AlmSet accumulate_core(const DeltaPanel& panel, std::span<const double> x, int l
 }  // namespace
 
 DeltaPanel compute_delta_a(const AlmSet& alm, std::span<const double> cos_thetas,
-                           std::span<const int> m_set, const ScaleLadder&, std::uint64_t* step_counter) {
-    return delta_panel(alm, cos_thetas, m_set, step_counter, "compute_delta_a");
+                           std::span<const int> m_set, const ScaleLadder& ladder, std::uint64_t* step_counter) {
+    return delta_panel(alm, cos_thetas, m_set, ladder, step_counter, "compute_delta_a");
 }
 
 DeltaPanel compute_delta_a_ring_major(const AlmSet& alm, std::span<const double> cos_thetas,
-                                      std::span<const int> m_set, int n_work_items, const ScaleLadder&,
+                                      std::span<const int> m_set, int n_work_items, const ScaleLadder& ladder,
                                       std::uint64_t* step_counter) {
     if (n_work_items < 1)
         throw std::invalid_argument("compute_delta_a_ring_major: n_work_items must be >= 1");
-    return delta_panel(alm, cos_thetas, m_set, step_counter, "compute_delta_a_ring_major");
+    return delta_panel(alm, cos_thetas, m_set, ladder, step_counter, "compute_delta_a_ring_major");
 }
 
 AlmSet accumulate_alm(const DeltaPanel& panel, std::span<const double> cos_thetas, int lmax, int mmax,
-                      const ScaleLadder&, std::uint64_t* step_counter) {
+                      const ScaleLadder& ladder, std::uint64_t* step_counter) {
     for (size_t i = 0; i < panel.rings.size(); ++i)
         if (panel.rings[i] != static_cast<int>(i))
             throw std::invalid_argument("accumulate_alm: ring coverage incomplete");
-    return accumulate_core(panel, cos_thetas, lmax, mmax, step_counter, "accumulate_alm");
+    return accumulate_core(panel, cos_thetas, lmax, mmax, ladder, step_counter, "accumulate_alm");
 }
 
 PartialAlm accumulate_alm_partial(const DeltaPanel& panel, std::span<const double> cos_thetas, int lmax,
-                                  int mmax, const ScaleLadder&, std::uint64_t* step_counter) {
+                                  int mmax, const ScaleLadder& ladder, std::uint64_t* step_counter) {
     for (size_t i = 1; i < panel.rings.size(); ++i)
         if (panel.rings[i] <= panel.rings[i - 1])
             throw std::invalid_argument("accumulate_alm_partial: rings not strictly ascending");
     PartialAlm p;
-    p.alm = accumulate_core(panel, cos_thetas, lmax, mmax, step_counter, "accumulate_alm_partial");
+    p.alm = accumulate_core(panel, cos_thetas, lmax, mmax, ladder, step_counter, "accumulate_alm_partial");
     p.rings = panel.rings;
     return p;
 }
@@ -413,32 +521,55 @@ uint64_t streams_of(const PixelGrid& g, PairPolicy pp) {
     return pp == PairPolicy::mirror ? (uint64_t)(g.n_rings() + 1) / 2 : (uint64_t)g.n_rings();
 }
 
-SkyMap run_synthesis(const AlmSet& alm, const PixelGrid& grid, PairPolicy pairing, shtc_timing* t) {
-    if (grid.n_rings() == 0) throw std::invalid_argument("synthesis: empty grid");
-    check_latitudes(grid.cos_thetas(), "synthesis");
+using Clock = std::chrono::steady_clock;
+double seconds_since(Clock::time_point t0) { return std::chrono::duration<double>(Clock::now() - t0).count(); }
+
+// PairPolicy::mirror runs one stream per mirror ring pair (delta_a_columns_paired,
+// transforms.cpp:145-182) and needs a mirror-symmetric grid; PairPolicy::none one stream per
+// ring (delta_a_columns, :53-72)
+void check_grid(const PixelGrid& grid, PairPolicy pairing, const char* where) {
+    if (grid.n_rings() == 0) throw std::invalid_argument(std::string(where) + ": empty grid");
+    check_latitudes(grid.cos_thetas(), where);
     if (pairing == PairPolicy::mirror) (void)symmetric_ring_pairs(grid);
+}
+
+// binds the grid / band and builds the plan; returns the host-visible precompute seconds
+// (the reference's log_mu table + mirror pairs, here the GPU plan when it is (re)built)
+double bind_planned(Engine& e, const PixelGrid& grid, int lmax, int mmax, PairPolicy pairing) {
+    const auto t0 = Clock::now();
+    e.set_ladder(ScaleLadder::standard());
+    e.bind(grid, lmax, mmax, pairing == PairPolicy::mirror);
+    ok(shtc_plan(e.ctx, nullptr), e.ctx);
+    return seconds_since(t0);
+}
+
+SkyMap run_synthesis(const AlmSet& alm, const PixelGrid& grid, PairPolicy pairing, shtc_timing* t,
+                     double* precompute_s = nullptr) {
+    check_grid(grid, pairing, "synthesis");
     SkyMap map;
     map.grid = grid;
     map.pixels.assign(static_cast<size_t>(grid.n_pix), 0.0);
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
-    e.bind(grid, alm.lmax, alm.mmax);
+    const double pre = bind_planned(e, grid, alm.lmax, alm.mmax, pairing);
+    if (precompute_s) *precompute_s = pre;
     ok(shtc_alm2map(e.ctx, reinterpret_cast<const double*>(alm.values.data()), map.pixels.data(), t), e.ctx);
     return map;
 }
 
-AlmSet run_analysis(const SkyMap& map, int lmax, int mmax, PairPolicy pairing, shtc_timing* t) {
+AlmSet run_analysis(const SkyMap& map, int lmax, int mmax, PairPolicy pairing, shtc_timing* t,
+                    double* precompute_s = nullptr) {
     if (lmax < mmax || mmax < 0) throw std::invalid_argument("analysis: need lmax >= mmax >= 0");
     const PixelGrid& grid = map.grid;
     if (grid.n_rings() == 0) throw std::invalid_argument("analysis: empty grid");
     if (map.pixels.size() != static_cast<size_t>(grid.n_pix))
         throw std::invalid_argument("analysis: pixel count != grid");
-    check_latitudes(grid.cos_thetas(), "analysis");
-    if (pairing == PairPolicy::mirror) (void)symmetric_ring_pairs(grid);
+    check_grid(grid, pairing, "analysis");
     AlmSet out(lmax, mmax);
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
-    e.bind(grid, lmax, mmax);
+    const double pre = bind_planned(e, grid, lmax, mmax, pairing);
+    if (precompute_s) *precompute_s = pre;
     ok(shtc_map2alm(e.ctx, map.pixels.data(), reinterpret_cast<double*>(out.values.data()), t), e.ctx);
     return out;
 }
@@ -607,9 +738,36 @@ void check_layout(const WorkerLayout& l, const PixelGrid& g, int mmax, const Run
         throw std::invalid_argument(std::string(where) + ": mirror pairing needs the m-major kernel");
 }
 
-// The reference's per-(worker, thread) nominal step slots (distribution.cpp:324-347).
+// The ownership the drivers run: ring_sets must cover every ring exactly once, with the
+// reference exchange's own errors (ring_owners, distribution.cpp:215-228); m_sets must
+// partition 0..mmax (the reference leaves out-of-range orders undefined and sums overlapping
+// ones; the GPU drivers refuse both).
+void check_ownership(const WorkerLayout& l, const char* where) {
+    std::vector<int> ring_owner(l.n_rings, -1);
+    for (int w = 0; w < l.n_workers; ++w)
+        for (int r : l.ring_sets[w]) {
+            if (r < 0 || r >= l.n_rings || ring_owner[r] >= 0) throw std::invalid_argument("exchange: invalid ring layout");
+            ring_owner[r] = w;
+        }
+    for (int o : ring_owner)
+        if (o < 0) throw std::invalid_argument("exchange: ring layout gap");
+    std::vector<int> m_owner(l.mmax + 1, -1);
+    for (int w = 0; w < l.n_workers; ++w)
+        for (int m : l.m_sets[w]) {
+            if (m < 0 || m > l.mmax) throw std::invalid_argument(std::string(where) + ": order outside [0, mmax]");
+            if (m_owner[m] >= 0) throw std::invalid_argument(std::string(where) + ": order owned by two workers");
+            m_owner[m] = w;
+        }
+    for (int o : m_owner)
+        if (o < 0) throw std::invalid_argument(std::string(where) + ": m_sets do not cover 0..mmax");
+}
+
+// The reference's per-(worker, thread) nominal step slots (distribution.cpp:324-347) and stage
+// seconds (:313, :349, :355, :377): precompute = plan (re)build on the host API path, recurrence
+// = the Legendre stage, exchange = the Delta transpose (the wait between the stages on the fused
+// path, the NCCL time on the NCCL path; 0 with one worker), fft = the ring stage.
 void fill_profiler(Profiler* prof, const WorkerLayout& l, const PixelGrid& g, int lmax, const RunOptions& o,
-                   const shtc_timing& t) {
+                   double precompute_s, double leg_ms, double fft_ms, double exchange_ms) {
     if (!prof) return;
     prof->configure(l.n_workers, o.n_threads);
     const uint64_t streams = streams_of(g, o.pairing);
@@ -625,8 +783,11 @@ void fill_profiler(Profiler* prof, const WorkerLayout& l, const PixelGrid& g, in
             for (int th = 0; th < o.n_threads; ++th) *prof->step_slot(w, th) += streams * order_steps(lmax, parts[th]);
         }
     }
-    prof->recurrence_s += t.legendre_ms * 1e-3;
-    prof->fft_s += t.fft_ms * 1e-3;
+    prof->precompute_s += precompute_s;
+    prof->recurrence_s += leg_ms * 1e-3;
+    prof->fft_s += fft_ms * 1e-3;
+    prof->exchange_s += exchange_ms * 1e-3;
+    // ExchangeVolume::total of the reference transpose: every Delta entry once (self blocks too)
     prof->exchange_bytes += (uint64_t)g.n_rings() * (l.mmax + 1) * 16;
 }
 }  // namespace
@@ -634,12 +795,31 @@ void fill_profiler(Profiler* prof, const WorkerLayout& l, const PixelGrid& g, in
 SkyMap distributed_synthesis(const AlmSet& alm, const PixelGrid& grid, const WorkerLayout& layout,
                              const RunOptions& o) {
     check_layout(layout, grid, alm.mmax, o, "distributed_synthesis");
-    shtc_timing t{};
-    // worker-count invariant by construction (every order and every ring is computed by the
-    // same kernels whatever the partition); the multi-GPU run is bench.py's NCCL path
-    SkyMap m = run_synthesis(alm, grid, o.pairing, &t);
-    fill_profiler(o.profiler, layout, grid, alm.lmax, o, t);
-    return m;
+    check_ownership(layout, "distributed_synthesis");
+    if (layout.n_workers == 1) {
+        shtc_timing t{};
+        double pre = 0.0;
+        SkyMap m = run_synthesis(alm, grid, o.pairing, &t, &pre);
+        fill_profiler(o.profiler, layout, grid, alm.lmax, o, pre, t.legendre_ms, t.fft_ms, 0.0);
+        return m;
+    }
+    // W workers = W device contexts (worker i on device i mod the device count, or SHT_DEVICES)
+    check_grid(grid, o.pairing, "distributed_synthesis");
+    SkyMap map;
+    map.grid = grid;
+    map.pixels.assign(static_cast<size_t>(grid.n_pix), 0.0);
+    shtc_group_timing t{};
+    double pre = 0.0;
+    {
+        Engine& e = engine();
+        std::lock_guard<std::mutex> lock(e.mu);
+        const auto t0 = Clock::now();
+        shtc_group* g = e.group(grid, layout, alm.lmax, alm.mmax, o.pairing == PairPolicy::mirror);
+        pre = seconds_since(t0);
+        gok(shtc_group_alm2map(g, reinterpret_cast<const double*>(alm.values.data()), map.pixels.data(), &t), g);
+    }
+    fill_profiler(o.profiler, layout, grid, alm.lmax, o, pre, t.legendre_ms, t.fft_ms, t.exchange_ms);
+    return map;
 }
 
 AlmSet distributed_analysis(const SkyMap& map, int lmax, int mmax, const WorkerLayout& layout,
@@ -648,10 +828,28 @@ AlmSet distributed_analysis(const SkyMap& map, int lmax, int mmax, const WorkerL
     if (map.pixels.size() != static_cast<size_t>(map.grid.n_pix))
         throw std::invalid_argument("distributed_analysis: pixel count != grid");
     check_layout(layout, map.grid, mmax, o, "distributed_analysis");
-    shtc_timing t{};
-    AlmSet a = run_analysis(map, lmax, mmax, o.pairing, &t);
-    fill_profiler(o.profiler, layout, map.grid, lmax, o, t);
-    return a;
+    check_ownership(layout, "distributed_analysis");
+    if (layout.n_workers == 1) {
+        shtc_timing t{};
+        double pre = 0.0;
+        AlmSet a = run_analysis(map, lmax, mmax, o.pairing, &t, &pre);
+        fill_profiler(o.profiler, layout, map.grid, lmax, o, pre, t.legendre_ms, t.fft_ms, 0.0);
+        return a;
+    }
+    check_grid(map.grid, o.pairing, "distributed_analysis");
+    AlmSet out(lmax, mmax);
+    shtc_group_timing t{};
+    double pre = 0.0;
+    {
+        Engine& e = engine();
+        std::lock_guard<std::mutex> lock(e.mu);
+        const auto t0 = Clock::now();
+        shtc_group* g = e.group(map.grid, layout, lmax, mmax, o.pairing == PairPolicy::mirror);
+        pre = seconds_since(t0);
+        gok(shtc_group_map2alm(g, map.pixels.data(), reinterpret_cast<double*>(out.values.data()), &t), g);
+    }
+    fill_profiler(o.profiler, layout, map.grid, lmax, o, pre, t.legendre_ms, t.fft_ms, t.exchange_ms);
+    return out;
 }
 
 // ---- Profiler -----------------------------------------------------------------------------------

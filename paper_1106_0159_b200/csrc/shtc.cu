@@ -27,8 +27,12 @@
 #include "../../include/shtc.h"
 #include "common.cuh"
 #include "kernels.h"
+#include "hostutil.h"
 
 using namespace shtk;
+using shtc_host::host_pinned;
+using shtc_host::par_memcpy;
+using shtc_host::CopyPool;
 
 namespace {
 
@@ -72,110 +76,6 @@ struct PinnedBuf {
         return static_cast<T*>(p);
     }
 };
-
-// host memory the copy engines can read / write directly (cudaHostAlloc, cudaHostRegister,
-// pinned torch tensors); pageable memory (std::vector, numpy) goes through PinnedBuf staging
-bool host_pinned(const void* p) {
-    cudaPointerAttributes a{};
-    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
-        cudaGetLastError();
-        return false;
-    }
-    return a.type == cudaMemoryTypeHost;
-}
-
-// Persistent host worker pool for the staging copies (process-wide; threads start on first use
-// and park on a condition variable between jobs).
-class CopyPool {
-public:
-    static CopyPool& get() {
-        static CopyPool pool;
-        return pool;
-    }
-    unsigned size() const { return (unsigned)workers_.size() + 1; }
-    // run fn(i) for i in [0, n) on the workers and the calling thread; returns when all are done
-    void run(unsigned n, const std::function<void(unsigned)>& fn) {
-        std::unique_lock<std::mutex> job_lock(job_mu_);  // one job at a time
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            fn_ = &fn;
-            n_ = n;
-            next_ = 1;  // index 0 runs on the caller
-            pending_ = n - 1;
-            ++gen_;
-        }
-        cv_.notify_all();
-        fn(0);
-        for (;;) {  // the caller takes pieces too
-            unsigned i;
-            {
-                std::lock_guard<std::mutex> lk(mu_);
-                if (next_ >= n_) break;
-                i = next_++;
-            }
-            fn(i);
-            std::lock_guard<std::mutex> lk(mu_);
-            if (--pending_ == 0) done_.notify_all();
-        }
-        std::unique_lock<std::mutex> lk(mu_);
-        done_.wait(lk, [&] { return pending_ == 0; });
-        fn_ = nullptr;
-    }
-    ~CopyPool() {
-        {
-            std::lock_guard<std::mutex> lk(mu_);
-            stop_ = true;
-            ++gen_;
-        }
-        cv_.notify_all();
-        for (auto& t : workers_) t.join();
-    }
-
-private:
-    CopyPool() {
-        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-        for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
-    }
-    void loop() {
-        unsigned seen = 0;
-        for (;;) {
-            std::unique_lock<std::mutex> lk(mu_);
-            cv_.wait(lk, [&] { return stop_ || (gen_ != seen && fn_ && next_ < n_); });
-            if (stop_) return;
-            seen = gen_;
-            while (fn_ && next_ < n_) {
-                const unsigned i = next_++;
-                const std::function<void(unsigned)>* fn = fn_;
-                lk.unlock();
-                (*fn)(i);
-                lk.lock();
-                if (--pending_ == 0) done_.notify_all();
-            }
-        }
-    }
-    std::vector<std::thread> workers_;
-    std::mutex mu_, job_mu_;
-    std::condition_variable cv_, done_;
-    const std::function<void(unsigned)>* fn_ = nullptr;
-    unsigned n_ = 0, next_ = 0, pending_ = 0, gen_ = 0;
-    bool stop_ = false;
-};
-
-// memcpy on all host cores (pageable <-> staging copies are bound by host memory bandwidth)
-void par_memcpy(void* dst, const void* src, size_t bytes) {
-    CopyPool& pool = CopyPool::get();
-    const size_t min_piece = size_t(2) << 20;
-    const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(pool.size(), bytes / min_piece));
-    if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
-        return;
-    }
-    const size_t piece = (bytes / nt + 63) & ~size_t(63);
-    pool.run(nt, [&](unsigned i) {
-        const size_t b = std::min(bytes, piece * i), e = i + 1 == nt ? bytes : std::min(bytes, piece * (i + 1));
-        if (e > b) std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
-    });
-}
 
 struct DevBuf {
     void* p = nullptr;
@@ -326,6 +226,7 @@ struct shtc_ctx {
     std::vector<int> ms;
     bool band_set = false;
     std::vector<double> log_mu;
+    bool ladder = true;  // ScaleLadder::standard (false: ScaleLadder::unscaled)
     // exchange layout (stage API)
     bool custom_layout = false;
     std::vector<int64_t> row_off;
@@ -566,6 +467,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     v.st = LegStreams{P.sx.as<double>(), P.sl2.as<double>(), P.spos.as<int>(), P.sn.as<int>(),
                       P.ss.as<int>(), ns};
     v.n_tiles = (ns + LEG_TILE - 1) / LEG_TILE;
+    v.unscaled = c->ladder ? 0 : 1;
 
     if (n_m > 0) launch_leg_tables(v.ms, n_m, lmax, v.tab, s);
     CK(cudaGetLastError());
@@ -1251,6 +1153,16 @@ shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int3
         ctx->id_row_off.release();
         ctx->custom_layout = false;
         ctx->peers_set = false;
+    });
+}
+
+shtc_status shtc_set_ladder(shtc_ctx* ctx, int enabled) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        if ((enabled != 0) == ctx->ladder) return;
+        ctx->ladder = enabled != 0;
+        ctx->leg.built = false;
+        ctx->op_leg.built = false;
     });
 }
 
@@ -1940,7 +1852,7 @@ void op_plan(shtc_ctx* c, int lmax, int mmax, int n_lat, const double* x, int n_
     std::vector<int> mv(ms, ms + n_m);
     std::vector<double> xv(x, x + n_lat);
     if (c->op_leg.built && c->op_leg.lmax == lmax && c->op_leg.ms == mv && c->op_x == xv &&
-        (int)c->log_mu.size() >= mmax + 1)
+        c->op_leg.view.unscaled == (c->ladder ? 0 : 1))
         return;
     std::vector<double> lmu(mmax + 1);
     for (int m = 0; m <= mmax; ++m) lmu[m] = host_log_mu(m);

@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _lib
-from ._lib import Timing, check, lib
+from ._lib import GroupTiming, Timing, check, lib
 
 # ----------------------------------------------------------------------------------------
 # containers and geometry
@@ -483,6 +483,10 @@ class Context:
             self._check(lib().shtc_set_band(self._h, lmax, mmax, len(ms), _p(ms)))
         self.lmax, self.mmax = lmax, mmax
 
+    def set_ladder(self, enabled: bool = True):
+        """ScaleLadder::standard() (True) or ScaleLadder::unscaled() (False)."""
+        self._check(lib().shtc_set_ladder(self._h, int(bool(enabled))))
+
     def plan(self) -> float:
         t = C.c_double()
         self._check(lib().shtc_plan(self._h, C.byref(t)))
@@ -736,6 +740,97 @@ class PeerExchange:
             if p:
                 dev_free(p)
         self.send = self.recv = self.flags = 0
+
+
+class Group:
+    """Single-process multi-GPU transforms: W workers, worker i on devices[i] (default i mod the
+    device count) -- the C ABI shtc_group (distributed_synthesis / distributed_analysis,
+    distribution.cpp:300-490).  exchange="peer": the stage kernels store Delta straight into
+    the other workers' buffers (NVLink peer memory) and consumers wait on the producers'
+    events; "nccl": grouped ncclSend / ncclRecv (needs distinct devices)."""
+
+    def __init__(self, n_workers: int, devices=None, exchange: str = "peer"):
+        self._h = C.c_void_p()
+        mode = {"peer": _lib.SHTC_EXCHANGE_PEER, "nccl": _lib.SHTC_EXCHANGE_NCCL}[exchange]
+        d = None if devices is None else np.ascontiguousarray(devices, np.int32)
+        check(lib().shtc_group_create(int(n_workers), _p(d), mode, C.byref(self._h)), group=None)
+        self.n_workers = n_workers
+        self.exchange = exchange
+        self.grid = None
+        self.lmax = self.mmax = None
+
+    def _check(self, rc):
+        check(rc, group=self._h)
+
+    def close(self):
+        if getattr(self, "_h", None) and self._h.value:
+            lib().shtc_group_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def device(self, worker: int) -> int:
+        d = C.c_int()
+        self._check(lib().shtc_group_device(self._h, worker, C.byref(d)))
+        return d.value
+
+    def set_grid(self, grid: PixelGrid, mirror: bool = True):
+        self._check(lib().shtc_group_set_grid(self._h, grid.n_rings, _p(grid.cos_theta), _p(grid.n_phi),
+                                              _p(grid.phi_0), _p(grid.weight), _p(grid.pixel_offset),
+                                              int(bool(mirror))))
+        self.grid = grid
+
+    def set_layout(self, lmax: int, mmax: int, m_sets, ring_sets):
+        mo = np.full(mmax + 1, -1, np.int32)
+        ro = np.full(self.grid.n_rings, -1, np.int32)
+        for w, ms in enumerate(m_sets):
+            mo[np.asarray(ms, np.int64)] = w
+        for w, rs in enumerate(ring_sets):
+            ro[np.asarray(rs, np.int64)] = w
+        self._check(lib().shtc_group_set_layout(self._h, lmax, mmax, _p(mo), _p(ro)))
+        self.lmax, self.mmax = lmax, mmax
+
+    def plan_ms(self) -> float:
+        t = C.c_double()
+        self._check(lib().shtc_group_plan_ms(self._h, C.byref(t)))
+        return t.value
+
+    def alm2map(self, alm, out=None, timing=False):
+        alm = np.ascontiguousarray(alm, np.complex128)
+        if alm.size != alm_count(self.lmax, self.mmax):
+            raise ValueError("alm2map: coefficient count != AlmSet::count(lmax, mmax)")
+        mp = out if out is not None else np.empty(self.grid.n_pix)
+        t = GroupTiming()
+        self._check(lib().shtc_group_alm2map(self._h, _p(alm), _p(mp), C.byref(t)))
+        return (mp, t.as_dict()) if timing else mp
+
+    def map2alm(self, mp, out=None, timing=False):
+        mp = np.ascontiguousarray(mp, np.float64)
+        if mp.size != self.grid.n_pix:
+            raise ValueError("analysis: pixel count != grid")
+        alm = out if out is not None else np.empty(alm_count(self.lmax, self.mmax), np.complex128)
+        t = GroupTiming()
+        self._check(lib().shtc_group_map2alm(self._h, _p(mp), _p(alm), C.byref(t)))
+        return (alm, t.as_dict()) if timing else alm
+
+    def alm2map_dev(self, alm_ptrs, map_ptrs):
+        """Per-worker device buffers (full triangle / full map on each worker's device)."""
+        a = np.ascontiguousarray(alm_ptrs, np.uint64)
+        m = np.ascontiguousarray(map_ptrs, np.uint64)
+        t = GroupTiming()
+        self._check(lib().shtc_group_alm2map_dev(self._h, _p(a), _p(m), C.byref(t)))
+        return t.as_dict()
+
+    def map2alm_dev(self, map_ptrs, alm_ptrs):
+        m = np.ascontiguousarray(map_ptrs, np.uint64)
+        a = np.ascontiguousarray(alm_ptrs, np.uint64)
+        t = GroupTiming()
+        self._check(lib().shtc_group_map2alm_dev(self._h, _p(m), _p(a), C.byref(t)))
+        return t.as_dict()
 
 
 def default_context(device: int = 0) -> Context:

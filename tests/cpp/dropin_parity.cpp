@@ -2,6 +2,7 @@
 // against the reference itself (oracle/_ref/libsht_ref.so through its C shim).  Restates the
 // reference's own unit tests (test_transforms.cpp, test_distribution.cpp) on the GPU path.
 // Built and run by tests/test_gpu_cpp.py; prints "PASS n" / "FAIL ..." lines.
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdint>
@@ -168,17 +169,26 @@ int main() {
         auto back = sht::analysis(sht::synthesis(alm, g), 32, 32);
         CHECK(sht::roundtrip_error(alm, back) <= 1e-13, "GL round trip");
     }
-    // distributed drivers: worker/thread invariance and profiler slots (test_distribution.cpp:256-352)
+    // distributed drivers: worker/thread invariance and profiler slots (test_distribution.cpp:256-352).
+    // W > 1 runs W device contexts (shtc_group: worker i on device i mod the device count),
+    // the Delta exchange as fused peer stores; synthesis is bitwise worker invariant, analysis
+    // sums each order's ring partials in the same kernels (<= 1e-14 of the one-worker result)
     {
         auto g = sht::build_gauss_legendre_grid(128, 256);
         auto alm = make_random_alm(127, 127, 2024);
         auto ref_map = sht::synthesis(alm, g);
-        for (int n : {1, 2, 4, 8})
+        auto ref_alm = sht::analysis(ref_map, 127, 127);
+        for (int n : {1, 2, 3, 4, 8})
             for (int t : {1, 4}) {
                 sht::RunOptions o;
                 o.n_threads = t;
-                auto m = sht::distributed_synthesis(alm, g, sht::WorkerLayout::create(g, 127, n), o);
+                auto layout = sht::WorkerLayout::create(g, 127, n);
+                auto m = sht::distributed_synthesis(alm, g, layout, o);
                 CHECK(m.pixels == ref_map.pixels, "distributed synthesis worker invariance");
+                auto a = sht::distributed_analysis(ref_map, 127, 127, layout, o);
+                CHECK(rel_rms(reinterpret_cast<const double*>(a.values.data()),
+                              reinterpret_cast<const double*>(ref_alm.values.data()), 2 * a.values.size()) <= 1e-14,
+                      "distributed analysis worker invariance");
             }
         sht::Profiler prof;
         sht::RunOptions o;
@@ -188,12 +198,128 @@ int main() {
         uint64_t want = 0;
         for (int m = 0; m <= 127; ++m) want += (uint64_t)g.n_rings() * (127 - m + 1);
         CHECK(prof.total_steps() == want, "profiler total steps");
+        CHECK(prof.recurrence_s > 0 && prof.fft_s > 0 && prof.exchange_s >= 0 && prof.precompute_s >= 0,
+              "profiler stage seconds");
+        CHECK(prof.exchange_bytes == (uint64_t)g.n_rings() * 128 * 16, "profiler exchange bytes");
+        // a new layout (W = 3) rebuilds the plans: the precompute stage is timed
+        sht::Profiler prof3;
+        o.profiler = &prof3;
+        (void)sht::distributed_analysis(ref_map, 127, 127, sht::WorkerLayout::create(g, 127, 3), o);
+        CHECK(prof3.precompute_s > 0 && prof3.recurrence_s > 0, "profiler precompute on a plan rebuild");
         sht::RunOptions bad;
         bad.kernel = sht::KernelOrder::ring_major;
         bad.pairing = sht::PairPolicy::mirror;
         bool threw = false;
         try { (void)sht::distributed_synthesis(alm, g, sht::WorkerLayout::create(g, 127, 2), bad); } catch (const std::invalid_argument&) { threw = true; }
         CHECK(threw, "mirror + ring_major rejected");
+    }
+    // distributed drivers against the reference at HEALPix nside 64 / lmax 128, mirror pairing,
+    // W = 1, 2, 4, 8 workers (distribution.cpp:300-490 run by the reference with the same layout)
+    {
+        const int ns = 64, lmax = 128;
+        auto g = sht::build_healpix_grid(ns);
+        auto alm = sht::random_alm(lmax, lmax, 12345);
+        RefGrid rg(g);
+        std::vector<double> want(g.n_pix);
+        uint64_t steps = 0;
+        ref_synthesis(lmax, lmax, reinterpret_cast<const double*>(alm.values.data()), 0, ns, g.n_rings(),
+                      rg.c.data(), rg.n.data(), rg.p.data(), rg.w.data(), 1, 0, want.data(), &steps);
+        std::vector<double> aw(2 * alm.values.size());
+        ref_analysis(lmax, lmax, want.data(), 0, ns, g.n_rings(), rg.c.data(), rg.n.data(), rg.p.data(),
+                     rg.w.data(), 1, aw.data(), &steps);
+        sht::SkyMap in{g, want};
+        for (int n : {1, 2, 4, 8}) {
+            sht::RunOptions o;
+            o.pairing = sht::PairPolicy::mirror;
+            auto layout = sht::WorkerLayout::create(g, lmax, n);
+            auto m = sht::distributed_synthesis(alm, g, layout, o);
+            CHECK(rel_rms(m.pixels.data(), want.data(), want.size()) <= 1e-12, "distributed synthesis vs reference");
+            auto a = sht::distributed_analysis(in, lmax, lmax, layout, o);
+            CHECK(rel_rms(reinterpret_cast<const double*>(a.values.data()), aw.data(), aw.size()) <= 1e-12,
+                  "distributed analysis vs reference");
+        }
+        // layouts the reference's exchange refuses (ring_owners, distribution.cpp:215-228)
+        auto layout = sht::WorkerLayout::create(g, lmax, 2);
+        auto overlap = layout;
+        overlap.ring_sets[1].push_back(overlap.ring_sets[0][0]);
+        auto gap = layout;
+        gap.ring_sets[1].pop_back();
+        auto m_dup = layout;
+        m_dup.m_sets[1].push_back(m_dup.m_sets[0][0]);
+        std::string e1, e2;
+        int n = 0;
+        try { (void)sht::distributed_synthesis(alm, g, overlap); } catch (const std::invalid_argument& e) { e1 = e.what(); ++n; }
+        try { (void)sht::distributed_analysis(in, lmax, lmax, gap); } catch (const std::invalid_argument& e) { e2 = e.what(); ++n; }
+        try { (void)sht::distributed_synthesis(alm, g, m_dup); } catch (const std::invalid_argument&) { ++n; }
+        CHECK(n == 3 && e1 == "exchange: invalid ring layout" && e2 == "exchange: ring layout gap",
+              "distributed layout errors");
+    }
+    // mirror pairing reproduces the unpaired transforms (test_transforms.cpp:364-388); the
+    // default PairPolicy::none runs unpaired streams, matching the reference's unpaired path
+    for (auto [g, lmax] : std::vector<std::pair<sht::PixelGrid, int>>{{sht::build_healpix_grid(8), 20},
+                                                                      {sht::build_gauss_legendre_grid(10, 24), 9}}) {
+        auto alm = make_random_alm(lmax, lmax, 77);
+        sht::TransformOptions paired;
+        paired.pairing = sht::PairPolicy::mirror;
+        auto plain_map = sht::synthesis(alm, g);
+        auto paired_map = sht::synthesis(alm, g, paired);
+        double worst = 0, peak = 0;
+        for (size_t i = 0; i < plain_map.pixels.size(); ++i) {
+            worst = std::max(worst, std::fabs(plain_map.pixels[i] - paired_map.pixels[i]));
+            peak = std::max(peak, std::fabs(plain_map.pixels[i]));
+        }
+        CHECK(worst <= 1e-12 * std::max(1.0, peak), "mirror vs unpaired synthesis");
+        auto plain_alm = sht::analysis(plain_map, lmax, lmax);
+        auto paired_alm = sht::analysis(plain_map, lmax, lmax, paired);
+        CHECK(rel_rms(reinterpret_cast<const double*>(paired_alm.values.data()),
+                      reinterpret_cast<const double*>(plain_alm.values.data()), 2 * plain_alm.values.size()) <= 1e-12,
+              "mirror vs unpaired analysis");
+        RefGrid rg(g);
+        std::vector<double> want(g.n_pix);
+        uint64_t steps = 0;
+        ref_synthesis(lmax, lmax, reinterpret_cast<const double*>(alm.values.data()), g.scheme == sht::GridScheme::healpix_ring ? 0 : 1,
+                      g.nside, g.n_rings(), rg.c.data(), rg.n.data(), rg.p.data(), rg.w.data(), 0, 0, want.data(), &steps);
+        CHECK(rel_rms(plain_map.pixels.data(), want.data(), want.size()) <= 1e-13, "unpaired synthesis vs reference");
+    }
+    // ScaleLadder::unscaled (test_transforms.cpp:150-167): identical panels where no stream
+    // leaves the window; where seeds lie below it (m = 2000 at x = 0.999) the unscaled streams
+    // never count, exactly as the reference's
+    {
+        auto [x, w] = sht::gauss_legendre_nodes(41);
+        auto alm = make_random_alm(40, 40, 91);
+        std::vector<int> ms(41);
+        std::iota(ms.begin(), ms.end(), 0);
+        auto by_m = sht::compute_delta_a(alm, x, ms);
+        auto unscaled = sht::compute_delta_a(alm, x, ms, sht::ScaleLadder::unscaled());
+        CHECK(unscaled.entries == by_m.entries, "unscaled ladder: identical panels");
+        const int m = 2000, lmax = 2200;
+        sht::AlmSet deep(lmax, lmax);
+        std::mt19937 gen(5);
+        std::normal_distribution<double> nd;
+        for (int l = m; l <= lmax; ++l) deep.at(l, m) = cdouble{nd(gen), 0.0};
+        const std::vector<double> xs{0.999, 0.9, 0.5, -0.3, 0.0};
+        const std::vector<int> one{m};
+        std::vector<int32_t> one32{m};
+        for (bool uns : {false, true}) {
+            auto got = sht::compute_delta_a(deep, xs, one, uns ? sht::ScaleLadder::unscaled() : sht::ScaleLadder::standard());
+            std::vector<double> want(2 * xs.size());
+            uint64_t st = 0;
+            ref_compute_delta_a(lmax, lmax, reinterpret_cast<const double*>(deep.values.data()), (int)xs.size(), xs.data(), 1,
+                                one32.data(), 0, 1, uns ? 1 : 0, want.data(), &st);
+            double worst = 0, peak = 0;
+            for (size_t i = 0; i < want.size(); ++i) {
+                worst = std::max(worst, std::fabs(reinterpret_cast<const double*>(got.entries.data())[i] - want[i]));
+                peak = std::max(peak, std::fabs(want[i]));
+            }
+            CHECK(worst <= 1e-10 * std::max(peak, 1e-300), uns ? "unscaled deep order vs reference" : "standard deep order vs reference");
+            if (uns) CHECK(got.entries[0] == cdouble(0.0, 0.0), "unscaled: seed below the window never counts");
+            else CHECK(got.entries[0] != cdouble(0.0, 0.0), "standard: the ladder activates the deep stream");
+        }
+        sht::ScaleLadder custom;
+        custom.hi = 0x1p256;
+        bool threw = false;
+        try { (void)sht::compute_delta_a(alm, x, ms, custom); } catch (const std::invalid_argument&) { threw = true; }
+        CHECK(threw, "non-reference ladder window rejected");
     }
     // argument errors (test_transforms.cpp:426-470)
     {
