@@ -176,3 +176,23 @@ def test_host_pipeline_matches_device_path(gpu_ctx, nside, lmax):
     assert np.array_equal(map_pin, want_map)
     gpu_ctx.map2alm(map_pin, out=out_pin)
     assert np.array_equal(out_pin, first)
+
+
+@pytest.mark.parametrize("unscaled", [False, True])
+def test_ladder_modes_match_reference(gpu_ctx, unscaled):
+    """ScaleLadder::standard vs ::unscaled (legendre.hpp:26-47): at m = 1500, x = 0.5 the seed
+    (~2^-305) lies below the window, so the standard ladder activates the stream later while the
+    unscaled one never counts it; elsewhere both agree (test_transforms.cpp:150-167)."""
+    m, lmax = 1500, 2200
+    alm = ref.random_alm(lmax, lmax, 31)
+    x = np.array([0.5, 0.3, 0.0, 0.6, -0.5, 0.999])
+    ms = [0, 7, 800, 1500, 2100]
+    want, wsteps = ref.compute_delta_a(alm, lmax, lmax, x, ms, unscaled=unscaled)
+    gpu_ctx.set_ladder(not unscaled)
+    try:
+        got, steps = gpu_ctx.delta_a(alm, lmax, lmax, x, ms)
+    finally:
+        gpu_ctx.set_ladder(True)
+    assert steps == wsteps
+    assert rel_rms(got, want) <= 1e-12, rel_rms(got, want)
+    assert (got[0, 3] == 0) == unscaled and (want[0, 3] == 0) == unscaled
