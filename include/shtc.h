@@ -94,14 +94,17 @@ shtc_status shtc_set_ladder(shtc_ctx* ctx, int enabled);
 /* Builds (and caches) the Legendre plan (recurrence tables, underflow activation scan)
  * and the ring-FFT plan; otherwise built lazily by the first transform. */
 shtc_status shtc_plan(shtc_ctx* ctx, double* plan_ms);
-/* Exact pair-step accounting of the plan: nominal, executed (after dead-tile skipping),
- * useful (steps whose term the reference keeps, i.e. ladder scale k == 0). */
+/* Exact pair-step accounting of the plan: nominal, executed (map2alm, after dead-tile
+ * skipping; its passes run tile pairs from the earlier start), useful (steps whose term the
+ * reference keeps, i.e. ladder scale k == 0). */
 shtc_status shtc_plan_stats(shtc_ctx* ctx, uint64_t* nominal, uint64_t* executed,
                             uint64_t* useful);
 /* Executed pair-steps split by kernel phase: before the tile's first activation (recurrence +
  * ladder check only), inside the activation window (checked), after it (unchecked). */
 shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* checked,
                                   uint64_t* fast);
+/* Executed pair-steps per transform: alm2map (single-tile items) and map2alm (tile pairs). */
+shtc_status shtc_plan_executed(shtc_ctx* ctx, uint64_t* alm2map, uint64_t* map2alm);
 
 /* ---- whole transforms ---------------------------------------------------------------- */
 /* alm: 2*AlmSet::count(lmax,mmax) doubles; map: n_pix doubles.  Host buffers: the copies are

@@ -17,7 +17,7 @@ SHTC_OK, SHTC_EINVAL, SHTC_EDOMAIN, SHTC_ECUDA, SHTC_ENOMEM, SHTC_EUNSUPPORTED =
 # every symbol include/shtc.h declares (checked by the CPU test suite)
 EXPORTED = [
     "shtc_create", "shtc_destroy", "shtc_last_error", "shtc_device_count", "shtc_set_stream",
-    "shtc_set_grid", "shtc_set_band", "shtc_plan", "shtc_plan_stats", "shtc_plan_phase_stats", "shtc_alm2map",
+    "shtc_set_grid", "shtc_set_band", "shtc_plan", "shtc_plan_stats", "shtc_plan_phase_stats", "shtc_plan_executed", "shtc_alm2map",
     "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev", "shtc_set_exchange_layout",
     "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev", "shtc_ring_synthesis_dev",
     "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
@@ -83,6 +83,7 @@ def lib():
         L.shtc_plan.argtypes = [vp, C.POINTER(dbl)]
         L.shtc_plan_stats.argtypes = [vp, u64p, u64p, u64p]
         L.shtc_plan_phase_stats.argtypes = [vp, u64p, u64p, u64p]
+        L.shtc_plan_executed.argtypes = [vp, u64p, u64p]
         for f in ("shtc_alm2map", "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev",
                   "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev",
                   "shtc_ring_synthesis_dev", "shtc_ring_analysis_dev"):

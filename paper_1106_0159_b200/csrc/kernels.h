@@ -50,8 +50,11 @@ static_assert(LEG_CL % 32 == 0, "whole entries per lane");
 #ifndef LEG_A2M_MINB
 #define LEG_A2M_MINB 3  // resident CTAs per SM the alm2map kernel is compiled for
 #endif
+#ifndef LEG_M2A_P
+#define LEG_M2A_P 2  // tiles a map2alm warp runs at once (LEG_R x LEG_M2A_P streams per lane)
+#endif
 #ifndef LEG_M2A_MINB
-#define LEG_M2A_MINB 4
+#define LEG_M2A_MINB (LEG_M2A_P > 1 ? 3 : 4)
 #endif
 #ifndef LEG_M2A_GROUP_DEF
 #define LEG_M2A_GROUP_DEF 4

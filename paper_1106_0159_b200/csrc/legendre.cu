@@ -523,14 +523,20 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
 
 // ---------------------------------------------------------------------------------------
 // map2alm: a_lm = c_l sum_r Delta^S_m(r) Q_lm(x_r), mirror paired
+//
+// A warp runs LEG_M2A_P tiles of one work item at once (S = LEG_R x LEG_M2A_P streams per
+// lane): every lane sums its S streams per degree before the cross-lane reduction, so the
+// shared-memory transpose -- which co-limited the kernel with the FP64 pipe at S = 4 (16
+// STS.128 + 32 LDS.64 + 31 DADD per lane per 16 degrees, ~95% of the FP64 time in shared-
+// memory wavefronts) -- is paid once per S x 16 stream-steps instead of once per 4 x 16.
 // ---------------------------------------------------------------------------------------
 namespace {
 
-template <int R>
+template <int S>
 struct M2ALane {
-    double x[R], q0[R], q1[R];
-    double2 ds[R], dd[R];  // north+south / north-south ring Delta of the lane's streams
-    int act[R];
+    double x[S], q0[S], q1[S];
+    double2 ds[S], dd[S];  // north+south / north-south ring Delta of the lane's streams
+    int act[S];
 };
 
 __device__ __forceinline__ void m2a_load_d(double2& ds, double2& dd, int s, const LegPlanView& p,
@@ -548,12 +554,12 @@ __device__ __forceinline__ void m2a_load_d(double2& ds, double2& dd, int s, cons
     }
 }
 
-// One plain step; returns the lane's contribution (re, im) summed over its R streams.
-template <int R, bool ODD>
-__device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, double A) {
+// One plain step; returns the lane's contribution (re, im) summed over its S streams.
+template <int S, bool ODD>
+__device__ __forceinline__ double2 m2a_step(M2ALane<S>& L, double A) {
     double2 part = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < S; ++r) {
         const double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
         const double2 d = ODD ? L.dd[r] : L.ds[r];
         part.x = __fma_rn(d.x, q2, part.x);
@@ -565,12 +571,12 @@ __device__ __forceinline__ double2 m2a_step(M2ALane<R>& L, double A) {
 }
 
 // step i where some lanes activate (checkpointed (Q_{i-1}, Q_i))
-template <int R, bool ODD>
-__device__ __forceinline__ double2 m2a_step_act(M2ALane<R>& L, double A, int i, const double2 (*ck)[32],
+template <int S, bool ODD>
+__device__ __forceinline__ double2 m2a_step_act(M2ALane<S>& L, double A, int i, const double2 (*ck)[32],
                                                 int lane) {
     double2 part = make_double2(0.0, 0.0);
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
+    for (int r = 0; r < S; ++r) {
         double q2 = rec_step(A, L.x[r], L.q1[r], L.q0[r]);
         if (L.act[r] == i) {
             const double2 c = ck[r][lane];
@@ -586,68 +592,168 @@ __device__ __forceinline__ double2 m2a_step_act(M2ALane<R>& L, double A, int i, 
     return part;
 }
 
-// Cross-lane reduction of the per-lane partials (16 values per 8 degrees: degree x re/im).
-// Default: a shared-memory transpose over 16 degrees (each lane writes its row, lane j sums
-// column j).  LEG_M2A_SHFL=1: a register butterfly, reduce-scatter over the 32 lanes with
-// __shfl_xor (31 values exchanged per lane per 16 degrees, half the bytes of the transpose);
-// measured slower at C4 (11.2 against 8.85 ms): 64-bit shuffles cost more issue than the
-// shared-memory traffic they replace.
-#ifndef LEG_M2A_SHFL
-#define LEG_M2A_SHFL 0
-#endif
-#ifndef LEG_M2A_APIPE
-#define LEG_M2A_APIPE 1  // FAST-group coefficient loads: 0 per pair, 1 one pair ahead (8.67 -> 8.57 ms
-                         // at C4), 2 all upfront (8.64 ms)
-#endif
-#if LEG_M2A_SHFL
-constexpr int M2A_G = 8;  // degrees per cross-lane reduction group
-#else
-constexpr int M2A_G = 16;
-#endif
+constexpr int M2A_G = 16;  // degrees per cross-lane reduction group
+constexpr int M2A_S = LEG_R * LEG_M2A_P;
 
-template <int R>
+// Per-warp shared memory (dynamic: 4 warps x ~14 KB exceeds the 48 KB static limit)
 struct M2AWarpSmem {
     double A[LEG_CL];
-#if !LEG_M2A_SHFL
     double red[32][2 * M2A_G + 2];  // lane rows of (degree, re/im) partials, 16-byte aligned
-#endif
-    double2 ck[R][32];  // activation checkpoints of the current tile
+    double2 ck[M2A_S][32];          // activation checkpoints of the current tiles
 };
 
-#if LEG_M2A_SHFL
-// Butterfly reduce-scatter: value c = 2u + comp (v[u].x / v[u].y) summed over the warp ends on
-// lanes 2c and 2c + 1 (both hold the same sum: the last stage adds a + b on one lane and b + a
-// on the other).  Fixed lane pairing and order, so the result is deterministic.
-__device__ __forceinline__ double m2a_reduce8(const double2 (&v)[8], int lane) {
-    double h[8];
-    const bool b4 = lane & 16;
+// Lanes of NP tiles at once: stream index q*R + r is stream r of tiles[q]; tiles[q] < 0 is an
+// absent tile (its streams stay zero).  Seed lanes (act == 0) start from (0, P_mm).
+template <int R, int NP>
+__device__ __forceinline__ void m2a_lanes_setup(const LegPlanView& p, int mi, const int (&tiles)[NP],
+                                                int lane, M2ALane<R * NP>& L, double2 (*ck)[32],
+                                                const double2* __restrict__ delta,
+                                                const int64_t* __restrict__ row_off) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const double lo = (i & 1) ? v[i >> 1].y : v[i >> 1].x;               // c = i
-        const double hi = (i & 1) ? v[(i + 8) >> 1].y : v[(i + 8) >> 1].x;   // c = i + 8
-        const double recv = __shfl_xor_sync(0xffffffffu, b4 ? lo : hi, 16);
-        h[i] = (b4 ? hi : lo) + recv;
-    }
-    const bool b3 = lane & 8;
+    for (int q = 0; q < NP; ++q) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-        const double recv = __shfl_xor_sync(0xffffffffu, b3 ? h[i] : h[i + 4], 8);
-        h[i] = (b3 ? h[i + 4] : h[i]) + recv;
+        for (int r = 0; r < R; ++r) {
+            const int k = q * R + r;
+            const int s = tiles[q] * (32 * R) + r * 32 + lane;
+            L.x[k] = 0.0;
+            L.q0[k] = L.q1[k] = 0.0;
+            L.act[k] = INT_MAX;
+            L.ds[k] = L.dd[k] = make_double2(0.0, 0.0);
+            if (tiles[q] >= 0 && s < p.st.n) {
+                const size_t o = (size_t)mi * p.st.n + s;
+                L.x[k] = p.st.x[s];
+                L.act[k] = p.ck_act[o];
+                const double2 c = p.ck_q[o];
+                ck[k][lane] = c;
+                if (L.act[k] == 0) {
+                    L.q0[k] = c.x;
+                    L.q1[k] = c.y;
+                }
+                m2a_load_d(L.ds[k], L.dd[k], s, p, delta, row_off, mi);
+            }
+        }
     }
-    const bool b2 = lane & 4;
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-        const double recv = __shfl_xor_sync(0xffffffffu, b2 ? h[i] : h[i + 2], 4);
-        h[i] = (b2 ? h[i + 2] : h[i]) + recv;
-    }
-    const bool b1 = lane & 2;
-    {
-        const double recv = __shfl_xor_sync(0xffffffffu, b1 ? h[0] : h[1], 2);
-        h[0] = (b1 ? h[1] : h[0]) + recv;
-    }
-    return h[0] + __shfl_xor_sync(0xffffffffu, h[0], 1);  // c = (lane >> 1) & 15
 }
-#endif
+
+// One pass of a work item: NP of its tiles run together from the earliest start among them;
+// the pass's per-degree sums go to the item's scratch slot (first pass stores, later passes
+// add in place: a single lane owns each word, so the order is the pass order).
+template <int R, int NP>
+__device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __restrict__ delta,
+                                         const int64_t* __restrict__ row_off, M2AWarpSmem& sm,
+                                         int mi, int n, const double* __restrict__ gA,
+                                         double2* __restrict__ part_out, const int (&tiles)[NP],
+                                         bool first, int lane) {
+    constexpr int S = R * NP;
+    int ic = INT_MAX, ie = -1;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+        if (tiles[q] < 0) continue;
+        const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tiles[q]];
+        ic = min(ic, leg_tile_start(info.x));  // first step of the run (even; 0: seeds)
+        ie = max(ie, info.y);
+    }
+    const int nchunks = (n + 1 - ic + LEG_CL - 1) / LEG_CL;  // degree offsets ic..n
+    if (first)  // degrees below the first pass's start get no other first write
+        for (int i = lane; i < ic; i += 32) part_out[i] = make_double2(0.0, 0.0);
+    M2ALane<S> L;
+    __syncwarp();
+    m2a_lanes_setup<R, NP>(p, mi, tiles, lane, L, sm.ck, delta, row_off);
+    __syncwarp();
+    int ev = next_activation<S>(L.act, ic - 1 + (ic == 0));
+
+    constexpr int K = LEG_CL / 32;  // entries per lane per chunk
+    auto fetch = [&](int c, double (&v)[K]) {
+#pragma unroll
+        for (int q = 0; q < K; ++q) {
+            const int i = ic + c * LEG_CL + q * 32 + lane;
+            v[q] = i <= n ? gA[i] : 0.0;
+        }
+    };
+    // this lane's (degree, component) of the group in the scratch slot
+    double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
+    double nxt[K];
+    fetch(0, nxt);
+    for (int c = 0; c < nchunks; ++c) {
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < K; ++q) sm.A[q * 32 + lane] = nxt[q];
+        __syncwarp();
+        if (c + 1 < nchunks) fetch(c + 1, nxt);
+        const int i0 = ic + c * LEG_CL;
+        const int cnt = min(LEG_CL, n - i0 + 1);
+        for (int g = 0; g < cnt; g += M2A_G) {
+            const int gc = min(M2A_G, cnt - g);
+            const int ig = i0 + g;  // even degree offset
+            const int iw = ig + (lane >> 1);
+            double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
+            rmw_ptr += 2 * M2A_G;
+            // per-step lane contributions go straight to this lane's transpose row
+            double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
+            if (ig > ie && gc == M2A_G) {
+                // after the last activation: straight-line steps, coefficients in pairs; the
+                // next pair's coefficients are loaded before this pair's partials are stored
+                // (the compiler cannot move the load across the stores)
+                double2 a = *reinterpret_cast<const double2*>(&sm.A[g]);
+#pragma unroll
+                for (int u = 0; u < M2A_G; u += 2) {
+                    const double2 an = *reinterpret_cast<const double2*>(&sm.A[g + (u + 2 < M2A_G ? u + 2 : u)]);
+                    row[u] = m2a_step<S, false>(L, a.x);
+                    row[u + 1] = m2a_step<S, true>(L, a.y);
+                    a = an;
+                }
+            } else {
+                // activation window (warp-uniform event test per step), seed, partial group
+                for (int u = 0; u < M2A_G; u += 2) {
+                    const int i = ig + u;
+                    double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
+                    if (u < gc) {
+                        if (i == 0) {
+                            // seed term (degree offset 0): no recurrence step
+#pragma unroll
+                            for (int r = 0; r < S; ++r) {
+                                v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
+                                v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
+                            }
+                        } else if (i == ev) {
+                            v1 = m2a_step_act<S, false>(L, sm.A[g + u], i, sm.ck, lane);
+                            ev = next_activation<S>(L.act, i);
+                        } else {
+                            v1 = m2a_step<S, false>(L, sm.A[g + u]);
+                        }
+                        if (u + 1 < gc) {
+                            if (i + 1 == ev) {
+                                v2 = m2a_step_act<S, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
+                                ev = next_activation<S>(L.act, i + 1);
+                            } else {
+                                v2 = m2a_step<S, true>(L, sm.A[g + u + 1]);
+                            }
+                        }
+                    }
+                    row[u] = v1;
+                    row[u + 1] = v2;
+                }
+            }
+            // lane j reduces column j (degree ig + j/2, component j&1) over the 32 lane rows
+            // in a fixed order (8 independent chains) and accumulates it into the slot
+            __syncwarp();
+            double s[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) s[k] = sm.red[k][lane];
+#pragma unroll
+            for (int rr = 8; rr < 32; rr += 8) {
+#pragma unroll
+                for (int k = 0; k < 8; ++k) s[k] += sm.red[rr + k][lane];
+            }
+            const double v = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
+            __syncwarp();
+            if (iw <= n) {
+                if (first) *wp = v;
+                else asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
+            }
+        }
+    }
+}
 
 }  // namespace
 
@@ -657,9 +763,9 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
                        const int64_t* __restrict__ row_off, int* __restrict__ queue,
                        double2* __restrict__ scratch) {
     static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
-    __shared__ M2AWarpSmem<R> sm_all[LEG_WARPS];
+    extern __shared__ __align__(16) unsigned char m2a_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    M2AWarpSmem<R>& sm = sm_all[warp];
+    M2AWarpSmem& sm = reinterpret_cast<M2AWarpSmem*>(m2a_smem)[warp];
 
     for (;;) {
         const int it = warp_next_item(queue);
@@ -668,196 +774,18 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
         const int mi = item.mi;
         const int m = p.ms[mi];
         const int n = p.lmax - m;
-        const int64_t toff = p.tab.tab_off[mi];
-        const double* __restrict__ gA = p.tab.A + toff;
+        const double* __restrict__ gA = p.tab.A + p.tab.tab_off[mi];
         double2* __restrict__ part_out = scratch + p.m2a_slot_base[mi] + (int64_t)item.g * (n + 1);
-        for (int tt = 0; tt < item.b; ++tt) {
-            const int tile = p.tile_list[item.a + tt];
-            const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
-            const int ie = info.y;
-            const int ic = leg_tile_start(info.x);  // first step of the run (even; 0: seeds)
-            const int nchunks = (n + 1 - ic + LEG_CL - 1) / LEG_CL;  // degree offsets ic..n
-            if (tt == 0)  // degrees below the first tile's start get no other first write
-                for (int i = lane; i < ic; i += 32) part_out[i] = make_double2(0.0, 0.0);
-            M2ALane<R> L;
-            __syncwarp();
-            lanes_setup<R>(p, mi, tile, lane, L.x, L.q0, L.q1, L.act, sm.ck);
+        int tt = 0;
+        for (; tt + LEG_M2A_P <= item.b; tt += LEG_M2A_P) {
+            int tiles[LEG_M2A_P];
 #pragma unroll
-            for (int r = 0; r < R; ++r) {
-                const int s = tile * (32 * R) + r * 32 + lane;
-                L.ds[r] = L.dd[r] = make_double2(0.0, 0.0);
-                if (s < p.st.n) m2a_load_d(L.ds[r], L.dd[r], s, p, delta, row_off, mi);
-            }
-            __syncwarp();
-            int ev = next_activation<R>(L.act, ic - 1 + (ic == 0));
-
-            constexpr int K = LEG_CL / 32;  // entries per lane per chunk
-            auto fetch = [&](int c, double (&v)[K]) {
-#pragma unroll
-                for (int q = 0; q < K; ++q) {
-                    const int i = ic + c * LEG_CL + q * 32 + lane;
-                    v[q] = i <= n ? gA[i] : 0.0;
-                }
-            };
-            // this lane's (degree, component) of the group in the scratch slot
-#if LEG_M2A_SHFL
-            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + (lane >> 1);
-#else
-            double* rmw_ptr = reinterpret_cast<double*>(part_out + ic) + lane;
-#endif
-            double nxt[K];
-            fetch(0, nxt);
-            for (int c = 0; c < nchunks; ++c) {
-                __syncwarp();
-#pragma unroll
-                for (int q = 0; q < K; ++q) sm.A[q * 32 + lane] = nxt[q];
-                __syncwarp();
-                if (c + 1 < nchunks) fetch(c + 1, nxt);
-                const int i0 = ic + c * LEG_CL;
-                const int cnt = min(LEG_CL, n - i0 + 1);
-                for (int g = 0; g < cnt; g += M2A_G) {
-                    const int gc = min(M2A_G, cnt - g);
-                    const int ig = i0 + g;  // even degree offset
-#if LEG_M2A_SHFL
-                    const int iw = ig + (lane >> 2);
-                    double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
-                    rmw_ptr += 2 * M2A_G;
-                    double2 row[M2A_G];  // this lane's partial (sum over its R streams) per degree
-                    if (ig > ie && gc == M2A_G) {
-                        // after the last activation: straight-line steps, coefficients in pairs
-#pragma unroll
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            const double2 a = *reinterpret_cast<const double2*>(&sm.A[g + u]);
-                            row[u] = m2a_step<R, false>(L, a.x);
-                            row[u + 1] = m2a_step<R, true>(L, a.y);
-                        }
-                    } else {
-                        // activation window (warp-uniform event test per step), seed, partial group
-#pragma unroll
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            const int i = ig + u;
-                            double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
-                            if (u < gc) {
-                                if (i == 0) {
-                                    // seed term (degree offset 0): no recurrence step
-#pragma unroll
-                                    for (int r = 0; r < R; ++r) {
-                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
-                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
-                                    }
-                                } else if (i == ev) {
-                                    v1 = m2a_step_act<R, false>(L, sm.A[g + u], i, sm.ck, lane);
-                                    ev = next_activation<R>(L.act, i);
-                                } else {
-                                    v1 = m2a_step<R, false>(L, sm.A[g + u]);
-                                }
-                                if (u + 1 < gc) {
-                                    if (i + 1 == ev) {
-                                        v2 = m2a_step_act<R, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
-                                        ev = next_activation<R>(L.act, i + 1);
-                                    } else {
-                                        v2 = m2a_step<R, true>(L, sm.A[g + u + 1]);
-                                    }
-                                }
-                            }
-                            row[u] = v1;
-                            row[u + 1] = v2;
-                        }
-                    }
-                    const double v = m2a_reduce8(row, lane);
-                    const bool writer = !(lane & 1);
-#else
-                    const int iw = ig + (lane >> 1);
-                    double* const wp = rmw_ptr;  // loop-carried: no per-group address rebuild
-                    rmw_ptr += 2 * M2A_G;
-                    // per-step lane contributions go straight to this lane's transpose row
-                    double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
-                    if (ig > ie && gc == M2A_G) {
-                        // after the last activation: straight-line steps, coefficients in pairs
-#if LEG_M2A_APIPE == 1
-                        // the next pair's coefficients are loaded before this pair's partials
-                        // are stored (the compiler cannot move the load across the stores)
-                        double2 a = *reinterpret_cast<const double2*>(&sm.A[g]);
-#pragma unroll
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            const double2 an = *reinterpret_cast<const double2*>(&sm.A[g + (u + 2 < M2A_G ? u + 2 : u)]);
-                            row[u] = m2a_step<R, false>(L, a.x);
-                            row[u + 1] = m2a_step<R, true>(L, a.y);
-                            a = an;
-                        }
-#elif LEG_M2A_APIPE == 2
-                        double2 ag[M2A_G / 2];
-#pragma unroll
-                        for (int u = 0; u < M2A_G / 2; ++u) ag[u] = *reinterpret_cast<const double2*>(&sm.A[g + 2 * u]);
-#pragma unroll
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            row[u] = m2a_step<R, false>(L, ag[u >> 1].x);
-                            row[u + 1] = m2a_step<R, true>(L, ag[u >> 1].y);
-                        }
-#else
-#pragma unroll
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            const double2 a = *reinterpret_cast<const double2*>(&sm.A[g + u]);
-                            row[u] = m2a_step<R, false>(L, a.x);
-                            row[u + 1] = m2a_step<R, true>(L, a.y);
-                        }
-#endif
-                    } else {
-                        // activation window (warp-uniform event test per step), seed, partial group
-                        for (int u = 0; u < M2A_G; u += 2) {
-                            const int i = ig + u;
-                            double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
-                            if (u < gc) {
-                                if (i == 0) {
-                                    // seed term (degree offset 0): no recurrence step
-#pragma unroll
-                                    for (int r = 0; r < R; ++r) {
-                                        v1.x = __fma_rn(L.ds[r].x, L.q1[r], v1.x);
-                                        v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
-                                    }
-                                } else if (i == ev) {
-                                    v1 = m2a_step_act<R, false>(L, sm.A[g + u], i, sm.ck, lane);
-                                    ev = next_activation<R>(L.act, i);
-                                } else {
-                                    v1 = m2a_step<R, false>(L, sm.A[g + u]);
-                                }
-                                if (u + 1 < gc) {
-                                    if (i + 1 == ev) {
-                                        v2 = m2a_step_act<R, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
-                                        ev = next_activation<R>(L.act, i + 1);
-                                    } else {
-                                        v2 = m2a_step<R, true>(L, sm.A[g + u + 1]);
-                                    }
-                                }
-                            }
-                            row[u] = v1;
-                            row[u + 1] = v2;
-                        }
-                    }
-                    // lane j reduces column j (degree ig + j/2, component j&1) over the 32 lane
-                    // rows in a fixed order and accumulates it into the warp's scratch slot
-                    __syncwarp();
-                    double s0 = sm.red[0][lane], s1 = sm.red[1][lane], s2 = sm.red[2][lane],
-                           s3 = sm.red[3][lane];
-#pragma unroll
-                    for (int rr = 4; rr < 32; rr += 4) {
-                        s0 += sm.red[rr][lane];
-                        s1 += sm.red[rr + 1][lane];
-                        s2 += sm.red[rr + 2][lane];
-                        s3 += sm.red[rr + 3][lane];
-                    }
-                    const double v = (s0 + s1) + (s2 + s3);
-                    __syncwarp();
-                    const bool writer = true;
-#endif
-                    // first tile stores; later tiles add in place (fire-and-forget reduction,
-                    // a single lane owns each word so the order is the tile order)
-                    if (writer && iw <= n) {
-                        if (tt == 0) *wp = v;
-                        else asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(wp), "d"(v) : "memory");
-                    }
-                }
-            }
+            for (int q = 0; q < LEG_M2A_P; ++q) tiles[q] = p.tile_list[item.a + tt + q];
+            m2a_pass<R, LEG_M2A_P>(p, delta, row_off, sm, mi, n, gA, part_out, tiles, tt == 0, lane);
+        }
+        for (; tt < item.b; ++tt) {  // leftover tiles one at a time
+            const int tiles[1] = {p.tile_list[item.a + tt]};
+            m2a_pass<R, 1>(p, delta, row_off, sm, mi, n, gA, part_out, tiles, tt == 0, lane);
         }
     }
 }
@@ -908,15 +836,28 @@ __global__ void leg_zero_orders_kernel(LegPlanView p, double2* __restrict__ alm)
     for (int i = threadIdx.x; i <= p.lmax - m; i += blockDim.x) out[i] = make_double2(0.0, 0.0);
 }
 
-int leg_m2a_warps(int device) {
+namespace {
+constexpr size_t kM2ASmem = LEG_WARPS * sizeof(M2AWarpSmem);
+
+// resident blocks per SM of the map2alm kernel (its dynamic shared memory opted in once per
+// device)
+int m2a_blocks_per_sm(int device) {
     static int cached[64] = {0};
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
-    int sms = 148, per = 1;
+    cudaFuncSetAttribute(leg_map2alm_kernel<LEG_R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kM2ASmem);
+    int per = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_map2alm_kernel<LEG_R>, LEG_WARPS * 32, kM2ASmem);
+    per = per > 0 ? per : 1;
+    if (device >= 0 && device < 64) cached[device] = per;
+    return per;
+}
+}  // namespace
+
+int leg_m2a_warps(int device) {
+    int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_map2alm_kernel<LEG_R>, LEG_WARPS * 32, 0);
-    const int v = sms * (per > 0 ? per : 1) * LEG_WARPS;
-    if (device >= 0 && device < 64) cached[device] = v;
-    return v;
+    return sms * m2a_blocks_per_sm(device) * LEG_WARPS;
 }
 
 void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_t* row_off,
@@ -930,14 +871,11 @@ void launch_leg_map2alm(const LegPlanView& p, const double2* delta, const int64_
     if (!(phases & LEG_PHASE_MAIN) || p.n_m2a_items == 0) return;
     int dev = 0;
     cudaGetDevice(&dev);
-    int sms = 148, per = 1;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_map2alm_kernel<LEG_R>, LEG_WARPS * 32, 0);
-    int blocks = sms * (per > 0 ? per : 1);
+    int blocks = leg_m2a_warps(dev) / LEG_WARPS;
     const int need = (p.n_m2a_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
     if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
-    leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, delta, row_off, counters, scratch);
+    leg_map2alm_kernel<LEG_R><<<blocks, LEG_WARPS * 32, kM2ASmem, s>>>(p, delta, row_off, counters, scratch);
     count_launch();
     // whole launches reduce every order's slots here; pipelined band launches (defer_final)
     // leave them to the caller, which finalizes each order once its last launch is done

@@ -156,7 +156,8 @@ struct LegPlan {
     DevBuf m2a_final_list;           // order indices final after each m2a launch, concatenated
     std::vector<int> m2a_final_off;  // launch j: [m2a_final_off[j], m2a_final_off[j+1])
     LegPlanView view{};
-    uint64_t nominal = 0, executed = 0, useful = 0;
+    // executed: map2alm passes (tile pairs); executed_a2m: alm2map (single tiles)
+    uint64_t nominal = 0, executed = 0, executed_a2m = 0, useful = 0;
     int m2a_group = LEG_M2A_GROUP;  // tiles per map2alm item of the device-resident set
     double build_ms = 0.0;
 };
@@ -411,7 +412,7 @@ std::vector<int> m2a_launch_bands() {
 
 // tiles per map2alm item of the pipelined (band) item set; SHTC_M2A_BAND_GROUP overrides
 int m2a_band_group() {
-    static const int g = std::getenv("SHTC_M2A_BAND_GROUP") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_BAND_GROUP"))) : 1;
+    static const int g = std::getenv("SHTC_M2A_BAND_GROUP") ? std::max(1, std::atoi(std::getenv("SHTC_M2A_BAND_GROUP"))) : (LEG_M2A_P > 1 ? 2 : 1);
     return g;
 }
 
@@ -513,60 +514,83 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     for (const int2& ti : info) alive_total += ti.x >= 0;
     int dev_id = 0;
     CK(cudaGetDevice(&dev_id));
+    // (a multiple of the pass width: the map2alm kernel runs an item's tiles LEG_M2A_P at a
+    // time, so every item's passes are consecutive tile pairs of one band)
+    constexpr int kPair = LEG_M2A_P > 1 ? 2 : 1;
     const int g_dev = (int)std::max<int64_t>(
-        1, std::min<int64_t>(LEG_M2A_GROUP, alive_total / (LEG_M2A_ITEMS_PER_WARP * (int64_t)leg_m2a_warps(dev_id))));
+        std::min(kPair, LEG_M2A_GROUP),
+        std::min<int64_t>(LEG_M2A_GROUP, alive_total / (LEG_M2A_ITEMS_PER_WARP * (int64_t)leg_m2a_warps(dev_id)))
+            / kPair * kPair);
     P.m2a_group = g_dev;
+    auto tile_start = [&](int mi, int t) { return leg_tile_start(info[(size_t)mi * v.n_tiles + t].x); };
+    // steps one pass runs (from the earliest start of its tiles): every step times the streams
+    // of its tiles; steps up to the last activation test for activation events ("checked"),
+    // later steps are plain recurrence + accumulation ("fast")
+    auto account = [&](int mi, const int* ts, int nt, uint64_t& executed, uint64_t* checked, uint64_t* fast) {
+        const int n = lmax - ms[mi];
+        int ic = INT_MAX, ie = -1, in_pass = 0;
+        for (int k = 0; k < nt; ++k) {
+            ic = std::min(ic, tile_start(mi, ts[k]));
+            ie = std::max(ie, info[(size_t)mi * v.n_tiles + ts[k]].y);
+            in_pass += std::min(LEG_TILE, ns - ts[k] * LEG_TILE);
+        }
+        const uint64_t run = (uint64_t)(n + 1 - ic);
+        const uint64_t fst = std::min<uint64_t>(run, (uint64_t)std::max(0, n - std::max(ie, ic)));
+        executed += run * in_pass;
+        if (fast) *fast += fst * in_pass;
+        if (checked) *checked += (run - fst) * in_pass;
+    };
+    P.executed_a2m = 0;
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
         P.nominal += (uint64_t)(n + 1) * ns;
         toffs[i] = (int)tl.size();
         std::vector<int> alive;
-        for (int t = 0; t < v.n_tiles; ++t) {
-            const int2 ti = info[(size_t)i * v.n_tiles + t];
-            if (ti.x < 0) continue;
-            alive.push_back(t);
-            a2m.push_back(LegItem{i, t, 0, 0});
-            const int in_tile = std::min(LEG_TILE, ns - t * LEG_TILE);
-            // the kernels run from ic; steps up to the last activation test for activation
-            // events ("checked"), later steps are plain recurrence + accumulation
-            const int ic = leg_tile_start(ti.x);
-            const uint64_t run = (uint64_t)(n + 1 - ic);
-            const uint64_t fst = std::min<uint64_t>(run, (uint64_t)std::max(0, n - std::max(ti.y, ic)));
-            P.executed += run * in_tile;
-            P.fast_steps += fst * in_tile;
-            P.checked_steps += (run - fst) * in_tile;
-        }
-        std::reverse(alive.begin(), alive.end());
+        for (int t = v.n_tiles - 1; t >= 0; --t)  // descending tile index: bands ascending
+            if (info[(size_t)i * v.n_tiles + t].x >= 0) alive.push_back(t);
         tl.insert(tl.end(), alive.begin(), alive.end());
         tcnt[i] = (int)alive.size();
-        // map2alm items: up to G consecutive alive tiles.  Device-resident set: G = g_dev
-        // (fewer partial slots; one launch, so long items only delay its start).
-        // Band set: G = m2a_band_group tiles of one pipeline band, so no item outlasts the
-        // band's launch.  The two sets sum in different groupings (both deterministic).
-        auto group = [&](int G, bool by_band, std::vector<LegItem>& out, int& cnt) {
+        for (int t : alive) {  // alm2map: one tile per item
+            a2m.push_back(LegItem{i, t, -1, 0});
+            account(i, &t, 1, P.executed_a2m, nullptr, nullptr);
+        }
+        // map2alm passes: consecutive alive tiles of one band in pairs (kPair)
+        for (size_t a = 0; a < alive.size();) {
+            const int nt = (kPair > 1 && a + 1 < alive.size() && tband[alive[a + 1]] == tband[alive[a]]) ? 2 : 1;
+            account(i, &alive[a], nt, P.executed, &P.checked_steps, &P.fast_steps);
+            a += nt;
+        }
+        // map2alm items: up to G consecutive alive tiles of one pipeline band.  Device-
+        // resident set: G = g_dev (fewer partial slots; one launch, so long items only delay
+        // its start).  Band set: G = m2a_band_group, so no item outlasts the band's launch.
+        // Sets with equal G are the same partition (same sums); otherwise both deterministic.
+        auto group = [&](int G, std::vector<LegItem>& out, int& cnt) {
             cnt = 0;
             for (size_t a = 0; a < alive.size();) {
                 size_t e = a + 1;
-                while (e < alive.size() && e - a < (size_t)G && (!by_band || tband[alive[e]] == tband[alive[a]])) ++e;
+                while (e < alive.size() && e - a < (size_t)G && tband[alive[e]] == tband[alive[a]]) ++e;
                 out.push_back(LegItem{i, toffs[i] + (int)a, (int)(e - a), cnt++});
                 a = e;
             }
         };
-        group(g_dev, false, m2a, per_m[i]);
-        group(m2a_band_group(), true, m2a_b, per_m_b[i]);
+        group(g_dev, m2a, per_m[i]);
+        group(m2a_band_group(), m2a_b, per_m_b[i]);
         slot[i] = slots;
         slots += (int64_t)per_m[i] * (n + 1);
         slot_b[i] = slots_b;
         slots_b += (int64_t)per_m_b[i] * (n + 1);
     }
-    // cost = degree steps actually run (from the tile's resume point)
-    auto tile_cost = [&](int mi, int t) {
-        return (int64_t)(lmax - ms[mi] + 1 - leg_tile_start(info[(size_t)mi * v.n_tiles + t].x));
+    // cost = degree steps actually run (from the pass's resume point) x tiles in the pass
+    auto pass_cost = [&](int mi, int ta, int tb) {
+        const int ic = tb >= 0 ? std::min(tile_start(mi, ta), tile_start(mi, tb)) : tile_start(mi, ta);
+        return (int64_t)(lmax - ms[mi] + 1 - ic) * (tb >= 0 ? 2 : 1);
     };
-    auto a2m_cost = [&](const LegItem& it) { return tile_cost(it.mi, it.a); };
+    auto a2m_cost = [&](const LegItem& it) { return pass_cost(it.mi, it.a, -1); };
     auto m2a_cost = [&](const LegItem& it) {
         int64_t c = 0;
-        for (int k = 0; k < it.b; ++k) c += tile_cost(it.mi, tl[it.a + k]);
+        int k = 0;
+        for (; k + kPair <= it.b; k += kPair) c += pass_cost(it.mi, tl[it.a + k], kPair > 1 ? tl[it.a + k + 1] : -1);
+        for (; k < it.b; ++k) c += pass_cost(it.mi, tl[it.a + k], -1);
         return c;
     };
     // order chunks of ~equal coefficient counts (H2D / D2H units of the pipelined paths)
@@ -961,7 +985,7 @@ void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, c
 }
 
 void fill_timing(shtc_timing* t, double leg, double fft, double h2d, double d2h, double total,
-                 const LegPlan& P) {
+                 const LegPlan& P, bool alm2map) {
     if (!t) return;
     t->legendre_ms = leg;
     t->fft_ms = fft;
@@ -969,7 +993,7 @@ void fill_timing(shtc_timing* t, double leg, double fft, double h2d, double d2h,
     t->d2h_ms = d2h;
     t->total_ms = total;
     t->nominal_steps = P.nominal;
-    t->executed_steps = P.executed;
+    t->executed_steps = alm2map ? P.executed_a2m : P.executed;
 }
 
 void do_alm2map_dev(shtc_ctx* c, const double* alm, double* map, shtc_timing* t, double h2d = 0) {
@@ -989,7 +1013,7 @@ void do_alm2map_dev(shtc_ctx* c, const double* alm, double* map, shtc_timing* t,
     if (t) {
         CK(cudaEventSynchronize(c->ev[2]));
         const double leg = elapsed(c->ev[0], c->ev[1]), fft = elapsed(c->ev[1], c->ev[2]);
-        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg);
+        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg, true);
     }
 }
 
@@ -1011,7 +1035,7 @@ void do_map2alm_dev(shtc_ctx* c, const double* map, double* alm, shtc_timing* t,
     if (t) {
         CK(cudaEventSynchronize(c->ev[2]));
         const double fft = elapsed(c->ev[0], c->ev[1]), leg = elapsed(c->ev[1], c->ev[2]);
-        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg);
+        fill_timing(t, leg, fft, h2d, 0.0, leg + fft, c->leg, false);
     }
 }
 
@@ -1192,6 +1216,15 @@ shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* che
         if (prefix) *prefix = ctx->leg.prefix_steps;
         if (checked) *checked = ctx->leg.checked_steps;
         if (fast) *fast = ctx->leg.fast_steps;
+    });
+}
+
+shtc_status shtc_plan_executed(shtc_ctx* ctx, uint64_t* alm2map, uint64_t* map2alm) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ensure_leg_plan(ctx);
+        if (alm2map) *alm2map = ctx->leg.executed_a2m;
+        if (map2alm) *map2alm = ctx->leg.executed;
     });
 }
 
@@ -1428,7 +1461,7 @@ shtc_status shtc_alm2map(shtc_ctx* ctx, const double* alm, double* map, shtc_tim
             for (int i : t_fft) fft += E.span(i);
             const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
             const float h2d = th < 0 ? 0.f : elapsed(ctx->tev[th], ctx->tev[th_last + 1]);
-            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
+            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P, true);
         }
     });
 }
@@ -1566,7 +1599,7 @@ shtc_status shtc_map2alm(shtc_ctx* ctx, const double* map, double* alm, shtc_tim
             for (int i : t_fft) fft += E.span(i);
             const float d2h = t_d2h_first < 0 ? 0.f : elapsed(ctx->tev[t_d2h_first], ctx->ev[6]);
             const float h2d = th < 0 ? 0.f : elapsed(ctx->tev[th], ctx->tev[th_last + 1]);
-            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P);
+            fill_timing(t, leg, fft, h2d, d2h, elapsed(ctx->ev[3], ctx->ev[6]), P, false);
         }
     });
 }
@@ -1626,7 +1659,7 @@ shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, doub
         if (t) {
             CK(cudaEventSynchronize(ctx->ev[1]));
             const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
-            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg, true);
         }
     });
 }
@@ -1646,7 +1679,7 @@ shtc_status shtc_legendre_map2alm_dev(shtc_ctx* ctx, const double* delta_dev, do
         if (t) {
             CK(cudaEventSynchronize(ctx->ev[1]));
             const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
-            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg, false);
         }
     });
 }
@@ -1790,7 +1823,7 @@ shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, sht
         if (t) {
             CK(cudaEventSynchronize(ctx->ev[1]));
             const double leg = elapsed(ctx->ev[0], ctx->ev[1]);
-            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg);
+            fill_timing(t, leg, 0, 0, 0, leg, ctx->leg, true);
         }
     });
 }

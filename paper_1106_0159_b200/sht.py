@@ -497,8 +497,11 @@ class Context:
         self._check(lib().shtc_plan_stats(self._h, C.byref(a), C.byref(b), C.byref(c)))
         d, e, f = C.c_uint64(), C.c_uint64(), C.c_uint64()
         self._check(lib().shtc_plan_phase_stats(self._h, C.byref(d), C.byref(e), C.byref(f)))
+        g, h = C.c_uint64(), C.c_uint64()
+        self._check(lib().shtc_plan_executed(self._h, C.byref(g), C.byref(h)))
         return {"nominal": a.value, "executed": b.value, "useful": c.value,
-                "prefix": d.value, "checked": e.value, "fast": f.value}
+                "prefix": d.value, "checked": e.value, "fast": f.value,
+                "executed_alm2map": g.value, "executed_map2alm": h.value}
 
     # host-buffer transforms ---------------------------------------------------------
     def alm2map(self, alm: np.ndarray, out: np.ndarray | None = None, timing: bool = False):
