@@ -301,6 +301,7 @@ def run_ours(args):
         import torch.distributed as dist
         row_off, send_c, recv_c, ring_list, m_base, m_stride = sht.exchange_layout(layout, rank)
         ctx.set_exchange_layout(row_off, ring_list, m_base, m_stride)
+        ctx.set_exchange_layout_synthesis(*sht.exchange_layout_synthesis(layout, rank))
         send = torch.empty(2 * sum(send_c), dtype=torch.float64, device=dev)
         recv = torch.empty(2 * sum(recv_c), dtype=torch.float64, device=dev)
         mp = torch.zeros(grid.n_pix, dtype=torch.float64, device=dev)

@@ -133,6 +133,17 @@ shtc_status shtc_map2alm_dev(shtc_ctx* ctx, const double* map_dev, double* alm_d
 shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int n_ring_list,
                                      const int32_t* ring_list, const int64_t* m_base,
                                      const int64_t* m_stride);
+/* Synthesis-direction layout on top of shtc_set_exchange_layout (same blocks, same ring list):
+ * Delta(r, order index mi) of the Legendre output at row_off[r] + mi * row_stride[r] and the
+ * ring synthesis input (ring_list[p], m) at m_base[m] + p * m_stride[m].  Order-major blocks
+ * ([|M_i| orders x |R_j| rings], row_stride = |R_j|) turn the Legendre kernel's stores --
+ * one order, consecutive rings per warp -- into contiguous runs (the NVLink stores of the
+ * fused exchange).  The analysis direction keeps the ring-major layout, whose unfold visits
+ * the orders grouped by m_base so each owner's block is stored contiguously.  NULL row_off:
+ * both directions use the shtc_set_exchange_layout layout.  Clears the peer targets. */
+shtc_status shtc_set_exchange_layout_synthesis(shtc_ctx* ctx, const int64_t* row_off,
+                                               const int64_t* row_stride, const int64_t* m_base,
+                                               const int64_t* m_stride);
 shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, double* delta_dev,
                                       shtc_timing* t);
 shtc_status shtc_legendre_map2alm_dev(shtc_ctx* ctx, const double* delta_dev, double* alm_dev,
@@ -155,9 +166,10 @@ shtc_status shtc_ipc_open(int device, const unsigned char* handle64, void** ptr)
 shtc_status shtc_ipc_close(void* ptr);
 /* Targets of this worker's stores (device addresses valid on this context's device), on top
  * of shtc_set_exchange_layout:
- *   row_ptr[r] (n_rings): ring r's row of this worker's orders in the ring owner's receive
- *     buffer (alm2map); col_ptr[m] (mmax+1): order m's column for this worker's first ring in
- *     the order owner's send buffer, rows m_stride[m] apart (map2alm).
+ *   row_ptr[r] (n_rings): ring r's element of this worker's first order in the ring owner's
+ *     receive buffer, further orders row_stride[r] apart (1 without a synthesis layout)
+ *     (alm2map); col_ptr[m] (mmax+1): order m's column for this worker's first ring in the
+ *     order owner's send buffer, rows m_stride[m] apart (map2alm).
  * NULL clears them. */
 shtc_status shtc_set_exchange_peers(shtc_ctx* ctx, const uint64_t* row_ptr, const uint64_t* col_ptr);
 /* Legendre stage writing Delta through row_ptr; ring analysis writing Delta^S through col_ptr. */

@@ -19,6 +19,7 @@ EXPORTED = [
     "shtc_create", "shtc_destroy", "shtc_last_error", "shtc_device_count", "shtc_set_stream",
     "shtc_set_grid", "shtc_set_band", "shtc_plan", "shtc_plan_stats", "shtc_plan_phase_stats", "shtc_plan_executed", "shtc_alm2map",
     "shtc_map2alm", "shtc_alm2map_dev", "shtc_map2alm_dev", "shtc_set_exchange_layout",
+    "shtc_set_exchange_layout_synthesis",
     "shtc_legendre_alm2map_dev", "shtc_legendre_map2alm_dev", "shtc_ring_synthesis_dev",
     "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
     "shtc_measure_fp64_peak", "shtc_dev_alloc", "shtc_dev_free", "shtc_ipc_handle", "shtc_ipc_open",
@@ -89,6 +90,7 @@ def lib():
                   "shtc_ring_synthesis_dev", "shtc_ring_analysis_dev"):
             getattr(L, f).argtypes = [vp, vp, vp, C.POINTER(Timing)]
         L.shtc_set_exchange_layout.argtypes = [vp, vp, i32, vp, vp, vp]
+        L.shtc_set_exchange_layout_synthesis.argtypes = [vp, vp, vp, vp, vp]
         L.shtc_delta_a.argtypes = [vp, vp, i32, i32, i32, vp, i32, vp, vp, u64p]
         L.shtc_accumulate_alm.argtypes = [vp, vp, i32, vp, i32, vp, i32, i32, vp, u64p]
         L.shtc_device_info.argtypes = [i32, C.c_char_p, i32, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]

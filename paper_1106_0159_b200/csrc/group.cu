@@ -258,15 +258,33 @@ void build_exchange(shtc_group* g) {
         cck(shtc_set_exchange_layout(wi.ctx, row_off.data(), (int)wi.rings.size(), wi.rings.data(), m_base.data(),
                                      m_stride.data()),
             wi, "exchange layout");
+        // synthesis direction: the same blocks order-major ([M_i x R_j]), so the Legendre
+        // kernel's stores (one order, consecutive rings per warp) are contiguous runs
+        std::vector<int64_t> s_row_off(g->n_rings, 0), s_row_stride(g->n_rings, 1), s_m_base(g->mmax + 1, 0),
+            s_m_stride(g->mmax + 1, 1);
+        for (int j = 0; j < W; ++j)
+            for (size_t p = 0; p < g->w[j].rings.size(); ++p) {
+                s_row_off[g->w[j].rings[p]] = wi.send_off[j] + (int64_t)p;
+                s_row_stride[g->w[j].rings[p]] = R[j];
+            }
+        for (int j = 0; j < W; ++j)
+            for (size_t c = 0; c < g->w[j].ms.size(); ++c) s_m_base[g->w[j].ms[c]] = wi.recv_off[j] + (int64_t)c * R[i];
+        // (SHTC_GROUP_RING_MAJOR=1 keeps the ring-major blocks: the comparison layout)
+        static const bool ring_major = std::getenv("SHTC_GROUP_RING_MAJOR") && std::atoi(std::getenv("SHTC_GROUP_RING_MAJOR"));
+        if (!ring_major)
+            cck(shtc_set_exchange_layout_synthesis(wi.ctx, s_row_off.data(), s_row_stride.data(), s_m_base.data(),
+                                                   s_m_stride.data()),
+                wi, "exchange layout (synthesis)");
         if (g->mode == SHTC_EXCHANGE_PEER) {
-            // store targets: ring r's row of worker i's orders in the ring owner's recv block from
-            // i; order m's column (ring position 0) in the order owner's send block for i
+            // store targets: ring r's element of worker i's first order in the ring owner's recv
+            // block from i (order-major); order m's column (ring position 0) in the order
+            // owner's send block for i (ring-major)
             std::vector<uint64_t> row_ptr(g->n_rings, 0), col_ptr(g->mmax + 1, 0);
             for (int j = 0; j < W; ++j) {
                 const Worker& wj = g->w[j];
                 for (size_t p = 0; p < wj.rings.size(); ++p)
-                    row_ptr[wj.rings[p]] =
-                        (uint64_t)wj.recv + 16ull * (uint64_t)(wj.recv_off[i] + (int64_t)p * M[i]);
+                    row_ptr[wj.rings[p]] = (uint64_t)wj.recv +
+                                           16ull * (uint64_t)(wj.recv_off[i] + (int64_t)p * (ring_major ? M[i] : 1));
                 for (size_t c = 0; c < wj.ms.size(); ++c)
                     col_ptr[wj.ms[c]] = (uint64_t)wj.send + 16ull * (uint64_t)(wj.send_off[i] + (int64_t)c);
             }

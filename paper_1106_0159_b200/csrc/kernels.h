@@ -99,6 +99,10 @@ struct LegPlanView {
     // fused exchange (alm2map): ring r's output row is row_ptr[r] (an address in the ring
     // owner's receive buffer, peer memory) instead of delta + row_off[r]; nullptr: local
     double2* const* row_ptr;
+    // element (ring r, order index mi) of the alm2map output at row + mi * row_stride[r]
+    // (nullptr: stride 1, rows of contiguous orders).  m-major exchange blocks (order-major
+    // [|M_i| x |R_j|], stride |R_j|) make a warp's stores -- consecutive rings -- contiguous.
+    const int64_t* row_stride;
     // ScaleLadder::unscaled() (legendre.hpp:26-47, the reference's transparency check): no
     // rescaling, so a stream counts from its seed if the seed is at scale k == 0 and never
     // otherwise (plan-time only: it changes the activation scan)
@@ -180,6 +184,10 @@ struct RingStageArgs {
     // fused exchange (analysis): Delta^S(ring_pos, m) goes to col_ptr[m] + ring_pos *
     // m_stride[m] (an address in the order owner's send buffer, peer memory); nullptr: local
     double2* const* col_ptr;
+    // analysis: the order in which the unfold visits m (thread t takes m_order[t + T j]); the
+    // exchange layouts list orders grouped by owner so consecutive threads store into one
+    // owner's block contiguously.  nullptr: ascending m.
+    const int* m_order;
 };
 
 // size classes.  Generic (any 7-smooth length, in-place mixed radix, odd-length rings):

@@ -75,11 +75,13 @@ __device__ __forceinline__ double rec_step(double A, double x, double q1, double
     return __fma_rn(__dmul_rn(A, x), q1, -q0);
 }
 
-// Delta row of ring r for the alm2map output: the local panel (delta + row_off[r]) or, on the
-// fused exchange path, ring r's row in its owner's receive buffer (peer memory over NVLink)
-__device__ __forceinline__ double2* leg_row(const LegPlanView& p, double2* delta,
-                                            const int64_t* __restrict__ row_off, int r) {
-    return p.row_ptr ? p.row_ptr[r] : delta + row_off[r];
+// Delta element (ring r, order index mi) of the alm2map output: in the local panel (delta +
+// row_off[r]) or, on the fused exchange path, in ring r's owner's receive buffer (peer memory
+// over NVLink); orders row_stride[r] apart (m-major exchange blocks) or contiguous
+__device__ __forceinline__ double2* leg_out(const LegPlanView& p, double2* delta,
+                                            const int64_t* __restrict__ row_off, int r, int mi) {
+    double2* row = p.row_ptr ? p.row_ptr[r] : delta + row_off[r];
+    return row + (p.row_stride ? (int64_t)mi * p.row_stride[r] : (int64_t)mi);
 }
 
 }  // namespace
@@ -471,8 +473,8 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
             if (s >= p.st.n) continue;
             const double2 e = L.ae[r], o = L.ao[r];  // dead lanes stayed zero
             const int north = p.st.north[s], south = p.st.south[s];
-            leg_row(p, delta, row_off, north)[mi] = cadd(e, o);
-            if (south >= 0) leg_row(p, delta, row_off, south)[mi] = csub(e, o);
+            *leg_out(p, delta, row_off, north, mi) = cadd(e, o);
+            if (south >= 0) *leg_out(p, delta, row_off, south, mi) = csub(e, o);
         }
     }
 }
@@ -486,9 +488,9 @@ __global__ void leg_zero_dead_kernel(LegPlanView p, double2* __restrict__ delta,
     const int t = s / LEG_TILE;
     if (p.tile_info[(size_t)mi * p.n_tiles + t].x >= 0) return;
     const double2 z = make_double2(0.0, 0.0);
-    leg_row(p, delta, row_off, p.st.north[s])[mi] = z;
+    *leg_out(p, delta, row_off, p.st.north[s], mi) = z;
     const int south = p.st.south[s];
-    if (south >= 0) leg_row(p, delta, row_off, south)[mi] = z;
+    if (south >= 0) *leg_out(p, delta, row_off, south, mi) = z;
 }
 
 int leg_persistent_blocks(int device) {

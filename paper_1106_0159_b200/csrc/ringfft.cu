@@ -869,23 +869,37 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
         const bool rot = d.phi0 != 0.0;
         const double2* __restrict__ hw = a.tabs + d.hw_off;
         const int Tn = T % n;
+        const int* __restrict__ mord = a.m_order;
         for (int m0 = t; m0 <= mmax; m0 += U * T) {
             // branch-free batch: indices clamped, table loads issued together, stores masked
-            int bb[U];
+            int bb[U], mm[U];
             bool cj[U];
             double2 w[U];
-            int b = m0 % n;
+            if (mord) {  // exchange layouts: orders grouped by owner
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                cj[u] = b > N;
-                bb[u] = cj[u] ? n - b : b;
-                w[u] = __ldg(&hw[bb[u]]);
-                b += Tn;
-                if (b >= n) b -= n;
+                for (int u = 0; u < U; ++u) {
+                    const int idx = m0 + u * T;
+                    mm[u] = idx <= mmax ? __ldg(mord + idx) : mmax + 1;
+                    const int b = (idx <= mmax ? mm[u] : 0) % n;
+                    cj[u] = b > N;
+                    bb[u] = cj[u] ? n - b : b;
+                    w[u] = __ldg(&hw[bb[u]]);
+                }
+            } else {
+                int b = m0 % n;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    mm[u] = m0 + u * T;
+                    cj[u] = b > N;
+                    bb[u] = cj[u] ? n - b : b;
+                    w[u] = __ldg(&hw[bb[u]]);
+                    b += Tn;
+                    if (b >= n) b -= n;
+                }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
-                const int m = m0 + u * T;
+                const int m = mm[u];
                 const double2 Zp = buf[p2pad(bb[u] == N ? 0 : bb[u])];
                 const double2 Zq = buf[p2pad(bb[u] == 0 ? 0 : N - bb[u])];
                 const double2 e = cscale(cadd(Zp, cconj(Zq)), 0.5);
@@ -1061,7 +1075,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                 const double wgt = d.weight;
                 const bool rot = d.phi0 != 0.0;
                 const double2* __restrict__ hw = a.tabs + d.hw_off;
-                for (int m = t; m <= mmax; m += T) {
+                for (int idx = t; idx <= mmax; idx += T) {
+                    const int m = a.m_order ? __ldg(a.m_order + idx) : idx;
                     const int b = m % n;
                     const bool cj = b > N;
                     const int bb = cj ? n - b : b;
@@ -1237,7 +1252,8 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_anal_kerne
     }
 
     // ---- unfold: Delta^S_m = w * bins[m mod n] * e^{-i m phi0} (fourier.cpp:42-47) ----
-    for (int m = t; m <= mmax; m += T) {
+    for (int idx = t; idx <= mmax; idx += T) {
+        const int m = a.m_order ? __ldg(a.m_order + idx) : idx;
         const int b = m % n;
         double2 val;
         if (half) {

@@ -234,6 +234,10 @@ struct shtc_ctx {
     std::vector<int> ring_list;
     std::vector<int64_t> m_base, m_stride;
     DevBuf row_off_d, m_base_d, m_stride_d;
+    DevBuf m_order_d;  // the orders by m_base: each owner's block contiguous (analysis unfold)
+    // synthesis-direction override (shtc_set_exchange_layout_synthesis): order-major blocks
+    bool syn_layout = false;
+    DevBuf syn_row_off_d, syn_row_stride_d, syn_m_base_d, syn_m_stride_d;
     // fused exchange over peer memory: per-ring row / per-order column addresses in the
     // owners' buffers (valid on this device: NVLink peer mappings or CUDA IPC)
     DevBuf peer_row_ptr, peer_col_ptr;
@@ -973,11 +977,12 @@ void run_ring_synth(shtc_ctx* c, FftPlan& F, const double2* delta, double* map,
 
 void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, const int64_t* mb,
                    const int64_t* mst, int range = -1, double2* const* col_ptr = nullptr,
-                   cudaStream_t s = nullptr) {
+                   cudaStream_t s = nullptr, const int* m_order = nullptr) {
     ring_stage(c, F, range, s ? s : c->stream, [&](int k, RingStageArgs& a, cudaStream_t st) {
         a.m_base = mb;
         a.m_stride = mst;
         a.col_ptr = col_ptr;
+        a.m_order = m_order;
         a.map_in = map;
         a.delta_out = delta;
         launch_ring_analysis(k, a, st);
@@ -1151,6 +1156,7 @@ shtc_status shtc_set_grid(shtc_ctx* ctx, int n_rings, const double* cos_theta, c
         ctx->fft_custom.built = false;
         ctx->id_row_off.release();
         ctx->custom_layout = false;
+        ctx->syn_layout = false;
         ctx->peers_set = false;  // peer targets index the old ring / order layout
     });
 }
@@ -1176,6 +1182,7 @@ shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int3
         ctx->leg.built = false;
         ctx->id_row_off.release();
         ctx->custom_layout = false;
+        ctx->syn_layout = false;
         ctx->peers_set = false;
     });
 }
@@ -1612,6 +1619,7 @@ shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int 
     return guarded(ctx, [&] {
         if (!ctx->grid_set || !ctx->band_set) fail(SHTC_EINVAL, "set grid and band first");
         ctx->peers_set = false;  // the peer targets are rebuilt on top of the new layout
+        ctx->syn_layout = false;
         if (!row_off) {
             ctx->custom_layout = false;
             return;
@@ -1631,8 +1639,37 @@ shtc_status shtc_set_exchange_layout(shtc_ctx* ctx, const int64_t* row_off, int 
         ctx->row_off_d.upload(ctx->row_off, ctx->stream);
         ctx->m_base_d.upload(ctx->m_base, ctx->stream);
         ctx->m_stride_d.upload(ctx->m_stride, ctx->stream);
+        std::vector<int> order(ctx->mmax + 1);
+        std::iota(order.begin(), order.end(), 0);
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int x, int y) { return ctx->m_base[x] < ctx->m_base[y]; });
+        // (SHTC_UNFOLD_ASCENDING=1: ascending m, the comparison order for the coalescing
+        // measurement in tools/exchange_coalesce.py)
+        static const bool ascending = std::getenv("SHTC_UNFOLD_ASCENDING") && std::atoi(std::getenv("SHTC_UNFOLD_ASCENDING"));
+        if (ascending) std::iota(order.begin(), order.end(), 0);
+        ctx->m_order_d.upload(order, ctx->stream);
         build_fft_plan(ctx, ctx->fft_custom, ctx->ring_list);
         ctx->custom_layout = true;
+    });
+}
+
+shtc_status shtc_set_exchange_layout_synthesis(shtc_ctx* ctx, const int64_t* row_off, const int64_t* row_stride,
+                                               const int64_t* m_base, const int64_t* m_stride) {
+    if (!ctx) return SHTC_EINVAL;
+    return guarded(ctx, [&] {
+        ctx->peers_set = false;  // row_ptr targets are read with this layout's strides
+        if (!row_off) {
+            ctx->syn_layout = false;
+            return;
+        }
+        if (!ctx->custom_layout) fail(SHTC_EINVAL, "exchange layout (synthesis): set the exchange layout first");
+        if (!row_stride || !m_base || !m_stride) fail(SHTC_EINVAL, "exchange layout (synthesis): malformed");
+        ctx->syn_row_off_d.upload(std::vector<int64_t>(row_off, row_off + ctx->n_rings), ctx->stream);
+        ctx->syn_row_stride_d.upload(std::vector<int64_t>(row_stride, row_stride + ctx->n_rings), ctx->stream);
+        ctx->syn_m_base_d.upload(std::vector<int64_t>(m_base, m_base + ctx->mmax + 1), ctx->stream);
+        ctx->syn_m_stride_d.upload(std::vector<int64_t>(m_stride, m_stride + ctx->mmax + 1), ctx->stream);
+        CK(cudaStreamSynchronize(ctx->stream));
+        ctx->syn_layout = true;
     });
 }
 
@@ -1649,9 +1686,11 @@ shtc_status shtc_legendre_alm2map_dev(shtc_ctx* ctx, const double* alm_dev, doub
     if (!ctx || !alm_dev || !delta_dev) return SHTC_EINVAL;
     return guarded(ctx, [&] {
         ensure_leg_plan(ctx);
-        const int64_t* ro = stage_row_off(ctx);
+        const int64_t* ro = ctx->syn_layout ? ctx->syn_row_off_d.as<int64_t>() : stage_row_off(ctx);
+        LegPlanView v = ctx->leg.view;
+        if (ctx->syn_layout) v.row_stride = ctx->syn_row_stride_d.as<int64_t>();
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        launch_leg_alm2map(ctx->leg.view, reinterpret_cast<const double2*>(alm_dev),
+        launch_leg_alm2map(v, reinterpret_cast<const double2*>(alm_dev),
                            reinterpret_cast<double2*>(delta_dev), ro, ctx->leg.counters.as<int>(),
                            ctx->stream);
         CK(cudaGetLastError());
@@ -1692,8 +1731,8 @@ shtc_status shtc_ring_synthesis_dev(shtc_ctx* ctx, const double* delta_dev, doub
         const int64_t *mb, *mst;
         if (ctx->custom_layout) {
             F = &ctx->fft_custom;
-            mb = ctx->m_base_d.as<int64_t>();
-            mst = ctx->m_stride_d.as<int64_t>();
+            mb = (ctx->syn_layout ? ctx->syn_m_base_d : ctx->m_base_d).as<int64_t>();
+            mst = (ctx->syn_layout ? ctx->syn_m_stride_d : ctx->m_stride_d).as<int64_t>();
         } else {
             require_full_band(ctx);
             ensure_fft_id(ctx);
@@ -1732,7 +1771,8 @@ shtc_status shtc_ring_analysis_dev(shtc_ctx* ctx, const double* map_dev, double*
             mst = nullptr;
         }
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
-        run_ring_anal(ctx, *F, map_dev, reinterpret_cast<double2*>(delta_dev), mb, mst);
+        run_ring_anal(ctx, *F, map_dev, reinterpret_cast<double2*>(delta_dev), mb, mst, -1, nullptr, nullptr,
+                      ctx->custom_layout ? ctx->m_order_d.as<int>() : nullptr);
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (t) {
             CK(cudaEventSynchronize(ctx->ev[1]));
@@ -1815,9 +1855,11 @@ shtc_status shtc_legendre_alm2map_peer(shtc_ctx* ctx, const double* alm_dev, sht
         ensure_leg_plan(ctx);
         LegPlanView v = ctx->leg.view;
         v.row_ptr = ctx->peer_row_ptr.as<double2*>();
+        if (ctx->syn_layout) v.row_stride = ctx->syn_row_stride_d.as<int64_t>();
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         launch_leg_alm2map(v, reinterpret_cast<const double2*>(alm_dev), nullptr,
-                           ctx->row_off_d.as<int64_t>(), ctx->leg.counters.as<int>(), ctx->stream);
+                           (ctx->syn_layout ? ctx->syn_row_off_d : ctx->row_off_d).as<int64_t>(),
+                           ctx->leg.counters.as<int>(), ctx->stream);
         CK(cudaGetLastError());
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (t) {
@@ -1835,7 +1877,8 @@ shtc_status shtc_ring_analysis_peer(shtc_ctx* ctx, const double* map_dev, shtc_t
             fail(SHTC_EINVAL, "exchange peers not set");
         CK(cudaEventRecord(ctx->ev[0], ctx->stream));
         run_ring_anal(ctx, ctx->fft_custom, map_dev, nullptr, ctx->m_base_d.as<int64_t>(),
-                      ctx->m_stride_d.as<int64_t>(), -1, ctx->peer_col_ptr.as<double2*>());
+                      ctx->m_stride_d.as<int64_t>(), -1, ctx->peer_col_ptr.as<double2*>(), nullptr,
+                      ctx->m_order_d.as<int>());
         CK(cudaEventRecord(ctx->ev[1], ctx->stream));
         if (t) {
             CK(cudaEventSynchronize(ctx->ev[1]));

@@ -401,6 +401,38 @@ def exchange_layout(layout: WorkerLayout, rank: int):
     return row_off, send_counts, recv_counts, np.asarray(Ri, np.int32), m_base, m_stride
 
 
+def exchange_layout_synthesis(layout: WorkerLayout, rank: int):
+    """Order-major synthesis layout of one worker (shtc_set_exchange_layout_synthesis): the
+    same blocks and offsets as exchange_layout, each block [orders x rings].
+
+    Send side (Legendre output): ring r = R_j[p] of this worker's order index c at
+    row_off[r] + c * row_stride[r] with row_off[r] = block offset + p, row_stride[r] = |R_j|,
+    so a warp's stores (one order, consecutive rings) are contiguous.  Receive side: order m
+    (index c in M_j) of ring position p at m_base[m] + p, m_base[m] = block offset + c |R_rank|,
+    m_stride = 1.  Returns (row_off, row_stride, m_base, m_stride) in complex units."""
+    W = layout.n_workers
+    Mi = layout.m_sets[rank]
+    row_off = np.zeros(layout.n_rings, np.int64)
+    row_stride = np.ones(layout.n_rings, np.int64)
+    off = 0
+    for j in range(W):
+        Rj = layout.ring_sets[j]
+        for p, r in enumerate(Rj):
+            row_off[r] = off + p
+            row_stride[r] = len(Rj)
+        off += len(Rj) * len(Mi)
+    Ri = layout.ring_sets[rank]
+    m_base = np.zeros(layout.mmax + 1, np.int64)
+    m_stride = np.ones(layout.mmax + 1, np.int64)
+    off = 0
+    for j in range(W):
+        Mj = layout.m_sets[j]
+        for c, m in enumerate(Mj):
+            m_base[m] = off + c * len(Ri)
+        off += len(Ri) * len(Mj)
+    return row_off, row_stride, m_base, m_stride
+
+
 def exchange_sizes(layout: WorkerLayout, rank: int):
     """(send, recv) buffer sizes of one worker in complex elements."""
     Mi, Ri = len(layout.m_sets[rank]), len(layout.ring_sets[rank])
@@ -409,13 +441,16 @@ def exchange_sizes(layout: WorkerLayout, rank: int):
     return send, recv
 
 
-def peer_exchange_pointers(layout: WorkerLayout, rank: int, recv_bases, send_bases):
+def peer_exchange_pointers(layout: WorkerLayout, rank: int, recv_bases, send_bases,
+                           order_major: bool = True):
     """Store targets of worker `rank` on the fused exchange path (shtc_set_exchange_peers).
 
     recv_bases[j] / send_bases[j]: device addresses (valid in this process) of worker j's
-    receive / send buffers, laid out as exchange_layout describes.  Returns
-      row_ptr[r]: where ring r's row of this worker's orders goes in the ring owner's receive
-                  buffer (the block from source `rank`, row pos * |M_rank|);
+    receive / send buffers, laid out as exchange_layout (map2alm) and, with order_major,
+    exchange_layout_synthesis (alm2map) describe.  Returns
+      row_ptr[r]: where ring r's element of this worker's first order goes in the ring owner's
+                  receive buffer (the block from source `rank`: position pos, further orders
+                  |R_owner| apart; ring-major without order_major: row pos * |M_rank|);
       col_ptr[m]: order m's column for this worker's ring position 0 in the order owner's send
                   buffer (the block for destination `rank`), rows |M_owner| apart (m_stride).
     Byte addresses as uint64 (16-byte complex elements)."""
@@ -426,7 +461,7 @@ def peer_exchange_pointers(layout: WorkerLayout, rank: int, recv_bases, send_bas
     for j in range(W):
         off = sum(Rsz[j] * Msz[s] for s in range(rank))  # block of source `rank` in j's recv
         for pos, r in enumerate(layout.ring_sets[j]):
-            row_ptr[r] = int(recv_bases[j]) + 16 * (off + pos * Msz[rank])
+            row_ptr[r] = int(recv_bases[j]) + 16 * (off + (pos if order_major else pos * Msz[rank]))
     col_ptr = np.zeros(layout.mmax + 1, np.uint64)
     for i in range(W):
         soff = sum(Rsz[d] * Msz[i] for d in range(rank))  # block for destination `rank` in i's send
@@ -544,6 +579,13 @@ class Context:
         mb = np.ascontiguousarray(m_base, np.int64)
         mst = np.ascontiguousarray(m_stride, np.int64)
         self._check(lib().shtc_set_exchange_layout(self._h, _p(ro), len(rl), _p(rl), _p(mb), _p(mst)))
+
+    def set_exchange_layout_synthesis(self, row_off=None, row_stride=None, m_base=None, m_stride=None):
+        if row_off is None:
+            self._check(lib().shtc_set_exchange_layout_synthesis(self._h, None, None, None, None))
+            return
+        a = [np.ascontiguousarray(x, np.int64) for x in (row_off, row_stride, m_base, m_stride)]
+        self._check(lib().shtc_set_exchange_layout_synthesis(self._h, *[_p(x) for x in a]))
 
     def legendre_alm2map_dev(self, alm_ptr, delta_ptr, timing=False):
         t = Timing()
@@ -666,8 +708,10 @@ class PeerExchange:
         map2alm: ring_analysis_peer(map) -> barrier -> legendre_map2alm_dev(send, alm)
     """
 
-    def __init__(self, ctx: Context, layout: WorkerLayout, rank: int, all_gather=None, peers=None):
+    def __init__(self, ctx: Context, layout: WorkerLayout, rank: int, all_gather=None, peers=None,
+                 order_major: bool = True):
         self.ctx, self.layout, self.rank = ctx, layout, rank
+        self.order_major = order_major
         W = layout.n_workers
         self.n = W
         send_c, recv_c = exchange_sizes(layout, rank)
@@ -700,9 +744,13 @@ class PeerExchange:
         a single-process group is constructed)."""
         row_off, send_c, recv_c, ring_list, m_base, m_stride = exchange_layout(self.layout, self.rank)
         self.ctx.set_exchange_layout(row_off, ring_list, m_base, m_stride)
+        # alm2map blocks order-major: every warp's NVLink stores are contiguous runs
+        # (order_major=False keeps the ring-major blocks of map2alm, the comparison layout)
+        if self.order_major:
+            self.ctx.set_exchange_layout_synthesis(*exchange_layout_synthesis(self.layout, self.rank))
         send_b = [p[0] for p in self._peers]
         recv_b = [p[1] for p in self._peers]
-        row_ptr, col_ptr = peer_exchange_pointers(self.layout, self.rank, recv_b, send_b)
+        row_ptr, col_ptr = peer_exchange_pointers(self.layout, self.rank, recv_b, send_b, self.order_major)
         self.ctx.set_exchange_peers(row_ptr, col_ptr)
         self._flag_ptrs = np.array([p[2] for p in self._peers], np.uint64)
         # build every plan now: no allocation or synchronising call may run once a worker's

@@ -28,7 +28,8 @@ def alltoall(sends, send_counts, recv_counts, W):
                                                  (64, 128, 4, "blocks"), (128, 256, 8, "blocks"),
                                                  (256, 512, 1, "blocks"), (64, 128, 4, "balanced"),
                                                  (128, 256, 8, "balanced"), (16, 40, 3, "interleaved")])
-def test_stage_path_matches_single_worker(nside, lmax, W, rings):
+@pytest.mark.parametrize("order_major", [True, False])
+def test_stage_path_matches_single_worker(nside, lmax, W, rings, order_major):
     dev = torch.device("cuda", 0)
     grid = sht.build_healpix_grid(nside)
     alm_h = sht.random_alm(lmax, lmax, 99)
@@ -48,6 +49,8 @@ def test_stage_path_matches_single_worker(nside, lmax, W, rings):
         meta = sht.exchange_layout(layout, w)
         row_off, send_c, recv_c, ring_list, m_base, m_stride = meta
         c.set_exchange_layout(row_off, ring_list, m_base, m_stride)
+        if order_major:  # alm2map blocks order-major (the fused / NCCL default)
+            c.set_exchange_layout_synthesis(*sht.exchange_layout_synthesis(layout, w))
         ctxs.append(c)
         metas.append(meta)
     send_counts = [m[1] for m in metas]

@@ -36,7 +36,7 @@ def _single(nside, lmax, seed):
 # another worker's waiting barrier kernel, so the one-process case runs in a fresh process with
 # 32 connections.  One process per GPU (the multi-GPU layout, and the IPC test below) does not
 # share queues between workers.
-def _one_process(nside, lmax, W, q):
+def _one_process(nside, lmax, W, q, order_major=True):
     try:
         dev = torch.device("cuda", 0)
         grid, alm_h, want_map, want_alm = _single(nside, lmax, 99)
@@ -47,7 +47,7 @@ def _one_process(nside, lmax, W, q):
             c = sht.Context(0)
             c.set_grid(grid)
             c.set_band(lmax, lmax, layout.m_sets[w])
-            xs.append(sht.PeerExchange(c, layout, w, peers=peers))
+            xs.append(sht.PeerExchange(c, layout, w, peers=peers, order_major=order_major))
         for x in xs:
             x.connect()
         alm = torch.from_numpy(alm_h.view(np.float64)).to(dev)
@@ -72,15 +72,17 @@ def _one_process(nside, lmax, W, q):
         q.put(("error", repr(e)))
 
 
-@pytest.mark.parametrize("nside,lmax,W", [(8, 16, 2), (32, 64, 3), (64, 128, 4), (128, 256, 4), (128, 256, 8)])
-def test_fused_exchange_one_process(nside, lmax, W):
+@pytest.mark.parametrize("nside,lmax,W,order_major", [(8, 16, 2, True), (32, 64, 3, True), (64, 128, 4, True),
+                                                      (128, 256, 4, True), (128, 256, 8, True),
+                                                      (64, 128, 4, False)])
+def test_fused_exchange_one_process(nside, lmax, W, order_major):
     import torch.multiprocessing as mp
     os.environ["CUDA_DEVICE_MAX_CONNECTIONS"] = "32"  # inherited by the spawned process
     os.environ["SHTC_FFT_AUX"] = "2"  # W contexts x 3 ring-stage streams stay within 32 queues
     try:
         ctx = mp.get_context("spawn")
         q = ctx.Queue()
-        p = ctx.Process(target=_one_process, args=(nside, lmax, W, q))
+        p = ctx.Process(target=_one_process, args=(nside, lmax, W, q, order_major))
         p.start()
         status, res = q.get(timeout=300)
         p.join(timeout=60)

@@ -4,7 +4,9 @@ must put every Delta entry exactly where the packed all-to-all would have delive
 
 Device memory is emulated: each worker's send / receive buffer is a numpy array at a fake base
 address, and the kernels' stores are replayed with the same address arithmetic
-(legendre.cu leg_row: row_ptr[r] + mi; ringfft.cu delta_out_at: col_ptr[m] + pos m_stride[m]).
+(legendre.cu leg_out: row_ptr[r] + mi row_stride[r]; ringfft.cu delta_out_at: col_ptr[m] +
+pos m_stride[m]).  Both synthesis layouts are covered: order-major blocks (the default: a
+warp's stores are contiguous runs) and the ring-major blocks shared with map2alm.
 The gloo case runs the pointer setup with the base addresses gathered across 2 processes.
 """
 import os
@@ -44,18 +46,29 @@ def _store(mem, addr, val):
     raise AssertionError(f"store outside every exchange buffer: {addr:#x}")
 
 
-def _replay(layout, send, recv, mem):
+def _synthesis_layout(layout, j, order_major):
+    """(row_stride, m_base, m_stride) of worker j's alm2map direction"""
+    if order_major:
+        _, row_stride, m_base, m_stride = sht.exchange_layout_synthesis(layout, j)
+        return row_stride, m_base, m_stride
+    _, _, _, _, m_base, m_stride = sht.exchange_layout(layout, j)
+    return np.ones(layout.n_rings, np.int64), m_base, m_stride
+
+
+def _replay(layout, send, recv, mem, order_major=True):
     W = layout.n_workers
-    ptrs = [sht.peer_exchange_pointers(layout, i, recv, send) for i in range(W)]
+    ptrs = [sht.peer_exchange_pointers(layout, i, recv, send, order_major) for i in range(W)]
     # alm2map: worker i's Legendre stage stores Delta(r, M_i[mi]) through row_ptr
     for i in range(W):
         row_ptr, _ = ptrs[i]
+        row_stride, _, _ = _synthesis_layout(layout, i, order_major)
         for r in range(layout.n_rings):
             for mi, m in enumerate(layout.m_sets[i]):
-                _store(mem, int(row_ptr[r]) + 16 * mi, code(r, m))
+                _store(mem, int(row_ptr[r]) + 16 * mi * int(row_stride[r]), code(r, m))
     # the ring stage of worker j reads Delta(pos, m) at m_base[m] + pos m_stride[m]
     for j in range(W):
-        _, _, _, ring_list, m_base, m_stride = sht.exchange_layout(layout, j)
+        ring_list = sht.exchange_layout(layout, j)[3]
+        _, m_base, m_stride = _synthesis_layout(layout, j, order_major)
         rv = mem[recv[j]]
         for pos, r in enumerate(ring_list):
             for m in range(layout.mmax + 1):
@@ -79,12 +92,38 @@ def _replay(layout, send, recv, mem):
 @pytest.mark.parametrize("nside,lmax,W,rings", [(2, 5, 1, "blocks"), (4, 12, 2, "blocks"), (4, 12, 3, "blocks"),
                                                  (8, 16, 4, "blocks"), (4, 9, 5, "blocks"), (8, 16, 4, "balanced"),
                                                  (4, 12, 3, "interleaved")])
-def test_peer_pointers_deliver_like_the_all_to_all(nside, lmax, W, rings):
+@pytest.mark.parametrize("order_major", [True, False])
+def test_peer_pointers_deliver_like_the_all_to_all(nside, lmax, W, rings, order_major):
     layout = sht.WorkerLayout.create(sht.build_healpix_grid(nside), lmax, W, rings=rings)
     send, recv, mem = _fake_bases(layout)
-    _replay(layout, send, recv, mem)
+    _replay(layout, send, recv, mem, order_major)
     for buf in mem.values():  # every slot of every exchange buffer written exactly as planned
         assert np.all(buf != 0)
+
+
+@pytest.mark.parametrize("W,rings", [(2, "blocks"), (4, "balanced"), (3, "interleaved")])
+def test_fused_stores_are_contiguous_runs(W, rings):
+    """The NVLink side of both directions coalesces: alm2map's Legendre stores (one order,
+    consecutive rings of one owner per warp) land 16 bytes apart in the order-major blocks;
+    map2alm's unfold, visiting orders grouped by owner (ascending m_base = the kernels'
+    m_order), stores each owner's orders of one ring 16 bytes apart."""
+    layout = sht.WorkerLayout.create(sht.build_healpix_grid(16), 40, W, rings=rings)
+    send, recv, _ = _fake_bases(layout)
+    for i in range(W):
+        row_ptr, col_ptr = sht.peer_exchange_pointers(layout, i, recv, send)
+        row_stride = sht.exchange_layout_synthesis(layout, i)[1]
+        for j in range(W):
+            Rj = layout.ring_sets[j]
+            for mi in range(len(layout.m_sets[i])):
+                addr = [int(row_ptr[r]) + 16 * mi * int(row_stride[r]) for r in Rj]
+                assert np.all(np.diff(addr) == 16)
+        m_base, m_stride = sht.exchange_layout(layout, i)[4:6]
+        order = np.argsort(m_base, kind="stable")
+        for j in range(W):  # order owners: a contiguous run of `order` each
+            mine = [m for m in order if m in set(layout.m_sets[j])]
+            for pos in (0, len(layout.ring_sets[i]) - 1):
+                addr = [int(col_ptr[m]) + 16 * pos * int(m_stride[m]) for m in mine]
+                assert np.all(np.diff(addr) == 16)
 
 
 def test_peer_pointers_gauss_legendre_grid():
