@@ -214,11 +214,48 @@ CostReport build_report(double r_n, double lmax, double mmax, int n_workers, con
     return rep;
 }
 
+namespace {
+// comm_time = alpha * ca + beta * cb for the branch the message size selects
+std::pair<double, double> comm_coeffs(double s, int n_workers, const CostParams& p) {
+    if (n_workers <= 1) return {0.0, 0.0};
+    const double n = n_workers;
+    if (s <= p.switch_bytes) return {std::log2(n), s * (n / 2.0) * std::log2(n)};
+    return {n - 1.0, s * (n - 1.0)};
+}
+}  // namespace
+
 CostParams calibrate(const CostParams& base, double r_n, double lmax, double mmax, int n_workers,
                      const Profiler& prof) {
     CostParams p = base;
     const auto f = flops_estimate(r_n, lmax, mmax, n_workers);
     if (f.recurrence > 0 && prof.recurrence_s > 0) p.gamma = prof.recurrence_s / f.recurrence;
+    if (n_workers > 1 && prof.exchange_s > 0 && prof.exchange_bytes > 0) {
+        const auto [ca, cb] = comm_coeffs(message_size(r_n, mmax, n_workers, p.n_c), n_workers, p);
+        const double rest = prof.exchange_s - p.alpha * ca;
+        if (cb > 0 && rest > 0) p.beta_inv_bw = rest / cb;
+    }
+    return p;
+}
+
+CostParams fit_exchange(const CostParams& base, std::span<const ExchangeSample> samples) {
+    // normal equations of min sum (alpha ca_i + beta cb_i - t_i)^2
+    double aa = 0, ab = 0, bb = 0, at = 0, bt = 0;
+    for (const auto& x : samples) {
+        if (x.n_workers < 2 || x.msg_bytes < 0 || x.seconds < 0)
+            throw std::invalid_argument("fit_exchange: samples need n_workers >= 2 and non-negative sizes");
+        const auto [ca, cb] = comm_coeffs(x.msg_bytes, x.n_workers, base);
+        aa += ca * ca;
+        ab += ca * cb;
+        bb += cb * cb;
+        at += ca * x.seconds;
+        bt += cb * x.seconds;
+    }
+    const double det = aa * bb - ab * ab;
+    if (!(std::fabs(det) > 1e-12 * std::max(aa * bb, 1e-300)))
+        throw std::invalid_argument("fit_exchange: samples do not determine alpha and beta");
+    CostParams p = base;
+    p.alpha = (at * bb - ab * bt) / det;
+    p.beta_inv_bw = (aa * bt - ab * at) / det;
     return p;
 }
 

@@ -46,6 +46,25 @@ int main(int argc, char** argv) {
     prof.recurrence_s = 0.01;
     const auto cal = sht::calibrate(p, 255, 128, 128, 2, prof);
     CHECK(std::fabs(cal.gamma - 0.01 / sht::flops_estimate(255, 128, 128, 2).recurrence) < 1e-25, "calibrate gamma");
+    // exchange recalibration: beta from a profiled exchange (alpha's share removed), and the
+    // least-squares fit recovering known alpha / beta exactly from samples of both branches
+    prof.exchange_s = 1e-3;
+    prof.exchange_bytes = 123456;
+    const double s_msg = sht::message_size(255, 128, 2, p.n_c);
+    const auto cal2 = sht::calibrate(p, 255, 128, 128, 2, prof);
+    CHECK(std::fabs(sht::comm_time(s_msg, 2, cal2) - 1e-3) < 1e-15, "calibrate beta reproduces the exchange");
+    sht::CostParams truth;
+    truth.alpha = 7.5e-6;
+    truth.beta_inv_bw = 1.0 / 640e9;
+    std::vector<sht::ExchangeSample> xs;
+    for (int n : {2, 4, 8})
+        for (double b : {4096.0, 1e5, 1e6, 3e7}) xs.push_back({n, b, sht::comm_time(b, n, truth)});
+    const auto fit = sht::fit_exchange(p, xs);
+    CHECK(std::fabs(fit.alpha - truth.alpha) < 1e-12 && std::fabs(fit.beta_inv_bw / truth.beta_inv_bw - 1.0) < 1e-9,
+          "fit_exchange recovers alpha and beta");
+    CHECK(throws<std::invalid_argument>([&] { sht::fit_exchange(p, std::span(xs.data(), 1)); }), "fit needs 2 samples");
+    prof.exchange_s = 0.0;
+    prof.exchange_bytes = 0;
     const auto rep = sht::build_report(255, 128, 128, 2, &prof, sht::CostParams::b200());
     CHECK(rep.stages.size() == 4 && rep.stages[1].has_measured && rep.stages[1].measured_s == 0.01, "report");
     // containers round trip bit for bit
