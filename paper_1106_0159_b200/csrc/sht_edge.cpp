@@ -134,8 +134,12 @@ AlmSet read_alm(const std::string& path) {
 // ---- performance model ----------------------------------------------------------------------
 CostParams CostParams::b200() {
     CostParams p;
-    p.alpha = 2.0e-5;            // NCCL all-to-all launch + handshake on NVLink 5 / NVSwitch
-    p.beta_inv_bw = 1.0 / 770e9; // measured peer copy, per direction per GPU (B200_PROFILING.md)
+    p.alpha = 1.1e-5;            // one fused-exchange barrier round per worker, launch included:
+                                 // 22.8 us for 2 workers, 75.7 us for 8 on one B200
+                                 // (tools/calibrate_exchange.py, profiles/r02_exchange_calibration.json)
+    p.beta_inv_bw = 1.0 / 770e9; // peer copy per direction per GPU as the B200 profiling guide
+                                 // measured it (a 1-GPU box has no NVLink to time; fit_exchange
+                                 // refits alpha and beta from multi-GPU samples)
     p.gamma = 1.42e-14;          // Legendre seconds per model flop at C4: (6.90 + 8.65) / 2 ms over
                                  // 4 R_N lmax mmax = 549.7 G (round 1, 1 GPU, profiles/r01_bench.json)
     return p;
