@@ -390,8 +390,9 @@ int a2m_head_bands() {
 }
 
 // map2alm pipeline: the band after whose ring analysis each band's Legendre items launch
-// (default: every band on its own; SHTC_M2A_GROUPS="1,1,2,2,2" = band counts per launch --
-// merged launches measured slower at C4).
+// (SHTC_M2A_GROUPS="1,1,2,2,2" = band counts per launch).  Default: every band on its own
+// except the last two, which launch together split by order chunk (C4 map2alm from pinned
+// memory 12.50 -> 12.13 ms median; merging more bands measured slower, 12.3-15.5 ms).
 std::vector<int> m2a_launch_bands() {
     std::vector<int> sizes;
     if (const char* e = std::getenv("SHTC_M2A_GROUPS")) {
@@ -402,6 +403,10 @@ std::vector<int> m2a_launch_bands() {
         }
     } else {
         sizes.assign(kPipeBands, 1);
+        if (kPipeBands >= 3) {
+            sizes.pop_back();
+            sizes.back() = 2;
+        }
     }
     std::vector<int> tag(kPipeBands, kPipeBands - 1);
     int first = 0;
