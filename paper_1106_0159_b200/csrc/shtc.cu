@@ -358,14 +358,24 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     static const double w0 = std::getenv("SHTC_BAND0_WEIGHT") ? std::atof(std::getenv("SHTC_BAND0_WEIGHT")) : 0.5;
     std::vector<double> cum(kPipeBands + 1, 0.0);
     for (int k = 0; k < kPipeBands; ++k) cum[k + 1] = cum[k] + (k == 0 ? w0 : 1.0);
+    // Bands are assigned per tile PAIR counted from the equatorial end (tiles nt-1 and nt-2,
+    // nt-3 and nt-4, ...): the map2alm kernel runs an item's tiles two at a time, and with no
+    // band boundary inside a pair only an order's most polar alive tile can be left to run
+    // on its own (16% of the C4 map2alm steps ran as single tiles with per-tile bands).
+    static const bool pairs = !std::getenv("SHTC_BAND_PAIRS") || std::atoi(std::getenv("SHTC_BAND_PAIRS")) != 0;
     std::vector<int> band(nt);
-    int64_t acc = 0;  // pixels of the tiles polar of t
-    for (int t = 0; t < nt; ++t) {
-        const double eq = (double)(total - acc - pix[t]) / (double)std::max<int64_t>(total, 1) * cum[kPipeBands];
+    int64_t acc = 0;  // pixels of the tiles polar of the pair
+    for (int t = 0; t < nt;) {
+        // pair {t, t+1} when (nt - 1 - t) is odd, i.e. t and t+1 are one pair from the top
+        const int len = (pairs && (nt - 1 - t) % 2 == 1 && t + 1 < nt) ? 2 : 1;
+        int64_t pp = 0;
+        for (int j = 0; j < len; ++j) pp += pix[t + j];
+        const double eq = (double)(total - acc - pp) / (double)std::max<int64_t>(total, 1) * cum[kPipeBands];
         int k = 0;
         while (k + 1 < kPipeBands && eq >= cum[k + 1]) ++k;
-        band[t] = k;
-        acc += pix[t];
+        for (int j = 0; j < len; ++j) band[t + j] = k;
+        acc += pp;
+        t += len;
     }
     return band;
 }
@@ -550,6 +560,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         if (checked) *checked += (run - fst) * in_pass;
     };
     P.executed_a2m = 0;
+    uint64_t single_steps = 0;  // map2alm steps run by single-tile passes (SHTC_PLAN_STATS)
     for (int i = 0; i < n_m; ++i) {
         const int n = lmax - ms[i];
         P.nominal += (uint64_t)(n + 1) * ns;
@@ -567,6 +578,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         for (size_t a = 0; a < alive.size();) {
             const int nt = (kPair > 1 && a + 1 < alive.size() && tband[alive[a + 1]] == tband[alive[a]]) ? 2 : 1;
             account(i, &alive[a], nt, P.executed, &P.checked_steps, &P.fast_steps);
+            if (nt == 1) account(i, &alive[a], 1, single_steps, nullptr, nullptr);
             a += nt;
         }
         // map2alm items: up to G consecutive alive tiles of one pipeline band.  Device-
@@ -589,6 +601,10 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         slot_b[i] = slots_b;
         slots_b += (int64_t)per_m_b[i] * (n + 1);
     }
+    if (std::getenv("SHTC_PLAN_STATS"))
+        std::fprintf(stderr, "plan stats: map2alm executed %llu (single-tile passes %llu), alm2map executed %llu, useful %llu\n",
+                     (unsigned long long)P.executed, (unsigned long long)single_steps,
+                     (unsigned long long)P.executed_a2m, (unsigned long long)P.useful);
     // cost = degree steps actually run (from the pass's resume point) x tiles in the pass
     auto pass_cost = [&](int mi, int ta, int tb) {
         const int ic = tb >= 0 ? std::min(tile_start(mi, ta), tile_start(mi, tb)) : tile_start(mi, ta);
