@@ -47,6 +47,10 @@ constexpr int LEG_WARPS = 4;      // warps per block of the persistent Legendre 
 #endif
 constexpr int LEG_CL = LEG_CL_DEF;  // degree steps staged per chunk (LEG_CL / 32 entries per lane)
 static_assert(LEG_CL % 32 == 0, "whole entries per lane");
+#ifndef LEG_A2M_P
+#define LEG_A2M_P 1  // tiles an alm2map warp runs at once; 2 (8 streams per lane) measured slower at C4:
+                     // 7.0 ms at 2 CTAs/SM, 7.4 ms at 3 (spills) against 6.89 ms
+#endif
 #ifndef LEG_A2M_MINB
 #define LEG_A2M_MINB 3  // resident CTAs per SM the alm2map kernel is compiled for
 #endif
@@ -65,7 +69,7 @@ constexpr int LEG_M2A_GROUP = LEG_M2A_GROUP_DEF;  // tiles per map2alm work item
 #endif
 
 // One warp-sized unit of work of the persistent kernels.
-//   alm2map: (mi, tile id, -, -); map2alm: (mi, first index into tile_list, tile count, item
+//   alm2map: (mi, tile id, second tile id or -1, -); map2alm: (mi, first index into tile_list, tile count, item
 //   index g within the order), items of an order write partial sums into scratch slots.
 struct LegItem {
     int mi, a, b, g;

@@ -262,25 +262,27 @@ __device__ __forceinline__ int next_activation(const int (&act)[R], int i) {
 
 // Lane setup shared by both kernels: zero state, activation steps, checkpoints staged in smem;
 // seed lanes (act == 0) start from their checkpoint (0, P_mm).
-template <int R>
-__device__ __forceinline__ void lanes_setup(const LegPlanView& p, int mi, int tile, int lane,
-                                            double (&x)[R], double (&q0)[R], double (&q1)[R],
-                                            int (&act)[R], double2 (*ck)[32]) {
+// Lane k = q*R + r is stream r of tiles[q] (tiles[q] < 0: absent, its lanes stay zero).
+template <int R, int NP>
+__device__ __forceinline__ void lanes_setup(const LegPlanView& p, int mi, const int (&tiles)[NP], int lane,
+                                            double (&x)[R * NP], double (&q0)[R * NP], double (&q1)[R * NP],
+                                            int (&act)[R * NP], double2 (*ck)[32]) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-        const int s = tile * (32 * R) + r * 32 + lane;
-        x[r] = 0.0;
-        q0[r] = q1[r] = 0.0;
-        act[r] = INT_MAX;
-        if (s < p.st.n) {
+    for (int k = 0; k < R * NP; ++k) {
+        const int q = k / R, r = k % R;
+        const int s = tiles[q] * (32 * R) + r * 32 + lane;
+        x[k] = 0.0;
+        q0[k] = q1[k] = 0.0;
+        act[k] = INT_MAX;
+        if (tiles[q] >= 0 && s < p.st.n) {
             const size_t o = (size_t)mi * p.st.n + s;
-            x[r] = p.st.x[s];
-            act[r] = p.ck_act[o];
+            x[k] = p.st.x[s];
+            act[k] = p.ck_act[o];
             const double2 c = p.ck_q[o];
-            ck[r][lane] = c;
-            if (act[r] == 0) {
-                q0[r] = c.x;
-                q1[r] = c.y;
+            ck[k][lane] = c;
+            if (act[k] == 0) {
+                q0[k] = c.x;
+                q1[k] = c.y;
             }
         }
     }
@@ -329,13 +331,16 @@ __device__ __forceinline__ void a2m_step_act(A2MLane<R>& L, const Coef& cf, int 
 
 }  // namespace
 
-template <int R>
+// A warp runs the NP tiles of one work item at once (S = R x NP streams per lane: the
+// coefficient loads and the loop overhead of a step are shared by twice the streams at NP = 2).
+template <int R, int NP>
 __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
     leg_alm2map_kernel(LegPlanView p, const double2* __restrict__ alm, double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, int* __restrict__ counter) {
+    constexpr int S = R * NP;
     struct WarpSmem {
         CoefSoA cf;
-        double2 ck[R][32];
+        double2 ck[S][32];
     };
     __shared__ WarpSmem sm_all[LEG_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -346,39 +351,47 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
         const int it = warp_next_item(counter);
         if (it >= p.n_a2m_items) return;
         const LegItem item = p.a2m_items[it];
-        const int mi = item.mi, tile = item.a;
+        const int mi = item.mi;
+        int tiles[NP];
+        tiles[0] = item.a;
+        if constexpr (NP > 1) tiles[1] = item.b;
         const int m = p.ms[mi];
         const int n = p.lmax - m;
         const int64_t toff = p.tab.tab_off[mi];
         const double* __restrict__ gA = p.tab.A + toff;
         const double* __restrict__ gC = p.tab.C + toff;
         const double2* __restrict__ galm = alm + alm_offset(m, p.lmax);
-        const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tile];
-        const int is = info.x, ie = info.y;
-        const int ic = leg_tile_start(is);  // first step of the run (0: seeds)
+        int ic = INT_MAX, ie = -1;  // the run starts at the earliest tile start (0: seeds)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+            if (tiles[q] < 0) continue;
+            const int2 info = p.tile_info[(size_t)mi * p.n_tiles + tiles[q]];
+            ic = min(ic, leg_tile_start(info.x));
+            ie = max(ie, info.y);
+        }
 
-        A2MLane<R> L;
+        A2MLane<S> L;
         __syncwarp();
-        lanes_setup<R>(p, mi, tile, lane, L.x, L.q0, L.q1, L.act, ck);
+        lanes_setup<R, NP>(p, mi, tiles, lane, L.x, L.q0, L.q1, L.act, ck);
         const double2 a0 = galm[0];
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
+        for (int r = 0; r < S; ++r) {
             // degree offset 0 term: a_mm P_mm (c_0 = 1) of lanes active from the seed
             L.ae[r] = make_double2(a0.x * L.q1[r], a0.y * L.q1[r]);
             L.ao[r] = make_double2(0.0, 0.0);
         }
         __syncwarp();
-        int ev = next_activation<R>(L.act, ic - 1 + (ic == 0));  // ic == 0: seeds are set
+        int ev = next_activation<S>(L.act, ic - 1 + (ic == 0));  // ic == 0: seeds are set
         if (ic) {
             // the even step ic on its own, then (odd, even) pairs from ic + 1
             const double cc = gC[ic];
             const double2 v = galm[ic];
             const Coef c0{gA[ic], v.x * cc, v.y * cc};
             if (ic == ev) {
-                a2m_step_act<R, false>(L, c0, ic, ck, lane);
-                ev = next_activation<R>(L.act, ic);
+                a2m_step_act<S, false>(L, c0, ic, ck, lane);
+                ev = next_activation<S>(L.act, ic);
             } else {
-                a2m_step<R, false>(L, c0);
+                a2m_step<S, false>(L, c0);
             }
         }
         const int i_first = ic + 1;
@@ -423,16 +436,16 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
                 const int i = i0 + j;
                 const Coef c1 = sm.get(j), c2 = sm.get(j + 1);
                 if (i == ev) {
-                    a2m_step_act<R, true>(L, c1, i, ck, lane);
-                    ev = next_activation<R>(L.act, i);
+                    a2m_step_act<S, true>(L, c1, i, ck, lane);
+                    ev = next_activation<S>(L.act, i);
                 } else {
-                    a2m_step<R, true>(L, c1);
+                    a2m_step<S, true>(L, c1);
                 }
                 if (i + 1 == ev) {
-                    a2m_step_act<R, false>(L, c2, i + 1, ck, lane);
-                    ev = next_activation<R>(L.act, i + 1);
+                    a2m_step_act<S, false>(L, c2, i + 1, ck, lane);
+                    ev = next_activation<S>(L.act, i + 1);
                 } else {
-                    a2m_step<R, false>(L, c2);
+                    a2m_step<S, false>(L, c2);
                 }
             }
             // after the last activation: groups of 8 steps, coefficients loaded up front
@@ -448,30 +461,32 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
                 }
 #pragma unroll
                 for (int u = 0; u < LEG_A2M_G; u += 2) {
-                    a2m_step<R, true>(L, cg[u]);
-                    a2m_step<R, false>(L, cg[u + 1]);
+                    a2m_step<S, true>(L, cg[u]);
+                    a2m_step<S, false>(L, cg[u + 1]);
                 }
             }
             for (; j + 1 < cnt; j += 2) {
-                a2m_step<R, true>(L, sm.get(j));
-                a2m_step<R, false>(L, sm.get(j + 1));
+                a2m_step<S, true>(L, sm.get(j));
+                a2m_step<S, false>(L, sm.get(j + 1));
             }
             if (j < cnt) {  // trailing odd step (last chunk only)
                 const int i = i0 + j;
                 if (i == ev) {
-                    a2m_step_act<R, true>(L, sm.get(j), i, ck, lane);
-                    ev = next_activation<R>(L.act, i);
+                    a2m_step_act<S, true>(L, sm.get(j), i, ck, lane);
+                    ev = next_activation<S>(L.act, i);
                 } else {
-                    a2m_step<R, true>(L, sm.get(j));
+                    a2m_step<S, true>(L, sm.get(j));
                 }
             }
         }
 
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int s = tile * (32 * R) + r * 32 + lane;
+        for (int k = 0; k < S; ++k) {
+            const int q = k / R, r = k % R;
+            if (tiles[q] < 0) continue;
+            const int s = tiles[q] * (32 * R) + r * 32 + lane;
             if (s >= p.st.n) continue;
-            const double2 e = L.ae[r], o = L.ao[r];  // dead lanes stayed zero
+            const double2 e = L.ae[k], o = L.ao[k];  // dead lanes stayed zero
             const int north = p.st.north[s], south = p.st.south[s];
             *leg_out(p, delta, row_off, north, mi) = cadd(e, o);
             if (south >= 0) *leg_out(p, delta, row_off, south, mi) = csub(e, o);
@@ -498,7 +513,7 @@ int leg_persistent_blocks(int device) {
     if (device >= 0 && device < 64 && cached[device]) return cached[device];
     int sms = 148, per = 1;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_alm2map_kernel<LEG_R>, LEG_WARPS * 32, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, leg_alm2map_kernel<LEG_R, LEG_A2M_P>, LEG_WARPS * 32, 0);
     const int v = sms * (per > 0 ? per : 1);
     if (device >= 0 && device < 64) cached[device] = v;
     return v;
@@ -519,7 +534,7 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
     const int need = (p.n_a2m_items + LEG_WARPS - 1) / LEG_WARPS;
     if (need < blocks) blocks = need;
     if (!(phases & LEG_PHASE_NO_RESET)) cudaMemsetAsync(counters, 0, sizeof(int), s);
-    leg_alm2map_kernel<LEG_R><<<blocks, LEG_WARPS * 32, 0, s>>>(p, alm, delta, row_off, counters);
+    leg_alm2map_kernel<LEG_R, LEG_A2M_P><<<blocks, LEG_WARPS * 32, 0, s>>>(p, alm, delta, row_off, counters);
     count_launch();
 }
 

@@ -570,9 +570,13 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
             if (info[(size_t)i * v.n_tiles + t].x >= 0) alive.push_back(t);
         tl.insert(tl.end(), alive.begin(), alive.end());
         tcnt[i] = (int)alive.size();
-        for (int t : alive) {  // alm2map: one tile per item
-            a2m.push_back(LegItem{i, t, -1, 0});
-            account(i, &t, 1, P.executed_a2m, nullptr, nullptr);
+        // alm2map items: consecutive alive tiles of one band in pairs (LEG_A2M_P), one tile
+        // when the pair would cross a band
+        for (size_t a = 0; a < alive.size();) {
+            const int nt = (LEG_A2M_P > 1 && a + 1 < alive.size() && tband[alive[a + 1]] == tband[alive[a]]) ? 2 : 1;
+            a2m.push_back(LegItem{i, alive[a], nt > 1 ? alive[a + 1] : -1, 0});
+            account(i, &alive[a], nt, P.executed_a2m, nullptr, nullptr);
+            a += nt;
         }
         // map2alm passes: consecutive alive tiles of one band in pairs (kPair)
         for (size_t a = 0; a < alive.size();) {
@@ -610,7 +614,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         const int ic = tb >= 0 ? std::min(tile_start(mi, ta), tile_start(mi, tb)) : tile_start(mi, ta);
         return (int64_t)(lmax - ms[mi] + 1 - ic) * (tb >= 0 ? 2 : 1);
     };
-    auto a2m_cost = [&](const LegItem& it) { return pass_cost(it.mi, it.a, -1); };
+    auto a2m_cost = [&](const LegItem& it) { return pass_cost(it.mi, it.a, it.b); };
     auto m2a_cost = [&](const LegItem& it) {
         int64_t c = 0;
         int k = 0;
@@ -887,8 +891,15 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
             else iv.push_back({b0, b1});
         }
         for (int cls = 0; cls < FFT_N_CLASSES; ++cls) {
+            // band, then ring length: rings that share their tables (hw, chirp, FFT(h) are one
+            // per length -- the north and south rings of a mirror pair) sit next to each other
+            // in the queue, so the second read of a table is an L2 hit instead of a second HBM
+            // read half a launch later
             std::stable_sort(per_class[cls].begin(), per_class[cls].end(),
-                             [&](const RingDesc& a, const RingDesc& b) { return band(a) < band(b); });
+                             [&](const RingDesc& a, const RingDesc& b) {
+                                 if (band(a) != band(b)) return band(a) < band(b);
+                                 return a.n < b.n;
+                             });
             F.descs[cls].upload(per_class[cls], s);
             F.range_start[cls].assign(kPipeBands + 1, 0);
             for (const RingDesc& d : per_class[cls]) F.range_start[cls][band(d) + 1]++;
