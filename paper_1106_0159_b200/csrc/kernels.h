@@ -160,6 +160,7 @@ struct RingDesc {
     int64_t hw_off;     // e^{-2 pi i k / n}, k <= N (half mode)
     int64_t chirp_off;  // Bluestein chirp e^{-i pi (j^2 mod 2N)/N}, j < N
     int64_t h_off;      // Bluestein FFT_B of conj(chirp) (cyclic), B entries
+    int64_t ph_off;     // e^{i m phi0}: m < 64, then m = 64 j (j <= mmax / 64); phi0 != 0 only
     double phi0;
     double weight;
     int n;              // samples on the ring
@@ -214,7 +215,9 @@ void launch_ring_analysis(int cls, const RingStageArgs& a, cudaStream_t s);
 struct TableJob {
     int64_t off;
     int L;     // length parameter
-    int kind;  // 0: e^{-2 pi i k/L}, k<L ; 1: e^{-2 pi i k/L}, k<=L/2 ; 2: chirp, k<L
+    int kind;  // 0: e^{-2 pi i k/L}, k<L ; 1: e^{-2 pi i k/L}, k<=L/2 ; 2: chirp, k<L ;
+               // 3: phase factors of phi0, k < L = 64 + mmax/64 + 1
+    double phi0;
 };
 void launch_fill_tables(const TableJob* jobs_dev, int n_jobs, double2* tabs, cudaStream_t s);
 // For each Bluestein ring descriptor (deduplicated by N): tabs[h_off..] = FFT_B(h).

@@ -263,17 +263,11 @@ struct PhaseTab {
     __device__ __forceinline__ double2 at(int m) const { return cmul(lo[m & 63], hi[m >> 6]); }
 };
 
-__device__ __forceinline__ void build_phase(double2* lo, double2* hi, int nhi, double phi0, int T) {
-    for (int j = threadIdx.x; j < 64 + nhi; j += T) {
-        double s, c;
-        if (j < 64) {
-            sincos((double)j * phi0, &s, &c);
-            lo[j] = make_double2(c, s);
-        } else {
-            sincos((double)((j - 64) * 64) * phi0, &s, &c);
-            hi[j - 64] = make_double2(c, s);
-        }
-    }
+// The ring's phase factors (lo then hi, built at plan time by fill_tables_kernel kind 3 with the
+// same sincos arguments, one table per distinct phi0) copied to shared memory: one load per
+// thread instead of 64 + (mmax+1)/64 sincos evaluations per ring.
+__device__ __forceinline__ void load_phase(double2* dst, const double2* __restrict__ src, int cnt, int T) {
+    for (int j = threadIdx.x; j < cnt; j += T) dst[j] = __ldg(src + j);
 }
 
 __device__ __forceinline__ int64_t delta_index(const RingStageArgs& a, int pos, int m) {
@@ -521,6 +515,7 @@ __device__ __forceinline__ void p2_prefetch_ring(const RingStageArgs& a, int ri)
         l2_prefetch<T>(a.map_in + d.pix_off, (int64_t)d.n * 8);
     }
     l2_prefetch<T>(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);
+    if (d.phi0 != 0.0) l2_prefetch<T>(a.tabs + d.ph_off, (int64_t)(64 + (a.mmax >> 6) + 1) * 16);
     if (d.flags & 2) {
         l2_prefetch<T>(a.tabs + d.chirp_off, (int64_t)d.N * 16);
         l2_prefetch<T>(a.tabs + d.h_off, (int64_t)M * 16);
@@ -589,7 +584,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             const double phi0 = d.phi0;
             const bool rot = phi0 != 0.0;
             if (rot) {
-                build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
                 __syncthreads();
             }
             P2T(0);
@@ -802,7 +797,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
             const RingDesc& d = desc_at(a, ri);
             const int N = d.N;
             const double phi0 = d.phi0;
-            if (phi0 != 0.0) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);  // published by later barriers
+            if (phi0 != 0.0) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);  // published by later barriers
             const int64_t po = d.pix_off;
             const double* __restrict__ in = a.map_in + po;
             if ((po & 1) == 0) {
@@ -952,7 +947,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
             if (SYN) {
                 if (rot) {
-                    build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                    load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
                     __syncthreads();
                 }
                 // fold: H_k for 0 <= k <= N (n = 2N > mmax here: no wraps)
@@ -993,7 +988,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                 }
                 __syncthreads();  // H read before the first pass overwrites buf
             } else {
-                if (h == 0 && rot) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+                if (h == 0 && rot) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
                 const int64_t po = d.pix_off;
                 const double* __restrict__ in = a.map_in + po;
 #pragma unroll
@@ -1143,7 +1138,7 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_synth_kern
     const bool rot = phi0 != 0.0;
     const PhaseTab ph{phlo, phlo + 64};
     if (rot) {
-        build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);
+        load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
         __syncthreads();
     }
 
@@ -1213,7 +1208,7 @@ __global__ void __launch_bounds__(T, (T >= 1024 ? 1 : 1024 / T)) ring_anal_kerne
     const PhaseTab ph{phlo, phlo + 64};
     const double* __restrict__ in = a.map_in + d.pix_off;
     const int t = threadIdx.x;
-    if (rot) build_phase(phlo, phlo + 64, (mmax >> 6) + 1, phi0, T);  // ordered by later barriers
+    if (rot) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);  // ordered by later barriers
 
     if (half) {
         for (int j = t; j < N; j += T) buf[j] = make_double2(in[2 * j], in[2 * j + 1]);
@@ -1277,6 +1272,11 @@ __global__ void fill_tables_kernel(const TableJob* __restrict__ jobs, double2* _
     const int count = jb.kind == 1 ? jb.L / 2 + 1 : jb.L;
     for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < count; k += gridDim.x * blockDim.x) {
         double s, c;
+        if (jb.kind == 3) {  // phase factors e^{i m phi0}: lo (m < 64), then hi (m = 64 (k - 64))
+            sincos((double)(k < 64 ? k : (k - 64) * 64) * jb.phi0, &s, &c);
+            tabs[jb.off + k] = make_double2(c, s);
+            continue;
+        }
         if (jb.kind == 2) {
             const long long e = ((long long)k * k) % (2LL * jb.L);
             sincospi((double)e / (double)jb.L, &s, &c);  // e^{-i pi e / L}

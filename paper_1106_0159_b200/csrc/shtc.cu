@@ -196,6 +196,7 @@ int fft_aux_count() {
 
 struct FftPlan {
     bool built = false;
+    int mmax = -1;  // the phase-factor tables cover orders 0..mmax
     DevBuf descs[FFT_N_CLASSES];
     int count[FFT_N_CLASSES] = {};
     // latitude bands of the pipelined paths: class c's descriptors of band k are
@@ -605,10 +606,40 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         slot_b[i] = slots_b;
         slots_b += (int64_t)per_m_b[i] * (n + 1);
     }
-    if (std::getenv("SHTC_PLAN_STATS"))
+    if (std::getenv("SHTC_PLAN_STATS")) {
+        // activation events of the map2alm passes: distinct activation steps inside each
+        // pass's checked window (ic, ie], and the window lengths
+        std::vector<int> acts((size_t)n_m * ns);
+        CK(cudaMemcpy(acts.data(), P.ck_act.p, acts.size() * sizeof(int), cudaMemcpyDeviceToHost));
+        uint64_t events = 0, window = 0, passes = 0;
+        for (int i = 0; i < n_m; ++i) {
+            std::vector<int> alive;
+            for (int t = v.n_tiles - 1; t >= 0; --t)
+                if (info[(size_t)i * v.n_tiles + t].x >= 0) alive.push_back(t);
+            for (size_t a = 0; a < alive.size();) {
+                const int nt = (kPair > 1 && a + 1 < alive.size() && tband[alive[a + 1]] == tband[alive[a]]) ? 2 : 1;
+                int ic = INT_MAX, ie = -1;
+                std::vector<int> ev;
+                for (int k = 0; k < nt; ++k) {
+                    const int t = alive[a + k];
+                    ic = std::min(ic, tile_start(i, t));
+                    ie = std::max(ie, info[(size_t)i * v.n_tiles + t].y);
+                    for (int j = 0; j < LEG_TILE && t * LEG_TILE + j < ns; ++j) ev.push_back(acts[(size_t)i * ns + t * LEG_TILE + j]);
+                }
+                std::sort(ev.begin(), ev.end());
+                ev.erase(std::unique(ev.begin(), ev.end()), ev.end());
+                for (int e : ev) events += (e > ic && e != INT_MAX);
+                window += (uint64_t)std::max(0, ie - ic);
+                ++passes;
+                a += nt;
+            }
+        }
+        std::fprintf(stderr, "plan stats: map2alm passes %llu, checked-window steps %llu, activation events %llu\n",
+                     (unsigned long long)passes, (unsigned long long)window, (unsigned long long)events);
         std::fprintf(stderr, "plan stats: map2alm executed %llu (single-tile passes %llu), alm2map executed %llu, useful %llu\n",
                      (unsigned long long)P.executed, (unsigned long long)single_steps,
                      (unsigned long long)P.executed_a2m, (unsigned long long)P.useful);
+    }
     // cost = degree steps actually run (from the pass's resume point) x tiles in the pass
     auto pass_cost = [&](int mi, int ta, int tb) {
         const int ic = tb >= 0 ? std::min(tile_start(mi, ta), tile_start(mi, tb)) : tile_start(mi, ta);
@@ -790,10 +821,23 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         if (it != table_at.end()) return it->second;
         const int64_t off = tot;
         tot += (kind == 1) ? L / 2 + 1 : L;
-        jobs.push_back(TableJob{off, L, kind});
+        jobs.push_back(TableJob{off, L, kind, 0.0});
         table_at[key] = off;
         return off;
     };
+    // phase factor tables, one per distinct phi0 (the mirror rings of a pair share theirs)
+    std::map<double, int64_t> phase_at;
+    const int n_phase = 64 + (c->mmax >> 6) + 1;
+    auto phase_table = [&](double phi0) {
+        auto it = phase_at.find(phi0);
+        if (it != phase_at.end()) return it->second;
+        const int64_t off = tot;
+        tot += n_phase;
+        jobs.push_back(TableJob{off, n_phase, 3, phi0});
+        phase_at[phi0] = off;
+        return off;
+    };
+    F.mmax = c->mmax;
     std::map<int, int64_t> h_at;  // Bluestein N -> H offset
     std::vector<RingDesc> per_class[FFT_N_CLASSES];
     std::vector<RingDesc> blue_class[FFT_N_CLASSES];
@@ -812,6 +856,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         d.flags = (half ? 1 : 0) | (smooth ? 0 : 2);
         d.pix_off = c->pixoff[r];
         d.phi0 = c->phi0[r];
+        d.ph_off = d.phi0 != 0.0 ? phase_table(d.phi0) : 0;
         d.weight = c->weight[r];
         d.ring_pos = (int)pos;
         // half-mode rings with a power-of-two buffer (direct or Bluestein) run the register
@@ -1212,6 +1257,7 @@ shtc_status shtc_set_band(shtc_ctx* ctx, int lmax, int mmax, int n_m, const int3
         for (int m = 0; m <= mmax; ++m) ctx->log_mu[m] = host_log_mu(m);
         ctx->band_set = true;
         ctx->leg.built = false;
+        if (ctx->fft_id.mmax != mmax) ctx->fft_id.built = false;  // phase tables sized by mmax
         ctx->id_row_off.release();
         ctx->custom_layout = false;
         ctx->syn_layout = false;
