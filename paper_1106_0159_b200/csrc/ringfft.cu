@@ -619,6 +619,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 // issue back to back
 #pragma unroll
                 for (int j0 = 0; j0 < E; j0 += G) {
+                    if (T * j0 > N) break;  // Bluestein padding: no element of the batch is <= N
                     constexpr int GX = G + 1;
                     double2 x1[GX], x2[GX];
 #pragma unroll
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 // aliasing rings: wraps outer (two per iteration), G elements' loads together
 #pragma unroll
                 for (int j0 = 0; j0 < E; j0 += G) {
+                    if (T * j0 > N) break;  // Bluestein padding
                     constexpr int GX = G + 1;
                     double2 h[GX];
                     int kk[GX];
@@ -733,6 +735,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
 #pragma unroll
             for (int j = 0; j < E; ++j) {
                 const int k = t + T * j;
+                if (T * j >= N) continue;  // padding: not stored
                 const double2 c = __ldg(&chirp[k < N ? k : 0]);
                 v[j] = cscale(cmul(v[j], cconj(c)), inv);  // k >= N: not stored
             }
