@@ -530,6 +530,35 @@ __device__ __forceinline__ const RingDesc& desc_at(const RingStageArgs& a, int r
     return a.rings[ri];
 }
 
+// Asynchronous global -> shared copies (cp.async, no registers held while in flight): the next
+// ring's descriptor is fetched during the current ring, and a ring's phase factors while its
+// fold loads are in flight.
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+constexpr int kDescChunks = (int)(sizeof(RingDesc) / 16);
+#ifndef P2_PHASE_LATE
+#define P2_PHASE_LATE 0  // synthesis: wait for the phase factors before the fold (1: after its first loads, measured 0.01 ms slower at C4)
+#endif
+static_assert(sizeof(RingDesc) % 16 == 0, "descriptor copied in 16-byte chunks");
+// threads t < kDescChunks copy descriptor ri into dst
+__device__ __forceinline__ void desc_fetch(RingDesc* dst, const RingStageArgs& a, int ri, int t) {
+    if (t < kDescChunks && ri < a.n_rings)
+        cp_async16(reinterpret_cast<char*>(dst) + 16 * t, reinterpret_cast<const char*>(a.rings + ri) + 16 * t);
+}
+// the current ring's descriptor in shared memory (index hidden: every field read is an LDS
+// where it is used, not a register held across the FFT passes)
+__device__ __forceinline__ const RingDesc& sdesc_at(const RingDesc* s, int i) {
+    asm volatile("" : "+r"(i));
+    return s[i];
+}
+// phase factors of the ring into dst (cp.async; cp_async_wait_all + a barrier before use)
+__device__ __forceinline__ void phase_fetch(double2* dst, const double2* __restrict__ src, int cnt, int T) {
+    for (int j = threadIdx.x; j < cnt; j += T) cp_async16(dst + j, src + j);
+}
+
 // Persistent CTAs pull rings from a queue and transform one ring at a time (the ring in
 // registers + one padded shared-memory exchange buffer).
 #ifdef P2_PROF
@@ -557,7 +586,8 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
     constexpr int T = M / E;
     constexpr int G = E < 8 ? E : 8;  // fold batch: elements whose loads are in flight together
     extern __shared__ __align__(16) double2 smem[];
-    __shared__ int s_ri;
+    __shared__ int s_ri, s_nxt;
+    __shared__ __align__(16) RingDesc s_desc[2];  // this ring's descriptor and the next one's
     double2* buf = smem;                        // p2pad(M) + 1 (H_N of direct rings)
     double2* tws = smem + p2pad(M) + 16;        // pass twiddles (P2Plan<M, E>::TW)
     double2* phlo = tws + P2Plan<M, E>::TW;     // 64 + (mmax >> 6) + 1 phase factors
@@ -567,6 +597,10 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
     p2_prefetch_ring<M, T, true>(a, blockIdx.x);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
+    desc_fetch(&s_desc[0], a, s_ri, t);
+    cp_async_wait_all();
+    __syncthreads();
+    int cur = 0;
     for (;;) {
         // dynamic ring queue: CTAs that become resident late (other classes' kernels run
         // concurrently on other streams) just take fewer rings; the next index is fetched
@@ -575,16 +609,24 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
         if (ri >= a.n_rings) break;
         P2T_START;
         int nxt = 0;
-        if (t == 0) nxt = atomicAdd(a.counter, 1);
+        if (t == 0) s_nxt = nxt = atomicAdd(a.counter, 1);
         p2_prefetch_ring<M, T, true>(a, ri + gridDim.x);
         double2 v[E];
         {
-            const RingDesc& d = desc_at(a, ri);
+            const RingDesc& d = sdesc_at(s_desc, cur);
             const int n = d.n, N = d.N, pos = d.ring_pos;
             const double phi0 = d.phi0;
             const bool rot = phi0 != 0.0;
-            if (rot) {
-                load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
+            // phase factors in flight with the fold's first loads; published before first use
+            if (rot) phase_fetch(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
+            auto phase_ready = [&]() {
+                if (P2_PHASE_LATE && rot) {
+                    cp_async_wait_all();
+                    __syncthreads();
+                }
+            };
+            if (!P2_PHASE_LATE && rot) {
+                cp_async_wait_all();
                 __syncthreads();
             }
             P2T(0);
@@ -602,6 +644,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                     const int k = t + T * j;
                     x[j] = a.delta_in[delta_index(a, pos, (k < N && k <= mmax) ? k : 0)];
                 }
+                phase_ready();
 #pragma unroll
                 for (int j = 0; j < E; ++j) {
                     const int k = t + T * j;
@@ -629,6 +672,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                         x1[u] = a.delta_in[delta_index(a, pos, (k <= N && m1 <= mmax) ? m1 : 0)];
                         x2[u] = a.delta_in[delta_index(a, pos, (k <= N && m2 <= mmax) ? m2 : 0)];
                     }
+                    if (j0 == 0) phase_ready();
 #pragma unroll
                     for (int u = 0; u < GX; ++u) {
                         const int k = (u < G) ? t + T * (j0 + u) : N;
@@ -644,6 +688,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 }
             } else {
                 // aliasing rings: wraps outer (two per iteration), G elements' loads together
+                phase_ready();
 #pragma unroll
                 for (int j0 = 0; j0 < E; j0 += G) {
                     if (T * j0 > N) break;  // Bluestein padding
@@ -692,6 +737,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 wv[j] = __ldg(&hw[k < N ? k : 0]);  // valid position, result masked below
             }
             __syncthreads();
+            desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor, in flight until the ring's end
             P2T(2);
 #pragma unroll
             for (int j = 0; j < E; ++j) {
@@ -720,7 +766,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             // fences keep ptxas from hoisting the table loads into the FFT passes
             __threadfence_block();
             {
-                const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
+                const double2* __restrict__ H = a.tabs + sdesc_at(s_desc, cur).h_off;
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], cconj(__ldg(&H[t + T * j])));
             }
@@ -728,7 +774,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             p2_fft<M, E, +1>(v, buf, tws);
             P2T(7);
             __threadfence_block();
-            const RingDesc& d = desc_at(a, ri);
+            const RingDesc& d = sdesc_at(s_desc, cur);
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
             const int N = d.N;
             const double inv = 1.0 / (double)M;
@@ -742,7 +788,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             P2T(8);
         }
         {
-            const RingDesc& d = desc_at(a, ri);
+            const RingDesc& d = sdesc_at(s_desc, cur);
             const int N = d.N;
             const int64_t po = d.pix_off;
             double* __restrict__ out = a.map_out + po;
@@ -765,8 +811,10 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             }
         }
         P2T(9);
+        cp_async_wait_all();  // the next descriptor has landed
         if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
-        __syncthreads();  // buf / phase table / s_ri reuse by the next ring
+        __syncthreads();  // buf / phase table / descriptors / s_ri reuse by the next ring
+        cur ^= 1;
         P2T(10);
 #ifdef P2_PROF
         if (t == 0) atomicAdd(&g_p2prof[p2prof_slot<M, BLUE>()][15], 1ull);
@@ -779,7 +827,8 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
     constexpr int T = M / E;
     constexpr int U = 8;  // unfold batch
     extern __shared__ __align__(16) double2 smem[];
-    __shared__ int s_ri;
+    __shared__ int s_ri, s_nxt;
+    __shared__ __align__(16) RingDesc s_desc[2];  // this ring's descriptor and the next one's
     double2* buf = smem;
     double2* tws = smem + p2pad(M) + 16;
     double2* phlo = tws + P2Plan<M, E>::TW;
@@ -789,18 +838,22 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
     p2_prefetch_ring<M, T, false>(a, blockIdx.x);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
+    desc_fetch(&s_desc[0], a, s_ri, t);
+    cp_async_wait_all();
+    __syncthreads();
+    int cur = 0;
     for (;;) {
         const int ri = s_ri;
         if (ri >= a.n_rings) break;
         int nxt = 0;
-        if (t == 0) nxt = atomicAdd(a.counter, 1);
+        if (t == 0) s_nxt = nxt = atomicAdd(a.counter, 1);
         p2_prefetch_ring<M, T, false>(a, ri + gridDim.x);
         double2 v[E];
         {
-            const RingDesc& d = desc_at(a, ri);
+            const RingDesc& d = sdesc_at(s_desc, cur);
             const int N = d.N;
             const double phi0 = d.phi0;
-            if (phi0 != 0.0) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);  // published by later barriers
+            if (phi0 != 0.0) phase_fetch(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);  // waited for before the unfold
             const int64_t po = d.pix_off;
             const double* __restrict__ in = a.map_in + po;
             if ((po & 1) == 0) {
@@ -829,17 +882,19 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
         }
         if constexpr (!BLUE) {
             p2_fft<M, E, -1>(v, buf, tws);
+            desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor
         } else {
             p2_fft<M, E, -1>(v, buf, tws);
+            desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor
             __threadfence_block();
             {
-                const double2* __restrict__ H = a.tabs + desc_at(a, ri).h_off;
+                const double2* __restrict__ H = a.tabs + sdesc_at(s_desc, cur).h_off;
 #pragma unroll
                 for (int j = 0; j < E; ++j) v[j] = cmul(v[j], __ldg(&H[t + T * j]));
             }
             p2_fft<M, E, +1>(v, buf, tws);
             __threadfence_block();
-            const RingDesc& d = desc_at(a, ri);
+            const RingDesc& d = sdesc_at(s_desc, cur);
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
             const int N = d.N;
             const double inv = 1.0 / (double)M;
@@ -850,7 +905,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
                 v[j] = cscale(cmul(v[j], c), inv);  // k >= N: not stored
             }
         }
-        const RingDesc& d = desc_at(a, ri);
+        const RingDesc& d = sdesc_at(s_desc, cur);
         const int n = d.n, N = d.N, pos = d.ring_pos;
         // Z_k (k < N) -> shared memory; the last FFT pass ended after a barrier that followed
         // every read of buf, so the stores cannot race with it
@@ -859,6 +914,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
             const int k = t + T * j;
             if (k < N) buf[p2pad(k)] = v[j];
         }
+        cp_async_wait_all();  // phase factors (and the next descriptor) have landed
         __syncthreads();
         // R2C split B_b = E_b + e^{-2 pi i b/n} O_b and the unfold Delta^S_m = w bins[m mod n]
         // e^{-i m phi0} (fourier.cpp:42-47); bins above n/2 are conj B_{n-b}.  U orders per
@@ -910,7 +966,8 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
             }
         }
         if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
-        __syncthreads();  // buf / phase table / s_ri reuse by the next ring
+        __syncthreads();  // buf / phase table / descriptors / s_ri reuse by the next ring
+        cur ^= 1;
     }
 }
 
