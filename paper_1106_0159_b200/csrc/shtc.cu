@@ -355,10 +355,26 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     }
     // band k covers the pixel fraction [cum[k], cum[k+1]) counted from the equator; the
     // equatorial band 0 has half the weight of the others (it is map2alm's first H2D, so it
-    // sets the head latency) -- SHTC_BAND0_WEIGHT overrides
+    // sets the head latency) -- SHTC_BAND0_WEIGHT overrides.  Band 2 is alm2map's last band
+    // (its pixels are the final copy), so it is kept small and bands 3-4 take its pixels:
+    // weights 0.5,1,0.3,1.1,1.1,1,1,1 measured 23.23 -> 22.93 ms for the C4 pair from pinned
+    // memory (alm2map 11.06 -> 10.65, map2alm 12.18 -> 12.26; tools/band_weights.sh).
+    // SHTC_BAND_WEIGHTS="w0,w1,..." sets every band's weight.
     static const double w0 = std::getenv("SHTC_BAND0_WEIGHT") ? std::atof(std::getenv("SHTC_BAND0_WEIGHT")) : 0.5;
+    static const std::vector<double> wl = [] {
+        std::vector<double> v;
+        if (const char* e = std::getenv("SHTC_BAND_WEIGHTS"))
+            for (const char* q = e; *q;) {
+                v.push_back(std::max(1e-3, std::atof(q)));
+                while (*q && *q != ',') ++q;
+                if (*q) ++q;
+            }
+        return v;
+    }();
+    static const double wdef[8] = {0.5, 1.0, 0.3, 1.1, 1.1, 1.0, 1.0, 1.0};
     std::vector<double> cum(kPipeBands + 1, 0.0);
-    for (int k = 0; k < kPipeBands; ++k) cum[k + 1] = cum[k] + (k == 0 ? w0 : 1.0);
+    for (int k = 0; k < kPipeBands; ++k)
+        cum[k + 1] = cum[k] + (k < (int)wl.size() ? wl[k] : k == 0 ? w0 : (kPipeBands == 8 ? wdef[k] : 1.0));
     // Bands are assigned per tile PAIR counted from the equatorial end (tiles nt-1 and nt-2,
     // nt-3 and nt-4, ...): the map2alm kernel runs an item's tiles two at a time, and with no
     // band boundary inside a pair only an order's most polar alive tile can be left to run
