@@ -967,7 +967,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
             for (int k = 0; k < kPipeBands; ++k) F.range_start[cls][k + 1] += F.range_start[cls][k];
         }
     }
-    F.counters.ensure(FFT_N_CLASSES * sizeof(int));  // no allocation on the transform path
+    F.counters.ensure((size_t)(kPipeBands + 1) * FFT_N_CLASSES * sizeof(int));  // no allocation on the transform path
     CK(cudaEventRecord(e1, s));
     CK(cudaStreamSynchronize(s));
     float el = 0.f;
@@ -1022,8 +1022,11 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         CK(cudaEventCreateWithFlags(&c->fft_fork, cudaEventDisableTiming));
         for (auto& e : c->fft_join) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     }
-    if (!F.counters.p) F.counters.ensure(FFT_N_CLASSES * sizeof(int));
-    CK(cudaMemsetAsync(F.counters.p, 0, FFT_N_CLASSES * sizeof(int), s));
+    // one counter slice per band (slice 0: whole-plan stages), so ring stages of different
+    // bands may run concurrently on different streams
+    F.counters.ensure((size_t)(kPipeBands + 1) * FFT_N_CLASSES * sizeof(int));
+    int* const ctr = F.counters.as<int>() + (range < 0 ? 0 : range + 1) * FFT_N_CLASSES;
+    CK(cudaMemsetAsync(ctr, 0, FFT_N_CLASSES * sizeof(int), s));
     CK(cudaEventRecord(c->fft_fork, s));
     bool used[kFftAux] = {};
     int side = 0;
@@ -1045,7 +1048,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         a.tabs = F.tabs.as<double2>();
         a.mmax = c->mmax;
         a.ld = c->mmax + 1;
-        a.counter = F.counters.as<int>() + k;
+        a.counter = ctr + k;
         a.p2_tw = a.tabs + F.tw_off[k];
         launch(k, a, st);
         CK(cudaGetLastError());
