@@ -4,11 +4,15 @@
 
 #include <cuda_runtime.h>
 
+#include <immintrin.h>
+
 #include <algorithm>
+#include <cstdint>
 #include <condition_variable>
 #include <cstring>
 #include <functional>
 #include <mutex>
+#include <cstdlib>
 #include <thread>
 #include <vector>
 
@@ -74,7 +78,8 @@ public:
 
 private:
     CopyPool() {
-        const unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        unsigned hw = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+        if (const char* e = std::getenv("SHTC_COPY_THREADS")) hw = std::max(1, std::atoi(e));
         for (unsigned i = 1; i < hw; ++i) workers_.emplace_back([this] { loop(); });
     }
     void loop() {
@@ -103,18 +108,51 @@ private:
 };
 
 // memcpy on all host cores (pageable <-> staging copies are bound by host memory bandwidth)
+// Large copies with non-temporal (streaming) AVX2 stores: the destination lines are not read
+// for ownership first, which cuts the host memory traffic of a staging copy by a third.
+__attribute__((target("avx2"))) inline void nt_memcpy(void* dst, const void* src, size_t n) {
+    char* d = static_cast<char*>(dst);
+    const char* s = static_cast<const char*>(src);
+    size_t i = 0;
+    while (i < n && (reinterpret_cast<uintptr_t>(d + i) & 31)) {
+        d[i] = s[i];
+        ++i;
+    }
+    for (; i + 128 <= n; i += 128) {
+        const __m256d a = _mm256_loadu_pd(reinterpret_cast<const double*>(s + i));
+        const __m256d b = _mm256_loadu_pd(reinterpret_cast<const double*>(s + i + 32));
+        const __m256d c = _mm256_loadu_pd(reinterpret_cast<const double*>(s + i + 64));
+        const __m256d e = _mm256_loadu_pd(reinterpret_cast<const double*>(s + i + 96));
+        _mm256_stream_pd(reinterpret_cast<double*>(d + i), a);
+        _mm256_stream_pd(reinterpret_cast<double*>(d + i + 32), b);
+        _mm256_stream_pd(reinterpret_cast<double*>(d + i + 64), c);
+        _mm256_stream_pd(reinterpret_cast<double*>(d + i + 96), e);
+    }
+    _mm_sfence();
+    if (i < n) std::memcpy(d + i, s + i, n - i);
+}
+
+inline void piece_copy(void* dst, const void* src, size_t bytes) {
+    static const bool nt = [] {
+        const char* e = std::getenv("SHTC_COPY_NT");
+        return (e ? std::atoi(e) != 0 : true) && __builtin_cpu_supports("avx2");
+    }();
+    if (nt && bytes >= (size_t(1) << 16)) nt_memcpy(dst, src, bytes);
+    else std::memcpy(dst, src, bytes);
+}
+
 inline void par_memcpy(void* dst, const void* src, size_t bytes) {
     CopyPool& pool = CopyPool::get();
     const size_t min_piece = size_t(2) << 20;
     const unsigned nt = (unsigned)std::max<size_t>(1, std::min<size_t>(pool.size(), bytes / min_piece));
     if (nt <= 1) {
-        std::memcpy(dst, src, bytes);
+        piece_copy(dst, src, bytes);
         return;
     }
     const size_t piece = (bytes / nt + 63) & ~size_t(63);
     pool.run(nt, [&](unsigned i) {
         const size_t b = std::min(bytes, piece * i), e = i + 1 == nt ? bytes : std::min(bytes, piece * (i + 1));
-        if (e > b) std::memcpy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
+        if (e > b) piece_copy(static_cast<char*>(dst) + b, static_cast<const char*>(src) + b, e - b);
     });
 }
 
