@@ -189,6 +189,11 @@ shtc_status shtc_peer_barrier(shtc_ctx* ctx, int rank, int n_workers, const uint
  * context stream; page-locked host memory for overlap. */
 shtc_status shtc_copy_orders(shtc_ctx* ctx, const double* src, double* dst, int to_device);
 
+/* Page-locked host memory (cudaHostAlloc, portable): buffers the copy engines read and write
+ * directly, e.g. the C++ drop-in's result buffers.  shtc_host_free(NULL) is a no-op. */
+shtc_status shtc_host_alloc(size_t bytes, void** out);
+void shtc_host_free(void* p);
+
 /* ---- single-process multi-GPU group -------------------------------------------------- */
 /* distributed_synthesis / distributed_analysis (distribution.cpp:300-490; distribution.hpp:
  * 70-77) as one process driving W device contexts, worker i on device_ids[i] (NULL: device

@@ -24,7 +24,7 @@ EXPORTED = [
     "shtc_ring_analysis_dev", "shtc_delta_a", "shtc_accumulate_alm", "shtc_device_info",
     "shtc_measure_fp64_peak", "shtc_dev_alloc", "shtc_dev_free", "shtc_ipc_handle", "shtc_ipc_open",
     "shtc_ipc_close", "shtc_set_exchange_peers", "shtc_legendre_alm2map_peer", "shtc_ring_analysis_peer",
-    "shtc_peer_barrier", "shtc_kernel_launches", "shtc_copy_orders",
+    "shtc_peer_barrier", "shtc_kernel_launches", "shtc_copy_orders", "shtc_host_alloc", "shtc_host_free",
     "shtc_group_create", "shtc_group_destroy", "shtc_group_last_error", "shtc_group_device",
     "shtc_group_set_grid", "shtc_group_set_layout", "shtc_group_plan_ms", "shtc_group_alm2map",
     "shtc_group_map2alm", "shtc_group_alm2map_dev", "shtc_group_map2alm_dev", "shtc_set_ladder",

@@ -75,7 +75,7 @@ def build_dropin(force: bool = False) -> Path:
     srcs = [CSRC / "sht_dropin.cpp", CSRC / "sht_edge.cpp"]
     if not srcs[0].exists():
         return DROPIN_LIB
-    hdrs = list((ROOT / "include" / "sht").glob("*.hpp")) + [ROOT / "include" / "shtc.h"]
+    hdrs = list((ROOT / "include" / "sht").glob("*.hpp")) + [ROOT / "include" / "shtc.h", CSRC / "hostcopy.h"]
     newest = max(p.stat().st_mtime for p in srcs + hdrs + [LIB, CSRC / "sht_cli.cpp"])
     if not force and DROPIN_LIB.exists() and CLI_BIN.exists() and DROPIN_LIB.stat().st_mtime >= newest:
         return DROPIN_LIB

@@ -19,11 +19,13 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <mutex>
 #include <numbers>
 #include <numeric>
 #include <stdexcept>
 #include <string>
+#include <thread>
 
 #include "sht/alm.hpp"
 #include "sht/distribution.hpp"
@@ -33,6 +35,7 @@
 #include "sht/perfmodel.hpp"
 #include "sht/transforms.hpp"
 #include "shtc.h"
+#include "hostcopy.h"
 
 namespace sht {
 
@@ -124,6 +127,21 @@ struct Engine {
     int grp_lmax = -1, grp_mmax = -1;
     std::vector<std::vector<int>> grp_msets, grp_rsets;
 
+    // page-locked result buffer (grows, kept for the process): large transforms write their
+    // output here while the returned container is value-initialised on a helper thread
+    void* pin = nullptr;
+    size_t pin_bytes = 0;
+    double* pinned(size_t bytes) {
+        if (bytes > pin_bytes) {
+            shtc_host_free(pin);
+            pin = nullptr;
+            pin_bytes = 0;
+            if (shtc_host_alloc(bytes, &pin) != SHTC_OK) throw std::runtime_error("sht: page-locked allocation failed");
+            pin_bytes = bytes;
+        }
+        return static_cast<double*>(pin);
+    }
+
     shtc_ctx* get() {
         if (!ctx) {
             const char* d = std::getenv("SHT_DEVICE");
@@ -202,6 +220,39 @@ struct Engine {
         return grp;
     }
 };
+
+// The reference API returns its results by value in value-initialised std::vectors.  For a
+// large result the zero fill (page faults on one thread: 147-160 ms for the 403 MB C4 map) costs
+// far more than the transform, so it runs on a helper thread (huge-page advice + parallel first
+// touch + memset, shtc_host::value_init) while the GPU transform writes into the engine's
+// page-locked buffer; the result is then copied in on all host cores with streaming stores.
+template <class T, class Xform>
+void into_container(Engine& e, std::vector<T>& v, size_t n, Xform&& xform) {
+    const size_t bytes = n * sizeof(T);
+    if (bytes < (size_t(16) << 20)) {
+        v.assign(n, T{});
+        xform(reinterpret_cast<double*>(v.data()));
+        return;
+    }
+    double* out = e.pinned(bytes);
+    std::exception_ptr fill_err;
+    std::thread filler([&] {
+        try {
+            shtc_host::value_init(v, n);
+        } catch (...) {
+            fill_err = std::current_exception();
+        }
+    });
+    try {
+        xform(out);
+    } catch (...) {
+        filler.join();
+        throw;
+    }
+    filler.join();
+    if (fill_err) std::rethrow_exception(fill_err);
+    shtc_host::par_memcpy(v.data(), out, bytes);
+}
 
 Engine& engine() {
     static Engine e;
@@ -548,12 +599,13 @@ SkyMap run_synthesis(const AlmSet& alm, const PixelGrid& grid, PairPolicy pairin
     check_grid(grid, pairing, "synthesis");
     SkyMap map;
     map.grid = grid;
-    map.pixels.assign(static_cast<size_t>(grid.n_pix), 0.0);
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
     const double pre = bind_planned(e, grid, alm.lmax, alm.mmax, pairing);
     if (precompute_s) *precompute_s = pre;
-    ok(shtc_alm2map(e.ctx, reinterpret_cast<const double*>(alm.values.data()), map.pixels.data(), t), e.ctx);
+    into_container(e, map.pixels, static_cast<size_t>(grid.n_pix), [&](double* out) {
+        ok(shtc_alm2map(e.ctx, reinterpret_cast<const double*>(alm.values.data()), out, t), e.ctx);
+    });
     return map;
 }
 
@@ -565,12 +617,16 @@ AlmSet run_analysis(const SkyMap& map, int lmax, int mmax, PairPolicy pairing, s
     if (map.pixels.size() != static_cast<size_t>(grid.n_pix))
         throw std::invalid_argument("analysis: pixel count != grid");
     check_grid(grid, pairing, "analysis");
-    AlmSet out(lmax, mmax);
+    AlmSet out;
+    out.lmax = lmax;
+    out.mmax = mmax;
     Engine& e = engine();
     std::lock_guard<std::mutex> lock(e.mu);
     const double pre = bind_planned(e, grid, lmax, mmax, pairing);
     if (precompute_s) *precompute_s = pre;
-    ok(shtc_map2alm(e.ctx, map.pixels.data(), reinterpret_cast<double*>(out.values.data()), t), e.ctx);
+    into_container(e, out.values, AlmSet::count(lmax, mmax), [&](double* dst) {
+        ok(shtc_map2alm(e.ctx, map.pixels.data(), dst, t), e.ctx);
+    });
     return out;
 }
 }  // namespace
@@ -807,7 +863,6 @@ SkyMap distributed_synthesis(const AlmSet& alm, const PixelGrid& grid, const Wor
     check_grid(grid, o.pairing, "distributed_synthesis");
     SkyMap map;
     map.grid = grid;
-    map.pixels.assign(static_cast<size_t>(grid.n_pix), 0.0);
     shtc_group_timing t{};
     double pre = 0.0;
     {
@@ -816,7 +871,9 @@ SkyMap distributed_synthesis(const AlmSet& alm, const PixelGrid& grid, const Wor
         const auto t0 = Clock::now();
         shtc_group* g = e.group(grid, layout, alm.lmax, alm.mmax, o.pairing == PairPolicy::mirror);
         pre = seconds_since(t0);
-        gok(shtc_group_alm2map(g, reinterpret_cast<const double*>(alm.values.data()), map.pixels.data(), &t), g);
+        into_container(e, map.pixels, static_cast<size_t>(grid.n_pix), [&](double* out) {
+            gok(shtc_group_alm2map(g, reinterpret_cast<const double*>(alm.values.data()), out, &t), g);
+        });
     }
     fill_profiler(o.profiler, layout, grid, alm.lmax, o, pre, t.legendre_ms, t.fft_ms, t.exchange_ms);
     return map;
@@ -837,7 +894,9 @@ AlmSet distributed_analysis(const SkyMap& map, int lmax, int mmax, const WorkerL
         return a;
     }
     check_grid(map.grid, o.pairing, "distributed_analysis");
-    AlmSet out(lmax, mmax);
+    AlmSet out;
+    out.lmax = lmax;
+    out.mmax = mmax;
     shtc_group_timing t{};
     double pre = 0.0;
     {
@@ -846,7 +905,9 @@ AlmSet distributed_analysis(const SkyMap& map, int lmax, int mmax, const WorkerL
         const auto t0 = Clock::now();
         shtc_group* g = e.group(map.grid, layout, lmax, mmax, o.pairing == PairPolicy::mirror);
         pre = seconds_since(t0);
-        gok(shtc_group_map2alm(g, map.pixels.data(), reinterpret_cast<double*>(out.values.data()), &t), g);
+        into_container(e, out.values, AlmSet::count(lmax, mmax), [&](double* dst) {
+            gok(shtc_group_map2alm(g, map.pixels.data(), dst, &t), g);
+        });
     }
     fill_profiler(o.profiler, layout, map.grid, lmax, o, pre, t.legendre_ms, t.fft_ms, t.exchange_ms);
     return out;

@@ -1323,6 +1323,22 @@ shtc_status shtc_plan_phase_stats(shtc_ctx* ctx, uint64_t* prefix, uint64_t* che
     });
 }
 
+shtc_status shtc_host_alloc(size_t bytes, void** out) {
+    if (!out) return SHTC_EINVAL;
+    *out = nullptr;
+    if (bytes == 0) return SHTC_OK;
+    if (cudaHostAlloc(out, bytes, cudaHostAllocPortable) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return SHTC_ENOMEM;
+    }
+    return SHTC_OK;
+}
+
+void shtc_host_free(void* p) {
+    if (p) cudaFreeHost(p);
+}
+
 shtc_status shtc_plan_executed(shtc_ctx* ctx, uint64_t* alm2map, uint64_t* map2alm) {
     if (!ctx) return SHTC_EINVAL;
     return guarded(ctx, [&] {
