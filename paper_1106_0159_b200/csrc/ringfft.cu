@@ -505,9 +505,12 @@ __device__ __forceinline__ void l2_prefetch(const void* p, int64_t bytes) {
 
 // Everything ring `ri` will read from HBM (its Delta row or ring samples and its tables), so
 // the next ring of this persistent CTA streams into L2 while the current one is transformed.
+#ifndef P2_PREFETCH
+#define P2_PREFETCH 1  // L2 prefetch of the ring one grid-stride ahead (0: off, experiments)
+#endif
 template <int M, int T, bool SYN>
 __device__ __forceinline__ void p2_prefetch_ring(const RingStageArgs& a, int ri) {
-    if (ri >= a.n_rings) return;
+    if (!P2_PREFETCH || ri >= a.n_rings) return;
     const RingDesc d = a.rings[ri];
     if (SYN) {
         if (!a.m_base) l2_prefetch<T>(a.delta_in + (int64_t)d.ring_pos * a.ld, (int64_t)(a.mmax + 1) * 16);
@@ -519,6 +522,30 @@ __device__ __forceinline__ void p2_prefetch_ring(const RingStageArgs& a, int ri)
     if (d.flags & 2) {
         l2_prefetch<T>(a.tabs + d.chirp_off, (int64_t)d.N * 16);
         l2_prefetch<T>(a.tabs + d.h_off, (int64_t)M * 16);
+    }
+}
+
+// The same with one bulk prefetch per range, issued by one thread from a descriptor already in
+// shared memory (cp.async.bulk.prefetch.L2: no per-line instructions, no descriptor load on the
+// issuing path).  Ranges are widened to 16-byte alignment.
+__device__ __forceinline__ void bulk_prefetch_l2(const void* p, int64_t bytes) {
+    if (bytes <= 0) return;
+    const uintptr_t b = reinterpret_cast<uintptr_t>(p) & ~uintptr_t(15);
+    const uintptr_t e = (reinterpret_cast<uintptr_t>(p) + (uintptr_t)bytes + 15) & ~uintptr_t(15);
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(b), "r"((unsigned)(e - b)) : "memory");
+}
+template <int M, bool SYN>
+__device__ __forceinline__ void p2_bulk_prefetch_ring(const RingStageArgs& a, const RingDesc& d) {
+    if (SYN) {
+        if (!a.m_base) bulk_prefetch_l2(a.delta_in + (int64_t)d.ring_pos * a.ld, (int64_t)(a.mmax + 1) * 16);
+    } else {
+        bulk_prefetch_l2(a.map_in + d.pix_off, (int64_t)d.n * 8);
+    }
+    bulk_prefetch_l2(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);
+    if (d.phi0 != 0.0) bulk_prefetch_l2(a.tabs + d.ph_off, (int64_t)(64 + (a.mmax >> 6) + 1) * 16);
+    if (d.flags & 2) {
+        bulk_prefetch_l2(a.tabs + d.chirp_off, (int64_t)d.N * 16);
+        bulk_prefetch_l2(a.tabs + d.h_off, (int64_t)M * 16);
     }
 }
 
@@ -588,13 +615,14 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
     extern __shared__ __align__(16) double2 smem[];
     __shared__ int s_ri, s_nxt;
     __shared__ __align__(16) RingDesc s_desc[2];  // this ring's descriptor and the next one's
+    __shared__ __align__(16) RingDesc s_pdesc;    // the ring one grid-stride ahead (L2 prefetch)
     double2* buf = smem;                        // p2pad(M) + 1 (H_N of direct rings)
     double2* tws = smem + p2pad(M) + 16;        // pass twiddles (P2Plan<M, E>::TW)
     double2* phlo = tws + P2Plan<M, E>::TW;     // 64 + (mmax >> 6) + 1 phase factors
     const int t = threadIdx.x, mmax = a.mmax;
     const PhaseTab ph{phlo, phlo + 64};
     p2_twsm_build<M, E>(tws, a.p2_tw);
-    p2_prefetch_ring<M, T, true>(a, blockIdx.x);
+    if (t == 0 && P2_PREFETCH && blockIdx.x < a.n_rings) p2_bulk_prefetch_ring<M, true>(a, a.rings[blockIdx.x]);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
     desc_fetch(&s_desc[0], a, s_ri, t);
@@ -610,7 +638,9 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
         P2T_START;
         int nxt = 0;
         if (t == 0) s_nxt = nxt = atomicAdd(a.counter, 1);
-        p2_prefetch_ring<M, T, true>(a, ri + gridDim.x);
+        // the ring one grid-stride ahead: its descriptor now (warp 1, asynchronously), its data
+        // into L2 after the fold barrier (one thread, bulk prefetches)
+        const int pri = ri + gridDim.x;
         double2 v[E];
         {
             const RingDesc& d = sdesc_at(s_desc, cur);
@@ -630,6 +660,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 __syncthreads();
             }
             P2T(0);
+            if (P2_PREFETCH && t >= 32) desc_fetch(&s_pdesc, a, pri, t - 32);  // waited for at the fold barrier
             // fold (ring_synthesis_into's bins, fourier.cpp:17-25): H_k for 0 <= k <= N, terms
             // in ascending m as the reference adds them.  k = N of a direct ring (N == M) is an
             // extra slot of thread 0 in the last batch.
@@ -736,8 +767,10 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                 const int k = t + T * j;
                 wv[j] = __ldg(&hw[k < N ? k : 0]);  // valid position, result masked below
             }
+            if (P2_PREFETCH && t >= 32 && t < 32 + kDescChunks) cp_async_wait_all();  // s_pdesc landed
             __syncthreads();
             desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor, in flight until the ring's end
+            if (P2_PREFETCH && t == 0 && pri < a.n_rings) p2_bulk_prefetch_ring<M, true>(a, s_pdesc);
             P2T(2);
 #pragma unroll
             for (int j = 0; j < E; ++j) {
@@ -829,13 +862,14 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
     extern __shared__ __align__(16) double2 smem[];
     __shared__ int s_ri, s_nxt;
     __shared__ __align__(16) RingDesc s_desc[2];  // this ring's descriptor and the next one's
+    __shared__ __align__(16) RingDesc s_pdesc;    // the ring one grid-stride ahead (L2 prefetch)
     double2* buf = smem;
     double2* tws = smem + p2pad(M) + 16;
     double2* phlo = tws + P2Plan<M, E>::TW;
     const int t = threadIdx.x, mmax = a.mmax;
     const PhaseTab ph{phlo, phlo + 64};
     p2_twsm_build<M, E>(tws, a.p2_tw);
-    p2_prefetch_ring<M, T, false>(a, blockIdx.x);
+    if (t == 0 && P2_PREFETCH && blockIdx.x < a.n_rings) p2_bulk_prefetch_ring<M, false>(a, a.rings[blockIdx.x]);
     if (t == 0) s_ri = atomicAdd(a.counter, 1);
     __syncthreads();
     desc_fetch(&s_desc[0], a, s_ri, t);
@@ -847,7 +881,8 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
         if (ri >= a.n_rings) break;
         int nxt = 0;
         if (t == 0) s_nxt = nxt = atomicAdd(a.counter, 1);
-        p2_prefetch_ring<M, T, false>(a, ri + gridDim.x);
+        const int pri = ri + gridDim.x;
+        if (P2_PREFETCH && t >= 32) desc_fetch(&s_pdesc, a, pri, t - 32);
         double2 v[E];
         {
             const RingDesc& d = sdesc_at(s_desc, cur);
@@ -880,12 +915,15 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
                 }
             }
         }
+        if (P2_PREFETCH && t >= 32 && t < 32 + kDescChunks) cp_async_wait_all();  // s_pdesc lands before the FFT's barriers
         if constexpr (!BLUE) {
             p2_fft<M, E, -1>(v, buf, tws);
             desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor
+            if (P2_PREFETCH && t == 0 && pri < a.n_rings) p2_bulk_prefetch_ring<M, false>(a, s_pdesc);
         } else {
             p2_fft<M, E, -1>(v, buf, tws);
             desc_fetch(&s_desc[cur ^ 1], a, s_nxt, t);  // the next ring's descriptor
+            if (P2_PREFETCH && t == 0 && pri < a.n_rings) p2_bulk_prefetch_ring<M, false>(a, s_pdesc);
             __threadfence_block();
             {
                 const double2* __restrict__ H = a.tabs + sdesc_at(s_desc, cur).h_off;
