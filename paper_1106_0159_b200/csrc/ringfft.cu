@@ -775,16 +775,20 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
 #pragma unroll
             for (int j = 0; j < E; ++j) {
                 const int k = t + T * j;
-                const int kc = k < N ? k : 0;  // table loads from valid positions, result masked
-                const double2 w = wv[j];
-                double2 c = make_double2(1.0, 0.0);
-                if constexpr (BLUE) c = __ldg(&chirp[kc]);
-                const double2 Hp = buf[p2pad(kc)], Hq = buf[p2pad(N - kc)];
-                const double2 e = cadd(Hp, cconj(Hq));
-                const double2 o = cmul(csub(Hp, cconj(Hq)), cconj(w));
-                double2 z = cadd(e, cmul_si(o, +1));
-                if constexpr (BLUE) z = cmul(z, cconj(c));
-                v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                if (BLUE && T * j >= N) {  // Bluestein zero padding (uniform over the CTA): no work
+                    v[j] = make_double2(0.0, 0.0);
+                } else {
+                    const int kc = k < N ? k : 0;  // table loads from valid positions, result masked
+                    const double2 w = wv[j];
+                    double2 c = make_double2(1.0, 0.0);
+                    if constexpr (BLUE) c = __ldg(&chirp[kc]);
+                    const double2 Hp = buf[p2pad(kc)], Hq = buf[p2pad(N - kc)];
+                    const double2 e = cadd(Hp, cconj(Hq));
+                    const double2 o = cmul(csub(Hp, cconj(Hq)), cconj(w));
+                    double2 z = cadd(e, cmul_si(o, +1));
+                    if constexpr (BLUE) z = cmul(z, cconj(c));
+                    v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                }
             }
             P2T(3);
         }
