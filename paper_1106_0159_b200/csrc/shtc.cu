@@ -10,6 +10,7 @@
 // There is no CPU fallback: every compute entry point needs the CUDA device.
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -18,6 +19,7 @@
 #include <memory>
 #include <numeric>
 #include <string>
+#include <tuple>
 #include <condition_variable>
 #include <mutex>
 #include <thread>
@@ -452,12 +454,50 @@ int m2a_band_group() {
     return g;
 }
 
+// LSD radix sort of 64-bit keys, 16-bit digits (4 passes; digits that are constant over all keys
+// are skipped): the plan's item sorts (~130 K keys at C4) in ~1 ms instead of ~3 ms each.
+void radix_sort_u64(std::vector<uint64_t>& v) {
+    std::vector<uint64_t> tmp(v.size());
+    std::vector<size_t> cnt(65536);
+    for (int sh = 0; sh < 64; sh += 16) {
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (uint64_t x : v) ++cnt[(x >> sh) & 0xffff];
+        if (!v.empty() && cnt[(v[0] >> sh) & 0xffff] == v.size()) continue;  // constant digit
+        size_t sum = 0;
+        for (auto& c : cnt) {
+            const size_t n = c;
+            c = sum;
+            sum += n;
+        }
+        for (uint64_t x : v) tmp[cnt[(x >> sh) & 0xffff]++] = x;
+        v.swap(tmp);
+    }
+}
+
+// SHTC_PLAN_TRACE=1: wall-clock ms of each plan phase (the stream synchronised at every mark)
+struct PlanTrace {
+    cudaStream_t s;
+    const char* what;
+    std::chrono::steady_clock::time_point t = std::chrono::steady_clock::now();
+    void mark(const char* phase) {
+        static const bool on = std::getenv("SHTC_PLAN_TRACE") != nullptr;
+        if (!on) return;
+        cudaStreamSynchronize(s);
+        const auto now = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "[plan %s] %s %.2f ms\n", what, phase,
+                     std::chrono::duration<double, std::milli>(now - t).count());
+        t = now;
+    }
+};
+
 void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set ms*/, const std::vector<int>& ms,
                     std::vector<Stream> streams, const std::vector<double>& log_mu) {
     cudaStream_t s = c->stream;
     cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
+    PlanTrace tr{s, "legendre"};
     CK(cudaEventRecord(e0, s));
     P = LegPlan();  // release previous
+    tr.mark("release");
     P.lmax = lmax;
     P.ms = ms;
     sort_streams(streams);
@@ -476,6 +516,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         sno[i] = streams[i].north;
         sso[i] = streams[i].south;
     }
+    tr.mark("streams + bands (host)");
     std::vector<int64_t> toff(n_m);
     int64_t tot = 0;
     for (int i = 0; i < n_m; ++i) {
@@ -490,6 +531,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     P.sn.upload(sno, s);
     P.ss.upload(sso, s);
     P.tab_off.upload(toff, s);
+    tr.mark("small uploads");
     P.A.ensure(tot * sizeof(double));
     P.C.ensure(tot * sizeof(double));
     P.T.ensure(tot * sizeof(double));
@@ -506,8 +548,10 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     v.n_tiles = (ns + LEG_TILE - 1) / LEG_TILE;
     v.unscaled = c->ladder ? 0 : 1;
 
+    tr.mark("streams + uploads");
     if (n_m > 0) launch_leg_tables(v.ms, n_m, lmax, v.tab, s);
     CK(cudaGetLastError());
+    tr.mark("recurrence tables");
 
     P.ck_act.ensure((size_t)std::max(1, n_m * ns) * sizeof(int));
     P.ck_q.ensure((size_t)std::max(1, n_m * ns) * sizeof(double2));
@@ -525,6 +569,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
                                 c->stats.as<unsigned long long>(), s);
         CK(cudaGetLastError());
     }
+    tr.mark("activation scan + tile summary");
     std::vector<int2> info((size_t)n_m * v.n_tiles);
     unsigned long long useful = 0;
     if (!info.empty())
@@ -533,6 +578,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     CK(cudaStreamSynchronize(s));
     P.useful = useful;
 
+    tr.mark("tile info to host");
     // alive tile lists per order and the cost-sorted work queues of the persistent kernels
     // Two item sets: cost-ordered for the device-resident single launches, band-ordered for
     // the pipelined host-buffer paths.  Tile lists run in descending tile index, i.e. bands in
@@ -669,6 +715,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         for (; k < it.b; ++k) c += pass_cost(it.mi, tl[it.a + k], -1);
         return c;
     };
+    tr.mark("items + accounting");
     // order chunks of ~equal coefficient counts (H2D / D2H units of the pipelined paths)
     std::vector<int> chunk_of(n_m, 0);
     P.chunk_mi.assign(1, 0);
@@ -696,10 +743,27 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
             acc += lmax - ms[i] + 1;
         }
     }
-    std::stable_sort(a2m.begin(), a2m.end(),
-                     [&](const LegItem& a, const LegItem& b) { return a2m_cost(a) > a2m_cost(b); });
-    std::stable_sort(m2a.begin(), m2a.end(),
-                     [&](const LegItem& a, const LegItem& b) { return m2a_cost(a) > m2a_cost(b); });
+    tr.mark("order chunks");
+    // stable sorts by a key computed once per item (sorting (key, original index) pairs): the
+    // cost functions walk tile lists, so evaluating them per comparison cost ~25 ms at C4
+    // Keys are packed into one 64-bit word: group (16 bits) | inverted cost (24 bits) | original
+    // index (24 bits), so a plain integer sort is the stable sort.
+    auto sort_items = [](std::vector<LegItem>& v, auto group, auto cost) {
+        if (v.size() >= (size_t(1) << 24)) fail(SHTC_EUNSUPPORTED, "plan: too many work items");
+        std::vector<uint64_t> kv(v.size());
+        for (size_t i = 0; i < v.size(); ++i) {
+            const uint64_t g = (uint64_t)group(v[i]) & 0xffff;
+            const uint64_t c = (uint64_t)std::min<int64_t>(cost(v[i]), (int64_t(1) << 24) - 1);
+            kv[i] = (g << 48) | ((((uint64_t(1) << 24) - 1) - c) << 24) | (uint64_t)i;
+        }
+        radix_sort_u64(kv);
+        std::vector<LegItem> out(v.size());
+        for (size_t i = 0; i < v.size(); ++i) out[i] = v[kv[i] & 0xffffff];
+        v.swap(out);
+    };
+    auto no_group = [](const LegItem&) { return 0; };
+    sort_items(a2m, no_group, a2m_cost);
+    sort_items(m2a, no_group, m2a_cost);
     // alm2map band set: band, then (band 0 only) order chunk, then cost
     // the head bands (0 .. a2m_head_bands()-1) run together, split by order chunk, while a_lm
     // arrives (launch band tag 0)
@@ -709,10 +773,10 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         return std::make_pair(head ? 0 : tc, head ? chunk_of[it.mi] : 0);
     };
     std::vector<LegItem> a2m_b = a2m;
-    std::stable_sort(a2m_b.begin(), a2m_b.end(), [&](const LegItem& a, const LegItem& b) {
-        if (a2m_key(a) != a2m_key(b)) return a2m_key(a) < a2m_key(b);
-        return a2m_cost(a) > a2m_cost(b);
-    });
+    sort_items(a2m_b, [&](const LegItem& it) {
+        const auto k = a2m_key(it);
+        return (k.first << 8) | k.second;
+    }, a2m_cost);
     P.a2m_launch.clear();
     for (size_t k = 0; k < a2m_b.size();) {
         size_t e = k;
@@ -728,10 +792,10 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         const int tag = m2a_tag[tband[tl[it.a + it.b - 1]]];
         return std::make_pair(tag, tag == kPipeBands - 1 ? m2a_chunk_of[it.mi] : 0);
     };
-    std::stable_sort(m2a_b.begin(), m2a_b.end(), [&](const LegItem& a, const LegItem& b) {
-        if (m2a_key(a) != m2a_key(b)) return m2a_key(a) < m2a_key(b);
-        return m2a_cost(a) > m2a_cost(b);
-    });
+    sort_items(m2a_b, [&](const LegItem& it) {
+        const auto k = m2a_key(it);
+        return (k.first << 8) | k.second;
+    }, m2a_cost);
     P.m2a_launch.clear();
     std::vector<int> last_launch(n_m, 0);  // orders without items are final from the start
     for (size_t k = 0; k < m2a_b.size();) {
@@ -757,6 +821,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
         P.m2a_final_off.push_back((int)fl.size());
     }
     if (fl.empty()) fl.push_back(0);
+    tr.mark("sorts + launch sets");
     P.m2a_final_list.upload(fl, s);
     if (tl.empty()) tl.push_back(0);
     P.tile_list.upload(tl, s);
@@ -796,6 +861,7 @@ void build_leg_plan(shtc_ctx* c, LegPlan& P, int lmax, int /*mmax: the order set
     float ms_el = 0.f;
     CK(cudaEventElapsedTime(&ms_el, e0, e1));
     P.build_ms = ms_el;
+    tr.mark("uploads");
     P.built = true;
 }
 
@@ -825,6 +891,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
                     const std::vector<int>& ring_band = {}) {
     cudaStream_t s = c->stream;
     cudaEvent_t e0 = c->ev[6], e1 = c->ev[7];
+    PlanTrace tr{s, "fft"};
     CK(cudaEventRecord(e0, s));
     for (auto& d : F.descs) d.release();
     F.tabs.release();
@@ -913,11 +980,14 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         per_class[cls].push_back(d);
         F.tw_off[cls] = clus ? table(0, FFT_P2C_B / 2) : d.tw_off;
     }
+    tr.mark("descriptors");
     F.tabs.ensure((size_t)std::max<int64_t>(tot, 1) * sizeof(double2));
+    tr.mark("table allocation");
     DevBuf jobs_d;
     jobs_d.upload(jobs, s);
     launch_fill_tables(jobs_d.as<TableJob>(), (int)jobs.size(), F.tabs.as<double2>(), s);
     CK(cudaGetLastError());
+    tr.mark("tables");
     for (int k = 0; k < FFT_N_CLASSES; ++k) {
         if (!blue_class[k].empty()) {
             DevBuf bd;
@@ -936,6 +1006,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         CK(cudaGetLastError());
         CK(cudaStreamSynchronize(s));
     }
+    tr.mark("bluestein FFT(h)");
     // pipeline bands: descriptors of each class grouped by band (ring order inside a band),
     // pixel intervals of each band for the host copies
     {
@@ -973,6 +1044,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
     float el = 0.f;
     CK(cudaEventElapsedTime(&el, e0, e1));
     F.build_ms = el;
+    tr.mark("band ranges + uploads");
     F.built = true;
 }
 
