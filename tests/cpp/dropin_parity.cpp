@@ -11,6 +11,7 @@
 #include <random>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "sht/distribution.hpp"
@@ -26,6 +27,10 @@ int ref_analysis(int, int, const double*, int, int, int, const double*, const in
 int ref_compute_delta_a(int, int, const double*, int, const double*, int, const int32_t*, int, int, int,
                         double*, uint64_t*);
 int ref_accumulate_alm(int, int, int, const double*, int, const int32_t*, const double*, double*, uint64_t*);
+int ref_distributed_synthesis(int, int, const double*, int, int, int, const double*, const int32_t*,
+                              const double*, const double*, int, int, int, int, double*, double*, uint64_t*);
+int ref_distributed_analysis(int, int, const double*, int, int, int, const double*, const int32_t*,
+                             const double*, const double*, int, int, int, int, double*, double*, uint64_t*);
 }
 
 static int fails = 0, passes = 0;
@@ -108,6 +113,43 @@ int main() {
         auto a = sht::analysis(in, lmax, lmax, opt);
         CHECK(rel_rms(reinterpret_cast<const double*>(a.values.data()), aw.data(), aw.size()) <= 1e-12,
               "healpix analysis vs reference");
+    }
+    // C2 (nside 1024, lmax 2048): results above the drop-in's large-container threshold, which
+    // are value-initialised on a helper thread while the GPU writes a page-locked buffer
+    {
+        const int ns = 1024, lmax = 2048;
+        auto g = sht::build_healpix_grid(ns);
+        auto alm = sht::random_alm(lmax, lmax, 2026);
+        RefGrid rg(g);
+        const int nt = (int)std::max(1u, std::thread::hardware_concurrency());
+        std::vector<double> want(g.n_pix);
+        ref_distributed_synthesis(lmax, lmax, reinterpret_cast<const double*>(alm.values.data()), 0, ns, g.n_rings(),
+                                  rg.c.data(), rg.n.data(), rg.p.data(), rg.w.data(), 1, nt, 1, 0, want.data(),
+                                  nullptr, nullptr);
+        sht::TransformOptions opt;
+        opt.pairing = sht::PairPolicy::mirror;
+        auto m = sht::synthesis(alm, g, opt);
+        CHECK(m.pixels.size() == want.size() && rel_rms(m.pixels.data(), want.data(), want.size()) <= 1e-10,
+              "C2 synthesis (large result container) vs reference");
+        std::vector<double> aw(2 * alm.values.size());
+        ref_distributed_analysis(lmax, lmax, want.data(), 0, ns, g.n_rings(), rg.c.data(), rg.n.data(), rg.p.data(),
+                                 rg.w.data(), 1, nt, 1, 0, aw.data(), nullptr, nullptr);
+        sht::SkyMap in{g, want};
+        auto a = sht::analysis(in, lmax, lmax, opt);
+        CHECK(a.lmax == lmax && a.mmax == lmax && a.values.size() == alm.values.size() &&
+                  rel_rms(reinterpret_cast<const double*>(a.values.data()), aw.data(), aw.size()) <= 1e-10,
+              "C2 analysis (large result container) vs reference");
+        // twice more: the page-locked buffer is reused and every call returns its own container
+        auto m2 = sht::synthesis(alm, g, opt);
+        CHECK(m2.pixels == m.pixels, "repeated C2 synthesis identical");
+        auto lay = sht::WorkerLayout::create(g, lmax, 2);
+        sht::RunOptions ro;
+        ro.pairing = sht::PairPolicy::mirror;
+        auto md = sht::distributed_synthesis(alm, g, lay, ro);
+        CHECK(md.pixels == m.pixels, "C2 distributed synthesis (2 workers) = synthesis");
+        auto ad = sht::distributed_analysis(in, lmax, lmax, lay, ro);
+        CHECK(rel_rms(reinterpret_cast<const double*>(ad.values.data()), aw.data(), aw.size()) <= 1e-10,
+              "C2 distributed analysis (2 workers) vs reference");
     }
     // delta panel and accumulation vs the reference (test_transforms.cpp:99-148)
     {
