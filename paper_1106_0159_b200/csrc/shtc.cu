@@ -1088,7 +1088,7 @@ float elapsed(cudaEvent_t a, cudaEvent_t b) {
 // the small-ring classes (latency bound: few CTAs, aliasing folds over many wraps) run on
 // kFftAux side streams at the same time, joined back before the stage ends.
 template <class Launch>
-void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launch) {
+void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launch, bool big_on_side = false) {
     if (!c->fft_fork) {
         for (int i = 0; i < fft_aux_count(); ++i) CK(cudaStreamCreateWithFlags(&c->fft_aux[i], cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&c->fft_fork, cudaEventDisableTiming));
@@ -1106,7 +1106,12 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         const int b = range < 0 ? 0 : F.range_start[k][range];
         const int e = range < 0 ? F.count[k] : F.range_start[k][range + 1];
         if (e <= b) continue;
-        const bool big = k >= FFT_N_GENERIC && fft_class_bmax(k) >= 2048;
+        // big_on_side: the large classes on side streams too, so one class's tail overlaps the
+        // next class's start (analysis: C4 0.73 -> 0.70 ms; synthesis measured no gain).
+        // SHTC_FFT_BIG_SIDE=0/1 forces it for both directions.
+        static const int big_side_env = std::getenv("SHTC_FFT_BIG_SIDE") ? std::atoi(std::getenv("SHTC_FFT_BIG_SIDE")) : -1;
+        const bool side_big = big_side_env >= 0 ? big_side_env != 0 : big_on_side;
+        const bool big = k >= FFT_N_GENERIC && fft_class_bmax(k) >= 2048 && !side_big;
         cudaStream_t st = s;
         if (!big) {
             const int i = side++ % fft_aux_count();
@@ -1154,7 +1159,7 @@ void run_ring_anal(shtc_ctx* c, FftPlan& F, const double* map, double2* delta, c
         a.map_in = map;
         a.delta_out = delta;
         launch_ring_analysis(k, a, st);
-    });
+    }, true);
 }
 
 void fill_timing(shtc_timing* t, double leg, double fft, double h2d, double d2h, double total,
