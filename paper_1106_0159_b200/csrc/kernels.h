@@ -193,6 +193,9 @@ struct RingStageArgs {
     // exchange layouts list orders grouped by owner so consecutive threads store into one
     // owner's block contiguously.  nullptr: ascending m.
     const int* m_order;
+    // 1: the class runs its alternative kernel (8192-point Bluestein: two 4096-point halves per
+    // CTA, p2_tw = the 4096-point table); chosen at plan time (every ring n > mmax)
+    int alt;
 };
 
 // size classes.  Generic (any 7-smooth length, in-place mixed radix, odd-length rings):

@@ -446,14 +446,22 @@ __device__ __forceinline__ constexpr int p2off(int r) {
     return r * NS + ((r * NS) >> 4);
 }
 
+// Barrier of the threads running one transform: the whole CTA (bar 0), or one of the thread
+// groups of a CTA that runs two half-size transforms side by side (named barrier bar, T threads)
+template <int T>
+__device__ __forceinline__ void p2_bar(int bar) {
+    if (bar == 0) __syncthreads();
+    else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(T) : "memory");
+}
+
 // One Stockham pass of radix R after NS points have been combined (butterfly b: inputs
-// b + r M/R, outputs (b/NS) NS R + b%NS + r NS).
-template <int M, int E, int R, int NS, bool LAST, int S>
-__device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const double2* tws) {
+// b + r M/R, outputs (b/NS) NS R + b%NS + r NS).  t: the thread's index in its group.
+template <int M, int E, int R, int NS, bool LAST, int S, bool GROUP>
+__device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const double2* tws, int tg, int bar) {
     constexpr int T = M / E;
     constexpr int Q = E / R;
     static_assert(T % 16 == 0, "padded exchange needs T % 16 == 0");
-    int t = threadIdx.x;
+    int t = GROUP ? tg : (int)threadIdx.x;
     asm volatile("" : "+r"(t));  // per-pass address arithmetic: nothing hoisted across passes
 #pragma unroll
     for (int q = 0; q < Q; ++q) {
@@ -473,24 +481,28 @@ __device__ __forceinline__ void p2_pass(double2 (&v)[E], double2* sm, const doub
         }
     }
     if constexpr (!LAST) {
-        __syncthreads();
+        if (GROUP) p2_bar<T>(bar);
+        else __syncthreads();
         const double2* const in = sm + p2pad(t);
 #pragma unroll
         for (int j = 0; j < E; ++j) v[j] = in[j * (T + T / 16)];
-        __syncthreads();
+        if (GROUP) p2_bar<T>(bar);
+        else __syncthreads();
     }
 }
 
-template <int M, int E, int S, int I = 0>
-__device__ __forceinline__ void p2_fft(double2 (&v)[E], double2* sm, const double2* tws) {
+// M-point FFT of the CTA (GROUP = false), or of a thread group of T = M/E threads (thread tg of
+// the group, named barrier bar) when a CTA runs two half-size transforms side by side
+template <int M, int E, int S, bool GROUP = false, int I = 0>
+__device__ __forceinline__ void p2_fft(double2 (&v)[E], double2* sm, const double2* tws, int tg = 0, int bar = 0) {
     using PL = P2Plan<M, E>;
     constexpr bool LAST = I == PL::P - 1;
     if constexpr (I == 0) {
-        p2_pass<M, E, PL::R0, 1, LAST, S>(v, sm, tws);
+        p2_pass<M, E, PL::R0, 1, LAST, S, GROUP>(v, sm, tws, tg, bar);
     } else {
-        p2_pass<M, E, E, PL::ns(I), LAST, S>(v, sm, tws + PL::off(I));
+        p2_pass<M, E, E, PL::ns(I), LAST, S, GROUP>(v, sm, tws + PL::off(I), tg, bar);
     }
-    if constexpr (!LAST) p2_fft<M, E, S, I + 1>(v, sm, tws);
+    if constexpr (!LAST) p2_fft<M, E, S, GROUP, I + 1>(v, sm, tws, tg, bar);
 }
 
 }  // namespace
@@ -1009,6 +1021,253 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_anal_kernel(RingStageArgs
         }
         if (t == 0) s_ri = nxt;  // every thread read s_ri before this ring's first barrier
         __syncthreads();  // buf / phase table / descriptors / s_ri reuse by the next ring
+        cur ^= 1;
+    }
+}
+
+// ---------------------------------------------------------------------------------------
+// Bluestein buffers of 8192 points (rings of 4098..8188 samples whose half length is not a
+// power of two: the largest polar-cap class at nside 2048) as two 4096-point halves in one
+// CTA.  The chirped input lives in [0, N) with N < 4096, so one decimation-in-frequency step
+// splits the forward transform into two independent 4096-point transforms of x_b (outputs
+// 2k) and x_b W_8192^b (outputs 2k + 1), one per thread group of 256 (named barriers 1 and 2);
+// after the pointwise product the inverse halves give u_b and v_b and the result is
+// y_b = u_b + W_8192^{-b} v_b for b < N (the 2-CTA cluster class below does the same split
+// across a cluster).  Against one 8192-point transform per CTA: 2 exchanges per transform
+// instead of 3, and one group's exchange overlaps the other group's arithmetic.  Used when
+// every ring of the class has n > mmax (no aliasing wraps).
+// ---------------------------------------------------------------------------------------
+constexpr int P2H_M = 8192, P2H_MH = 4096, P2H_E = 16, P2H_T = P2H_MH / P2H_E, P2H_TT = 2 * P2H_T;
+
+template <bool SYN>
+__global__ void __launch_bounds__(P2H_TT, 1) ring_p2h_kernel(RingStageArgs a) {
+    constexpr int M = P2H_M, MH = P2H_MH, E = P2H_E, T = P2H_T, TT = P2H_TT, G = 8, U = 8;
+    extern __shared__ __align__(16) double2 smem[];
+    __shared__ int s_ri, s_nxt;
+    __shared__ __align__(16) RingDesc s_desc[2];  // this ring's descriptor and the next one's
+    __shared__ __align__(16) RingDesc s_pdesc;    // the ring one grid-stride ahead (L2 prefetch)
+    double2* buf0 = smem;                         // group 0's exchange buffer; the fold's H; Z
+    double2* buf1 = smem + p2pad(MH) + 16;        // group 1's exchange buffer; W^-b v_b
+    double2* tws = buf1 + p2pad(MH) + 16;         // P2Plan<MH, E> pass twiddles (W_4096 powers)
+    double2* phlo = tws + P2Plan<MH, E>::TW;      // 64 + (mmax >> 6) + 1 phase factors
+    const int tid = threadIdx.x, h = tid / T, t = tid % T, mmax = a.mmax;
+    double2* const buf = h ? buf1 : buf0;
+    const int bar = 1 + h;
+    const PhaseTab ph{phlo, phlo + 64};
+    p2_twsm_build<MH, E>(tws, a.p2_tw);  // both groups write the same entries (a.p2_tw: W_4096)
+    if (tid == 0) s_ri = atomicAdd(a.counter, 1);
+    if (tid == 0 && P2_PREFETCH && blockIdx.x < a.n_rings) p2_bulk_prefetch_ring<M, SYN>(a, a.rings[blockIdx.x]);
+    __syncthreads();
+    desc_fetch(&s_desc[0], a, s_ri, tid);
+    cp_async_wait_all();
+    __syncthreads();
+    int cur = 0;
+    for (;;) {
+        const int ri = s_ri;
+        if (ri >= a.n_rings) break;
+        int nxt = 0;
+        if (tid == 0) s_nxt = nxt = atomicAdd(a.counter, 1);
+        const int pri = ri + gridDim.x;
+        double2 v[E];
+        {
+            const RingDesc& d = sdesc_at(s_desc, cur);
+            const int n = d.n, N = d.N, pos = d.ring_pos;
+            const bool rot = d.phi0 != 0.0;
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            const double2* __restrict__ twm = a.tabs + d.tw_off;  // e^{-2 pi i b / 8192}
+            if (rot) phase_fetch(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, TT);
+            if (SYN) {
+                if (rot) {
+                    cp_async_wait_all();
+                    __syncthreads();
+                }
+                if (P2_PREFETCH && tid >= 32) desc_fetch(&s_pdesc, a, pri, tid - 32);
+                // fold (fourier.cpp:17-25), no wraps (n > mmax): H_k = v_k [k <= mmax] + conj
+                // v_{n-k} [n-k <= mmax] for k <= N < 4096, by all TT threads into buf0
+#pragma unroll
+                for (int j0 = 0; j0 < MH / TT; j0 += G) {
+                    double2 x1[G], x2[G];
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const int k = tid + TT * (j0 + u);
+                        const int m1 = k, m2 = (k == 0) ? n : n - k;
+                        x1[u] = a.delta_in[delta_index(a, pos, (k <= N && m1 <= mmax) ? m1 : 0)];
+                        x2[u] = a.delta_in[delta_index(a, pos, (k <= N && m2 <= mmax) ? m2 : 0)];
+                    }
+#pragma unroll
+                    for (int u = 0; u < G; ++u) {
+                        const int k = tid + TT * (j0 + u);
+                        if (k <= N) {
+                            const int m1 = k, m2 = (k == 0) ? n : n - k;
+                            double2 hk = make_double2(0.0, 0.0);
+                            if (m1 <= mmax) hk = rot_value(x1[u], m1, rot, ph);
+                            if (m2 <= mmax) hk = cadd(hk, cconj(rot_value(x2[u], m2, rot, ph)));
+                            buf0[p2pad(k)] = hk;
+                        }
+                    }
+                }
+                const double2* __restrict__ hw = a.tabs + d.hw_off;
+                double2 wv[E];
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    wv[j] = __ldg(&hw[k < N ? k : 0]);
+                }
+                if (P2_PREFETCH && tid >= 32 && tid < 32 + kDescChunks) cp_async_wait_all();  // s_pdesc landed
+                __syncthreads();
+                desc_fetch(&s_desc[cur ^ 1], a, s_nxt, tid);  // the next ring's descriptor
+                if (P2_PREFETCH && tid == 0 && pri < a.n_rings) p2_bulk_prefetch_ring<M, true>(a, s_pdesc);
+                // chirped C2R input of this group: x_k = Z_k conj(c_k) (x W_M^k for group 1)
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (T * j >= N) {
+                        v[j] = make_double2(0.0, 0.0);
+                    } else {
+                        const int kc = k < N ? k : 0;
+                        const double2 c = __ldg(&chirp[kc]);
+                        const double2 Hp = buf0[p2pad(kc)], Hq = buf0[p2pad(N - kc)];
+                        const double2 e = cadd(Hp, cconj(Hq));
+                        const double2 o = cmul(csub(Hp, cconj(Hq)), cconj(wv[j]));
+                        double2 z = cmul(cadd(e, cmul_si(o, +1)), cconj(c));
+                        if (h) z = cmul(z, __ldg(&twm[kc]));
+                        v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                    }
+                }
+                __syncthreads();  // H read by both groups before group 0's passes overwrite buf0
+            } else {
+                if (P2_PREFETCH && tid >= 32) desc_fetch(&s_pdesc, a, pri, tid - 32);
+                const int64_t po = d.pix_off;
+                const double* __restrict__ in = a.map_in + po;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (T * j >= N) {
+                        v[j] = make_double2(0.0, 0.0);
+                        continue;
+                    }
+                    const int kc = k < N ? k : 0;
+                    const double2 x = ((po & 1) == 0) ? reinterpret_cast<const double2*>(in)[kc]
+                                                      : make_double2(in[2 * kc], in[2 * kc + 1]);
+                    double2 z = cmul(x, __ldg(&chirp[kc]));
+                    if (h) z = cmul(z, __ldg(&twm[kc]));
+                    v[j] = (k < N) ? z : make_double2(0.0, 0.0);
+                }
+                if (P2_PREFETCH && tid >= 32 && tid < 32 + kDescChunks) cp_async_wait_all();  // s_pdesc lands before the barriers
+            }
+        }
+        p2_fft<MH, E, -1, true>(v, buf, tws, t, bar);
+        if (SYN) __threadfence_block();
+        if (!SYN) {
+            desc_fetch(&s_desc[cur ^ 1], a, s_nxt, tid);  // the next ring's descriptor
+            if (P2_PREFETCH && tid == 0 && pri < a.n_rings) p2_bulk_prefetch_ring<M, false>(a, s_pdesc);
+        }
+        {
+            const double2* __restrict__ H = a.tabs + sdesc_at(s_desc, cur).h_off;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const double2 hv = __ldg(&H[2 * (t + T * j) + h]);
+                v[j] = cmul(v[j], SYN ? cconj(hv) : hv);
+            }
+        }
+        p2_fft<MH, E, +1, true>(v, buf, tws, t, bar);
+        __threadfence_block();
+        if (h) {  // W_M^{-b} v_b to shared memory (group 1's last exchange read is behind its barrier)
+            const double2* __restrict__ twm = a.tabs + sdesc_at(s_desc, cur).tw_off;
+#pragma unroll
+            for (int j = 0; j < E; ++j) buf1[p2pad(t + T * j)] = cmul(v[j], cconj(__ldg(&twm[t + T * j])));
+        }
+        __syncthreads();
+        const RingDesc& d = sdesc_at(s_desc, cur);
+        const int n = d.n, N = d.N, pos = d.ring_pos;
+        if (!h) {
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            const double inv = 1.0 / (double)M;
+#pragma unroll
+            for (int j = 0; j < E; ++j) {
+                const int k = t + T * j;
+                if (T * j >= N) continue;
+                const double2 y = cadd(v[j], buf1[p2pad(k)]);
+                const double2 c = __ldg(&chirp[k < N ? k : 0]);
+                v[j] = cscale(cmul(y, SYN ? cconj(c) : c), inv);  // k >= N: not stored
+            }
+            if (SYN) {
+                const int64_t po = d.pix_off;
+                double* __restrict__ out = a.map_out + po;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) {
+                        if ((po & 1) == 0) {
+                            reinterpret_cast<double2*>(out)[k] = v[j];
+                        } else {
+                            out[2 * k] = v[j].x;
+                            out[2 * k + 1] = v[j].y;
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) buf0[p2pad(k)] = v[j];  // group 0's last exchange read is behind the barrier
+                }
+            }
+        }
+        if (!SYN) {
+            cp_async_wait_all();  // phase factors and the next descriptor have landed
+            __syncthreads();
+            // R2C split and unfold (as ring_p2_anal_kernel), all TT threads
+            const double wgt = d.weight;
+            const bool rot = d.phi0 != 0.0;
+            const double2* __restrict__ hw = a.tabs + d.hw_off;
+            const int Tn = TT % n;
+            const int* __restrict__ mord = a.m_order;
+            for (int m0 = tid; m0 <= mmax; m0 += U * TT) {
+                int bb[U], mm[U];
+                bool cj[U];
+                double2 w[U];
+                if (mord) {
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int idx = m0 + u * TT;
+                        mm[u] = idx <= mmax ? __ldg(mord + idx) : mmax + 1;
+                        const int b = (idx <= mmax ? mm[u] : 0) % n;
+                        cj[u] = b > N;
+                        bb[u] = cj[u] ? n - b : b;
+                        w[u] = __ldg(&hw[bb[u]]);
+                    }
+                } else {
+                    int b = m0 % n;
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        mm[u] = m0 + u * TT;
+                        cj[u] = b > N;
+                        bb[u] = cj[u] ? n - b : b;
+                        w[u] = __ldg(&hw[bb[u]]);
+                        b += Tn;
+                        if (b >= n) b -= n;
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int m = mm[u];
+                    const double2 Zp = buf0[p2pad(bb[u] == N ? 0 : bb[u])];
+                    const double2 Zq = buf0[p2pad(bb[u] == 0 ? 0 : N - bb[u])];
+                    const double2 e = cscale(cadd(Zp, cconj(Zq)), 0.5);
+                    const double2 o = cmul_si(cscale(csub(Zp, cconj(Zq)), 0.5), -1);
+                    double2 B = cadd(e, cmul(w[u], o));
+                    if (cj[u]) B = cconj(B);
+                    double2 val = cscale(B, wgt);
+                    if (rot && m > 0) val = cmul(val, cconj(ph.at(m <= mmax ? m : 0)));
+                    if (m <= mmax) *delta_out_at(a, pos, m) = val;
+                }
+            }
+        } else {
+            cp_async_wait_all();  // the next descriptor has landed
+        }
+        if (tid == 0) s_ri = nxt;
+        __syncthreads();  // buffers / phase table / descriptors / s_ri reuse by the next ring
         cur ^= 1;
     }
 }
@@ -1559,6 +1818,22 @@ void p2_anal(const RingStageArgs& a, cudaStream_t s) {
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
     count_launch();
 }
+size_t p2h_smem(int mmax) {
+    return (size_t)(2 * (P2H_MH + (P2H_MH >> 4) + 16) + P2Plan<P2H_MH, P2H_E>::TW) * sizeof(double2) +
+           (size_t)(64 + (mmax >> 6) + 1) * sizeof(double2);
+}
+template <bool SYN>
+void p2h_run(const RingStageArgs& a, cudaStream_t s) {
+    auto k = ring_p2h_kernel<SYN>;
+    static bool once = (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)p2h_smem(kMaxPhaseM)),
+                        true);
+    (void)once;
+    const size_t sm = p2h_smem(a.mmax);
+    k<<<p2_grid(k, P2H_TT, sm, a.n_rings), P2H_TT, sm, s>>>(a);
+    count_launch();
+}
+
 // class -> (M, E, resident CTAs per SM, Bluestein)
 template <bool SYN, int M, int E, int MINB, bool BLUE>
 void p2_run(const RingStageArgs& a, cudaStream_t s) {
@@ -1580,7 +1855,11 @@ void p2_dispatch(int cls, const RingStageArgs& a, cudaStream_t s) {
         P2_CASE(2, 1024, 4, 3, 4, 3)
         P2_CASE(3, 2048, 16, 4, P2B_E_2048, P2B_MB_2048)
         P2_CASE(4, 4096, P2D_E_4096, P2D_MB_4096, P2B_E_4096, P2B_MB_4096)
-        P2_CASE(5, 8192, P2D_E_8192, P2D_MB_8192, P2B_E_8192, P2B_MB_8192)
+        case 5:
+            if (blue && a.alt) p2h_run<SYN>(a, s);
+            else if (blue) p2_run<SYN, 8192, P2B_E_8192, P2B_MB_8192, true>(a, s);
+            else p2_run<SYN, 8192, P2D_E_8192, P2D_MB_8192, false>(a, s);
+            break;
     }
 #undef P2_CASE
 }

@@ -208,6 +208,7 @@ struct FftPlan {
     DevBuf tabs;
     DevBuf counters;  // ring queues of the power-of-two engine's launches (one per class)
     int64_t tw_off[FFT_N_CLASSES] = {};  // twiddle table of each power-of-two class
+    int alt[FFT_N_CLASSES] = {};         // class runs its alternative kernel (RingStageArgs::alt)
     double build_ms = 0.0;
 };
 
@@ -894,6 +895,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
     PlanTrace tr{s, "fft"};
     CK(cudaEventRecord(e0, s));
     for (auto& d : F.descs) d.release();
+    std::fill(std::begin(F.alt), std::end(F.alt), 0);
     F.tabs.release();
     std::vector<TableJob> jobs;
     int64_t tot = 0;
@@ -979,6 +981,20 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         }
         per_class[cls].push_back(d);
         F.tw_off[cls] = clus ? table(0, FFT_P2C_B / 2) : d.tw_off;
+    }
+    // the 8192-point Bluestein class as two 4096-point halves per CTA when no ring of it aliases
+    // (n > mmax: the split kernel's fold has no wrap loop); SHTC_P2H=0 keeps the one-transform
+    // kernel
+    {
+        static const bool p2h_on = !std::getenv("SHTC_P2H") || std::atoi(std::getenv("SHTC_P2H")) != 0;
+        const int k8 = fft_p2_class_for(8192, true);
+        bool ok = p2h_on && k8 >= 0 && !per_class[k8].empty();
+        if (ok)
+            for (const RingDesc& d : per_class[k8]) ok = ok && (d.flags & 3) == 3 && d.n > c->mmax && d.N < 4096;
+        if (ok) {
+            F.alt[k8] = 1;
+            F.tw_off[k8] = table(0, 4096);
+        }
     }
     tr.mark("descriptors");
     F.tabs.ensure((size_t)std::max<int64_t>(tot, 1) * sizeof(double2));
@@ -1127,6 +1143,7 @@ void ring_stage(shtc_ctx* c, FftPlan& F, int range, cudaStream_t s, Launch launc
         a.ld = c->mmax + 1;
         a.counter = ctr + k;
         a.p2_tw = a.tabs + F.tw_off[k];
+        a.alt = F.alt[k];
         launch(k, a, st);
         CK(cudaGetLastError());
     }
