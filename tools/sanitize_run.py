@@ -21,7 +21,10 @@ ctx = sht.Context(0)
 worst = 0.0
 # HEALPix (mirror pairs, power-of-two and Bluestein ring classes, aliasing caps) and a
 # Gauss-Legendre grid with odd n_phi (generic mixed-radix class)
-cases = [(ref.healpix_grid(64), 128), (ref.healpix_grid(8), 40), (ref.gl_grid(17, 35), 16)]
+# rings of 6002 samples (N = 3001: 8192-point Bluestein, the split two-group kernel) and of
+# 8194 (N = 4097: not 7-smooth, 16384-point 2-CTA cluster class)
+cases = [(ref.healpix_grid(64), 128), (ref.healpix_grid(8), 40), (ref.gl_grid(17, 35), 16),
+         (ref.gl_grid(6, 6002), 5), (ref.gl_grid(4, 8194), 3)]
 for g, lmax in cases:
     alm = ref.random_alm(lmax, lmax, 99)
     want, _ = ref.synthesis(alm, lmax, lmax, g, pairing=True)
