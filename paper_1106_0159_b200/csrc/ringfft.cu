@@ -578,6 +578,15 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 constexpr int kDescChunks = (int)(sizeof(RingDesc) / 16);
+// Synthesis of aliasing rings (n <= mmax) in the classes up to 1024 points stages the ring's
+// whole Delta row in shared memory with cp.async (every load in flight at once) before the wrap
+// loop, which then reads shared memory: the fold was 50-90% of these classes' time as one
+// global-load round trip per wrap (C4, ncu: 256/512/1024-point Bluestein classes -43/-32/-15%;
+// the 2048-point classes lose more to the halved occupancy than they gain).  Orders up to
+// kStageMaxM (the row's shared memory).
+constexpr int kStageMaxM = 8192;
+template <int M>
+constexpr bool p2_stage_row() { return M <= 1024; }
 #ifndef P2_PHASE_LATE
 #define P2_PHASE_LATE 0  // synthesis: wait for the phase factors before the fold (1: after its first loads, measured 0.01 ms slower at C4)
 #endif
@@ -632,6 +641,7 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
     double2* tws = smem + p2pad(M) + 16;        // pass twiddles (P2Plan<M, E>::TW)
     double2* phlo = tws + P2Plan<M, E>::TW;     // 64 + (mmax >> 6) + 1 phase factors
     const int t = threadIdx.x, mmax = a.mmax;
+    double2* drow = phlo + 64 + (mmax >> 6) + 1;  // staged Delta row (p2_stage_row classes)
     const PhaseTab ph{phlo, phlo + 64};
     p2_twsm_build<M, E>(tws, a.p2_tw);
     if (t == 0 && P2_PREFETCH && blockIdx.x < a.n_rings) p2_bulk_prefetch_ring<M, true>(a, a.rings[blockIdx.x]);
@@ -732,6 +742,14 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
             } else {
                 // aliasing rings: wraps outer (two per iteration), G elements' loads together
                 phase_ready();
+                const bool staged = p2_stage_row<M>() && !a.m_base && mmax <= kStageMaxM;
+                if (staged) {
+                    const double2* row = a.delta_in + (int64_t)pos * a.ld;
+                    for (int m = t; m <= mmax; m += T) cp_async16(drow + m, row + m);
+                    cp_async_wait_all();
+                    __syncthreads();
+                }
+                auto fv = [&](int m) { return staged ? rot_value(drow[m], m, rot, ph) : folded_value(a, pos, m, rot, ph); };
 #pragma unroll
                 for (int j0 = 0; j0 < E; j0 += G) {
                     if (T * j0 > N) break;  // Bluestein padding
@@ -750,10 +768,10 @@ __global__ void __launch_bounds__(M / E, MINB) ring_p2_synth_kernel(RingStageArg
                             if (k <= N) {
                                 const int m1 = base + k, m2 = base + (k == 0 ? n : n - k);
                                 double2 x1 = make_double2(0.0, 0.0), x2 = x1, x3 = x1, x4 = x1;
-                                if (m1 <= mmax) x1 = folded_value(a, pos, m1, rot, ph);
-                                if (m2 <= mmax) x2 = folded_value(a, pos, m2, rot, ph);
-                                if (m1 + n <= mmax) x3 = folded_value(a, pos, m1 + n, rot, ph);
-                                if (m2 + n <= mmax) x4 = folded_value(a, pos, m2 + n, rot, ph);
+                                if (m1 <= mmax) x1 = fv(m1);
+                                if (m2 <= mmax) x2 = fv(m2);
+                                if (m1 + n <= mmax) x3 = fv(m1 + n);
+                                if (m2 + n <= mmax) x4 = fv(m2 + n);
                                 if (m1 <= mmax) h[u] = cadd(h[u], x1);
                                 if (m2 <= mmax) h[u] = cadd(h[u], cconj(x2));
                                 if (m1 + n <= mmax) h[u] = cadd(h[u], x3);
@@ -1794,15 +1812,19 @@ int p2_grid(K kernel, int threads, size_t smem, int n_rings) {
     const int g = sms * (per > 0 ? per : 1);
     return n_rings < g ? n_rings : g;
 }
+template <int M, int E>
+size_t p2_synth_smem(int mmax) {
+    return p2_smem<M, E>(mmax) + (p2_stage_row<M>() && mmax <= kStageMaxM ? (size_t)(mmax + 1) * sizeof(double2) : 0);
+}
 template <int M, int E, int MINB, bool BLUE>
 void p2_synth(const RingStageArgs& a, cudaStream_t s) {
     static bool once = (cudaFuncSetAttribute(ring_p2_synth_kernel<M, E, MINB, BLUE>,
                                              cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)p2_smem<M, E>(kMaxPhaseM)),
+                                             (int)std::max(p2_smem<M, E>(kMaxPhaseM), p2_synth_smem<M, E>(kStageMaxM))),
                         true);
     (void)once;
     auto k = ring_p2_synth_kernel<M, E, MINB, BLUE>;
-    const size_t sm = p2_smem<M, E>(a.mmax);
+    const size_t sm = p2_synth_smem<M, E>(a.mmax);
     k<<<p2_grid(k, M / E, sm, a.n_rings), M / E, sm, s>>>(a);
     count_launch();
 }
