@@ -42,11 +42,20 @@ struct LegTables {
 constexpr int LEG_R = LEG_R_DEF;
 constexpr int LEG_TILE = 32 * LEG_R;
 constexpr int LEG_WARPS = 4;      // warps per block of the persistent Legendre kernels
+// Degree steps staged per chunk (LEG_CL / 32 entries per lane; the next chunk's raw entries
+// are held in registers across the current chunk).  Measured at C4 with the round-2 kernels:
+// alm2map 6.88 / 6.83 / 6.83 / 6.90 ms at 128 / 96 / 64 / 32; map2alm 8.30 / 8.25 / 8.25 /
+// 8.13 ms (its 8-stream lanes sit at the 168-register cap: every prefetched entry costs a
+// register, and at 32 nothing spills).
 #ifndef LEG_CL_DEF
-#define LEG_CL_DEF 128  // measured at C4: 32 -> 128 takes alm2map 6.92 -> 6.79 ms, map2alm 8.55 -> 8.48 ms
+#define LEG_CL_DEF 64
 #endif
-constexpr int LEG_CL = LEG_CL_DEF;  // degree steps staged per chunk (LEG_CL / 32 entries per lane)
-static_assert(LEG_CL % 32 == 0, "whole entries per lane");
+#ifndef LEG_M2A_CL_DEF
+#define LEG_M2A_CL_DEF 32
+#endif
+constexpr int LEG_CL = LEG_CL_DEF;          // alm2map
+constexpr int LEG_M2A_CL = LEG_M2A_CL_DEF;  // map2alm
+static_assert(LEG_CL % 32 == 0 && LEG_M2A_CL % 32 == 0, "whole entries per lane");
 #ifndef LEG_A2M_P
 #define LEG_A2M_P 1  // tiles an alm2map warp runs at once; 2 (8 streams per lane) measured slower at C4:
                      // 7.0 ms at 2 CTAs/SM, 7.4 ms at 3 (spills) against 6.89 ms

@@ -614,7 +614,7 @@ constexpr int M2A_S = LEG_R * LEG_M2A_P;
 
 // Per-warp shared memory (dynamic: 4 warps x ~14 KB exceeds the 48 KB static limit)
 struct M2AWarpSmem {
-    double A[LEG_CL];
+    double A[LEG_M2A_CL];
     double red[32][2 * M2A_G + 2];  // lane rows of (degree, re/im) partials, 16-byte aligned
     double2 ck[M2A_S][32];          // activation checkpoints of the current tiles
 };
@@ -670,7 +670,7 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
         ic = min(ic, leg_tile_start(info.x));  // first step of the run (even; 0: seeds)
         ie = max(ie, info.y);
     }
-    const int nchunks = (n + 1 - ic + LEG_CL - 1) / LEG_CL;  // degree offsets ic..n
+    const int nchunks = (n + 1 - ic + LEG_M2A_CL - 1) / LEG_M2A_CL;  // degree offsets ic..n
     if (first)  // degrees below the first pass's start get no other first write
         for (int i = lane; i < ic; i += 32) part_out[i] = make_double2(0.0, 0.0);
     M2ALane<S> L;
@@ -679,11 +679,11 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
     __syncwarp();
     int ev = next_activation<S>(L.act, ic - 1 + (ic == 0));
 
-    constexpr int K = LEG_CL / 32;  // entries per lane per chunk
+    constexpr int K = LEG_M2A_CL / 32;  // entries per lane per chunk
     auto fetch = [&](int c, double (&v)[K]) {
 #pragma unroll
         for (int q = 0; q < K; ++q) {
-            const int i = ic + c * LEG_CL + q * 32 + lane;
+            const int i = ic + c * LEG_M2A_CL + q * 32 + lane;
             v[q] = i <= n ? gA[i] : 0.0;
         }
     };
@@ -697,8 +697,8 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
         for (int q = 0; q < K; ++q) sm.A[q * 32 + lane] = nxt[q];
         __syncwarp();
         if (c + 1 < nchunks) fetch(c + 1, nxt);
-        const int i0 = ic + c * LEG_CL;
-        const int cnt = min(LEG_CL, n - i0 + 1);
+        const int i0 = ic + c * LEG_M2A_CL;
+        const int cnt = min(LEG_M2A_CL, n - i0 + 1);
         for (int g = 0; g < cnt; g += M2A_G) {
             const int gc = min(M2A_G, cnt - g);
             const int ig = i0 + g;  // even degree offset
@@ -779,7 +779,7 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_M2A_MINB)
     leg_map2alm_kernel(LegPlanView p, const double2* __restrict__ delta,
                        const int64_t* __restrict__ row_off, int* __restrict__ queue,
                        double2* __restrict__ scratch) {
-    static_assert(LEG_CL % M2A_G == 0, "chunk must hold whole reduction groups");
+    static_assert(LEG_M2A_CL % M2A_G == 0, "chunk must hold whole reduction groups");
     extern __shared__ __align__(16) unsigned char m2a_smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     M2AWarpSmem& sm = reinterpret_cast<M2AWarpSmem*>(m2a_smem)[warp];
