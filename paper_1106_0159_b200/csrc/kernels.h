@@ -61,7 +61,7 @@ static_assert(LEG_CL % 32 == 0 && LEG_M2A_CL % 32 == 0, "whole entries per lane"
                      // 7.0 ms at 2 CTAs/SM, 7.4 ms at 3 (spills) against 6.89 ms
 #endif
 #ifndef LEG_A2M_MINB
-#define LEG_A2M_MINB 3  // resident CTAs per SM the alm2map kernel is compiled for
+#define LEG_A2M_MINB 4  // resident CTAs per SM the alm2map kernel is compiled for (122 registers)
 #endif
 #ifndef LEG_M2A_P
 #define LEG_M2A_P 2  // tiles a map2alm warp runs at once (LEG_R x LEG_M2A_P streams per lane)
