@@ -496,17 +496,22 @@ __global__ void __launch_bounds__(LEG_WARPS * 32, LEG_A2M_MINB)
 }
 
 // Dead tiles: the reference writes exact zeros for streams that never reach k == 0.
+// Threads over orders, one block row per tile: a thread reads its (order, tile) summary once
+// and, when the tile is dead, writes the zeros of the tile's streams; consecutive threads write
+// consecutive entries of a ring row (coalesced).  The earlier form -- threads over streams,
+// one 16-byte entry per ring row each -- took 0.16 ms at C4 for ~170 MB of zeros.
 __global__ void leg_zero_dead_kernel(LegPlanView p, double2* __restrict__ delta,
-                                     const int64_t* __restrict__ row_off) {
-    const int mi = blockIdx.y;
-    const int s = blockIdx.x * blockDim.x + threadIdx.x;
-    if (s >= p.st.n) return;
-    const int t = s / LEG_TILE;
-    if (p.tile_info[(size_t)mi * p.n_tiles + t].x >= 0) return;
+                                     const int64_t* __restrict__ row_off, int t0) {
+    const int t = t0 + (int)blockIdx.y;
+    const int mi = blockIdx.x * blockDim.x + threadIdx.x;
+    if (mi >= p.n_m || p.tile_info[(size_t)mi * p.n_tiles + t].x >= 0) return;
     const double2 z = make_double2(0.0, 0.0);
-    *leg_out(p, delta, row_off, p.st.north[s], mi) = z;
-    const int south = p.st.south[s];
-    if (south >= 0) *leg_out(p, delta, row_off, south, mi) = z;
+    const int s_end = min(p.st.n, (t + 1) * LEG_TILE);
+    for (int s = t * LEG_TILE; s < s_end; ++s) {
+        *leg_out(p, delta, row_off, p.st.north[s], mi) = z;
+        const int south = p.st.south[s];
+        if (south >= 0) *leg_out(p, delta, row_off, south, mi) = z;
+    }
 }
 
 int leg_persistent_blocks(int device) {
@@ -524,9 +529,11 @@ void launch_leg_alm2map(const LegPlanView& p, const double2* alm, double2* delta
                         const int64_t* row_off, int* counters, cudaStream_t s, int phases) {
     if (p.n_m == 0) return;
     if (phases & LEG_PHASE_ZERO) {
-        dim3 zg((p.st.n + 127) / 128, p.n_m);
-        leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off);
-        count_launch();
+        for (int t0 = 0; t0 < p.n_tiles; t0 += 65535) {
+            dim3 zg((p.n_m + 127) / 128, std::min(65535, p.n_tiles - t0));
+            leg_zero_dead_kernel<<<zg, 128, 0, s>>>(p, delta, row_off, t0);
+            count_launch();
+        }
     }
     if (!(phases & LEG_PHASE_MAIN) || p.n_a2m_items == 0) return;
     int dev = 0;
