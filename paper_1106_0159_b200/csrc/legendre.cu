@@ -830,6 +830,14 @@ __global__ void leg_m2a_finalize_kernel(LegPlanView p, const int* __restrict__ m
     const double2* base = scratch + p.m2a_slot_base[mi] + i;
     double2 v = make_double2(0.0, 0.0);
     int g = 0;
+    // batches of 8 slot loads in flight (the slots are summed in slot order either way)
+    for (; g + 8 <= G; g += 8) {
+        double2 a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) a[u] = __ldcg(base + (int64_t)(g + u) * (n + 1));
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v = cadd(v, a[u]);
+    }
     for (; g + 4 <= G; g += 4) {
         const double2 a0 = __ldcg(base + (int64_t)g * (n + 1));
         const double2 a1 = __ldcg(base + (int64_t)(g + 1) * (n + 1));
