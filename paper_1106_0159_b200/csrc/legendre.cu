@@ -715,7 +715,7 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
             rmw_ptr += 2 * M2A_G;
             // per-step lane contributions go straight to this lane's transpose row
             double2* const row = reinterpret_cast<double2*>(&sm.red[lane][0]);
-            if (ig > ie && gc == M2A_G) {
+            if ((ig > ie || (ev >= ig + M2A_G && ig > 0)) && gc == M2A_G) {
                 // after the last activation: straight-line steps, coefficients in pairs; the
                 // next pair's coefficients are loaded before this pair's partials are stored
                 // (the compiler cannot move the load across the stores)
