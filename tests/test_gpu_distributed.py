@@ -27,7 +27,10 @@ def alltoall(sends, send_counts, recv_counts, W):
 @pytest.mark.parametrize("nside,lmax,W,rings", [(8, 16, 1, "blocks"), (8, 16, 2, "blocks"), (16, 40, 3, "blocks"),
                                                  (64, 128, 4, "blocks"), (128, 256, 8, "blocks"),
                                                  (256, 512, 1, "blocks"), (64, 128, 4, "balanced"),
-                                                 (128, 256, 8, "balanced"), (16, 40, 3, "interleaved")])
+                                                 (128, 256, 8, "balanced"), (16, 40, 3, "interleaved"),
+                                                 # polar caps of 4100..4396 samples: the split 8192-point
+                                                 # Bluestein class through the exchange layouts
+                                                 (1100, 64, 4, "balanced")])
 @pytest.mark.parametrize("order_major", [True, False])
 def test_stage_path_matches_single_worker(nside, lmax, W, rings, order_major):
     dev = torch.device("cuda", 0)

@@ -26,7 +26,8 @@ def as_sht(g):
 
 @pytest.mark.parametrize("nside,lmax,W,rings", [(16, 40, 1, "blocks"), (16, 40, 2, "blocks"), (32, 64, 3, "blocks"),
                                                  (64, 128, 4, "balanced"), (128, 256, 8, "blocks"),
-                                                 (128, 256, 8, "balanced")])
+                                                 (128, 256, 8, "balanced"),
+                                                 (1100, 64, 2, "balanced")])  # split 8192-point Bluestein class
 def test_group_matches_reference_and_one_context(nside, lmax, W, rings):
     g = ref.healpix_grid(nside)
     sg = as_sht(g)
