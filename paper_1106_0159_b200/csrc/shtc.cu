@@ -168,10 +168,13 @@ struct LegPlan {
 // copies) and order chunks (a_lm copies)
 constexpr int kMaxPipeBands = 16;
 // SHTC_PIPE_BANDS overrides the band count (experiments)
+// 6 bands: with the round-2 kernels the C4 pair from pinned memory measured 22.59 ms against
+// 22.80 ms for 8 (map2alm 11.88 vs 12.20; alm2map 10.71 vs 10.60), 10 and 12 slower
+// (tools/pipe_bands.sh, tools/pipe_bands_w.sh)
 int pipe_bands() {
     static const int b = std::getenv("SHTC_PIPE_BANDS")
                              ? std::min(kMaxPipeBands, std::max(1, std::atoi(std::getenv("SHTC_PIPE_BANDS"))))
-                             : 8;
+                             : 6;
     return b;
 }
 #define kPipeBands pipe_bands()
@@ -358,11 +361,11 @@ std::vector<int> tile_bands(const shtc_ctx* c, const std::vector<Stream>& st) {
     }
     // band k covers the pixel fraction [cum[k], cum[k+1]) counted from the equator; the
     // equatorial band 0 has half the weight of the others (it is map2alm's first H2D, so it
-    // sets the head latency) -- SHTC_BAND0_WEIGHT overrides.  Band 2 is alm2map's last band
-    // (its pixels are the final copy), so it is kept small and bands 3-4 take its pixels:
+    // sets the head latency) -- SHTC_BAND0_WEIGHT overrides.  With 8 bands, band 2 (alm2map's
+    // last band, whose pixels are the final copy) is kept small and bands 3-4 take its pixels:
     // weights 0.5,1,0.3,1.1,1.1,1,1,1 measured 23.23 -> 22.93 ms for the C4 pair from pinned
-    // memory (alm2map 11.06 -> 10.65, map2alm 12.18 -> 12.26; tools/band_weights.sh).
-    // SHTC_BAND_WEIGHTS="w0,w1,..." sets every band's weight.
+    // memory (tools/band_weights.sh); with 6 bands a small band 2 measured slower (23.05-23.17
+    // against 22.58 ms for 0.5,1,1,1,1,1).  SHTC_BAND_WEIGHTS="w0,w1,..." sets every weight.
     static const double w0 = std::getenv("SHTC_BAND0_WEIGHT") ? std::atof(std::getenv("SHTC_BAND0_WEIGHT")) : 0.5;
     static const std::vector<double> wl = [] {
         std::vector<double> v;
