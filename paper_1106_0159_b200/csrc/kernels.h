@@ -179,6 +179,9 @@ struct RingDesc {
     int ring_pos;       // row position of the ring in the Delta panel addressing
     int npass;
     unsigned long long radices;  // radix of pass p in bits [4p, 4p+4)
+    int K;              // odd rings of the 2-CTA cluster class: one-sided spectrum length
+                        // min(n, mmax + 1) (pruned Bluestein: n + K - 1 <= 16384)
+    int pad_[3];        // 16-byte multiple (descriptors are staged with 16-byte async copies)
 };
 
 struct RingStageArgs {

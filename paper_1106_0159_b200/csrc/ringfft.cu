@@ -1324,7 +1324,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
             const double phi0 = d.phi0;
             const bool rot = phi0 != 0.0;
             const double2* __restrict__ chirp = a.tabs + d.chirp_off;
-            if (SYN) {
+            const bool odd = !(d.flags & 1);
+            if (SYN && odd) {
+                // odd ring, one-sided: y_j = Re sum_{k<K} C_k e^{2 pi i jk/n} with C_k the sum of
+                // c_m = (m ? 2 : 1) Delta_m e^{i m phi0} over m = k (mod n) (fourier.cpp:10-28)
+                if (rot) {
+                    load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
+                    __syncthreads();
+                }
+                const int K = d.K;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    double2 z = make_double2(0.0, 0.0);
+                    if (k < K) {
+                        for (int m = k; m <= mmax; m += n) {
+                            const double2 c = rot_value(a.delta_in[delta_index(a, pos, m)], m, rot, ph);
+                            z = cadd(z, m ? cscale(c, 2.0) : c);
+                        }
+                        z = cmul(z, cconj(__ldg(&chirp[k])));
+                    }
+                    v[j] = z;
+                }
+            } else if (SYN) {
                 if (rot) {
                     load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
                     __syncthreads();
@@ -1366,6 +1388,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                     v[j] = (k < N) ? z : make_double2(0.0, 0.0);
                 }
                 __syncthreads();  // H read before the first pass overwrites buf
+            } else if (odd) {
+                // odd ring: x_j c_j for j < n (n may exceed MH: the DIF split reads both halves)
+                if (h == 0 && rot) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
+                const double* __restrict__ in = a.map_in + d.pix_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int b = t + T * j;
+                    double2 lo = make_double2(0.0, 0.0), hi = lo;
+                    if (b < n) lo = cscale(__ldg(&chirp[b]), in[b]);
+                    if (b + MH < n) hi = cscale(__ldg(&chirp[b + MH]), in[b + MH]);
+                    v[j] = h == 0 ? cadd(lo, hi) : csub(lo, hi);
+                }
             } else {
                 if (h == 0 && rot) load_phase(phlo, a.tabs + d.ph_off, 64 + (mmax >> 6) + 1, T);
                 const int64_t po = d.pix_off;
@@ -1408,8 +1442,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
         cluster.sync();
         if (h == 0) {
             const double2* rb = cluster.map_shared_rank(buf, 1);
+            const RingDesc& d = desc_at(a, ri);
+            const bool odd_syn = SYN && !(d.flags & 1);
+            const int n = d.n;
+            const double2* __restrict__ chirp = a.tabs + d.chirp_off;
+            double* __restrict__ out = odd_syn ? a.map_out + d.pix_off : nullptr;
 #pragma unroll
-            for (int j = 0; j < E; ++j) v[j] = cadd(v[j], rb[p2pad(t + T * j)]);
+            for (int j = 0; j < E; ++j) {
+                const int b = t + T * j;
+                const double2 w = rb[p2pad(b)];
+                // odd synthesis: samples b + MH = u_b - W^-b v_b (n may exceed MH)
+                if (odd_syn && b + MH < n)
+                    out[b + MH] = cmul(csub(v[j], w), cconj(__ldg(&chirp[b + MH]))).x * (1.0 / (double)FFT_P2C_B);
+                v[j] = cadd(v[j], w);
+            }
         }
         cluster.sync();  // CTA 1's buffer is reused by the next ring
         if (h == 0) {
@@ -1423,7 +1469,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(512, 1) ring_p2c_ker
                 const double2 c = __ldg(&chirp[k < N ? k : 0]);
                 v[j] = cscale(cmul(v[j], SYN ? cconj(c) : c), inv);
             }
-            if (SYN) {
+            const bool odd = !(d.flags & 1);
+            if (SYN && odd) {
+                double* __restrict__ out = a.map_out + d.pix_off;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < N) out[k] = v[j].x;  // N = n: samples below MH
+                }
+            } else if (!SYN && odd) {
+                const int n = d.n, pos = d.ring_pos, K = d.K;
+#pragma unroll
+                for (int j = 0; j < E; ++j) {
+                    const int k = t + T * j;
+                    if (k < K) buf[p2pad(k)] = v[j];
+                }
+                __syncthreads();
+                const double wgt = d.weight;
+                const bool rot = d.phi0 != 0.0;
+                for (int idx = t; idx <= mmax; idx += T) {
+                    const int m = a.m_order ? __ldg(a.m_order + idx) : idx;
+                    double2 val = cscale(buf[p2pad(m % n)], wgt);  // fourier.cpp:50-55
+                    if (rot && m > 0) val = cmul(val, cconj(ph.at(m)));
+                    *delta_out_at(a, pos, m) = val;
+                }
+            } else if (SYN) {
                 const int64_t po = d.pix_off;
                 double* __restrict__ out = a.map_out + po;
 #pragma unroll
@@ -1480,9 +1550,13 @@ __global__ void __launch_bounds__(512, 1) p2c_h_kernel(const RingDesc* __restric
     const int h = blockIdx.x & 1, N = d.N, t = threadIdx.x;
     const double2* chirp = tabs + d.chirp_off;
     const double2* twm = tabs + d.tw_off;
+    // half-mode rings: h_d for |d| < N.  Odd rings (pruned, analysis orientation): lags
+    // m - j with m < K and j < n, i.e. d in (-n, K); synthesis uses conj(FFT(h)), the mirror.
+    const bool odd = !(d.flags & 1);
+    const int pos_lim = odd ? d.K : N, neg_lim = odd ? d.n : N;
     auto hval = [&](int i) {
-        if (i < N) return cconj(chirp[i]);
-        if (i > M - N) return cconj(chirp[M - i]);
+        if (i < pos_lim) return cconj(chirp[i]);
+        if (i > M - neg_lim) return cconj(chirp[M - i]);
         return make_double2(0.0, 0.0);
     };
     double2* tws = smem + p2pad(MH) + 16;

@@ -929,7 +929,7 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         return off;
     };
     F.mmax = c->mmax;
-    std::map<int, int64_t> h_at;  // Bluestein N -> H offset
+    std::map<int64_t, int64_t> h_at;  // Bluestein (N, half) -> H offset
     std::vector<RingDesc> per_class[FFT_N_CLASSES];
     std::vector<RingDesc> blue_class[FFT_N_CLASSES];
     std::vector<RingDesc> blue_clus;
@@ -954,10 +954,23 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         // resident power-of-two engine; the rest (odd rings, other 7-smooth lengths, tiny
         // buffers) the generic in-place mixed-radix kernels.  Bluestein's FFT(conj chirp) is
         // built by the generic class of the same length at plan time.
+        // odd rings whose Bluestein buffer exceeds the generic classes (n > 4096): one-sided
+        // (pruned) Bluestein on the 2-CTA cluster class -- K = min(n, mmax + 1) spectrum bins
+        // in, n samples out (or back), so n + K - 1 <= 16384 points suffice (the Gauss-Legendre
+        // n_phi = 2 lmax + 1 = 8193 at lmax 4096 needs 12289)
+        bool odd_clus = false;
+        if (!half && !smooth && fft_class_for(d.B) < 0) {
+            const int K = std::min(d.n, c->mmax + 1);
+            if ((int64_t)d.n + K - 1 <= FFT_P2C_B) {
+                d.B = FFT_P2C_B;
+                d.K = K;
+                odd_clus = true;
+            }
+        }
         const int gcls = fft_class_for(d.B);
         // 16384-point Bluestein buffers (N < 8192): 2-CTA clusters.  A direct 16384-point ring
         // (n_phi = 32768, N a power of two) is not one of them: it has no class and fails below
-        const bool clus = half && !smooth && d.B == FFT_P2C_B;
+        const bool clus = (half && !smooth && d.B == FFT_P2C_B) || odd_clus;
         int cls = clus ? FFT_P2C_CLASS : (half ? fft_p2_class_for(d.B, !smooth) : -1);
         if (cls < 0) cls = gcls;
         if (cls < 0)
@@ -974,11 +987,12 @@ void build_fft_plan(shtc_ctx* c, FftPlan& F, const std::vector<int>& rings,
         d.hw_off = half ? table(1, d.n) : 0;
         if (!smooth) {
             d.chirp_off = table(2, d.N);
-            auto it = h_at.find(d.N);
+            const int64_t hkey = 2 * (int64_t)d.N + (half ? 1 : 0);  // odd cluster rings: pruned h
+            auto it = h_at.find(hkey);
             if (it == h_at.end()) {
                 d.h_off = tot;
                 tot += d.B;
-                h_at[d.N] = d.h_off;
+                h_at[hkey] = d.h_off;
                 if (clus) blue_clus.push_back(d);
                 else blue_class[gcls].push_back(d);
             } else {
