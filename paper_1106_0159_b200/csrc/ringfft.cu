@@ -529,7 +529,7 @@ __device__ __forceinline__ void p2_prefetch_ring(const RingStageArgs& a, int ri)
     } else {
         l2_prefetch<T>(a.map_in + d.pix_off, (int64_t)d.n * 8);
     }
-    l2_prefetch<T>(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);
+    if (d.flags & 1) l2_prefetch<T>(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);  // half mode only
     if (d.phi0 != 0.0) l2_prefetch<T>(a.tabs + d.ph_off, (int64_t)(64 + (a.mmax >> 6) + 1) * 16);
     if (d.flags & 2) {
         l2_prefetch<T>(a.tabs + d.chirp_off, (int64_t)d.N * 16);
@@ -553,7 +553,7 @@ __device__ __forceinline__ void p2_bulk_prefetch_ring(const RingStageArgs& a, co
     } else {
         bulk_prefetch_l2(a.map_in + d.pix_off, (int64_t)d.n * 8);
     }
-    bulk_prefetch_l2(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);
+    if (d.flags & 1) bulk_prefetch_l2(a.tabs + d.hw_off, (int64_t)(d.N + 1) * 16);  // half mode only
     if (d.phi0 != 0.0) bulk_prefetch_l2(a.tabs + d.ph_off, (int64_t)(64 + (a.mmax >> 6) + 1) * 16);
     if (d.flags & 2) {
         bulk_prefetch_l2(a.tabs + d.chirp_off, (int64_t)d.N * 16);
