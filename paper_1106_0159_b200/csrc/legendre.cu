@@ -751,9 +751,13 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
                     a = an;
                 }
             } else {
-                // activation window (warp-uniform event test per step), seed, partial group
+                // activation window (warp-uniform event test per step), seed, partial group;
+                // each step pair's coefficients are loaded one pair ahead (as in the FAST path)
+                double2 anx = *reinterpret_cast<const double2*>(&sm.A[g]);
                 for (int u = 0; u < M2A_G; u += 2) {
                     const int i = ig + u;
+                    const double2 ap = anx;
+                    if (u + 2 < M2A_G) anx = *reinterpret_cast<const double2*>(&sm.A[g + u + 2]);
                     double2 v1 = make_double2(0.0, 0.0), v2 = make_double2(0.0, 0.0);
                     if (u < gc) {
                         if (i == 0) {
@@ -764,17 +768,17 @@ __device__ __forceinline__ void m2a_pass(const LegPlanView& p, const double2* __
                                 v1.y = __fma_rn(L.ds[r].y, L.q1[r], v1.y);
                             }
                         } else if (i == ev) {
-                            v1 = m2a_step_act<S, false>(L, sm.A[g + u], i, sm.ck, lane);
+                            v1 = m2a_step_act<S, false>(L, ap.x, i, sm.ck, lane);
                             ev = next_activation<S>(L.act, i);
                         } else {
-                            v1 = m2a_step<S, false>(L, sm.A[g + u]);
+                            v1 = m2a_step<S, false>(L, ap.x);
                         }
                         if (u + 1 < gc) {
                             if (i + 1 == ev) {
-                                v2 = m2a_step_act<S, true>(L, sm.A[g + u + 1], i + 1, sm.ck, lane);
+                                v2 = m2a_step_act<S, true>(L, ap.y, i + 1, sm.ck, lane);
                                 ev = next_activation<S>(L.act, i + 1);
                             } else {
-                                v2 = m2a_step<S, true>(L, sm.A[g + u + 1]);
+                                v2 = m2a_step<S, true>(L, ap.y);
                             }
                         }
                     }
